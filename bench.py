@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark: D-Iteration solves on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one cold solve to |F|_1 <= tol (every sweep of the hot path: frontier
+select, diffusion push/pull, residual reduction) on the synthetic graph of
+BASELINE.json configs[C] (default 2: n = 50M, ~1B weighted edges, tol 1e-9),
+already resident in HBM.  value = diffused edges / s; time_to_tol_s = seconds
+per solve.  e2e = the same metric through the C ABI from pinned HOST buffers
+(graph upload + build + solve + H download inside the timed region).
+`--impl reference` times the CPU oracle (oracle/, the reference arm of this
+tier) on the same workload, a bounded number of sweeps per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "diffused edges/s & time to |F|_1<=tol, fraction of HBM roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--variant", default="auto", choices=["auto", "push", "pull"])
+    p.add_argument("--theta", type=float, default=1.0)
+    p.add_argument("--tol", type=float, default=None)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--scale-n", type=int, default=None, help="override n (debug only)")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def spec_for(args):
+    spec = synth.CONFIGS[args.config]
+    if args.scale_n:
+        spec = spec.scaled(args.scale_n)
+    return spec
+
+
+def workload_name(spec, cfg):
+    return f"{spec.name} (BASELINE configs[{cfg}])"
+
+
+# ------------------------------------------------------------------ CPU oracle
+def oracle_sweeps(spec, g, sweeps):
+    """The CPU oracle (oracle/, test infrastructure) timed as it stands: `sweeps`
+    frontier sweeps from the cold start F_0 = (1-d)Z, single-threaded C."""
+    from oracle import di as odi
+    from oracle import graph as ograph
+    cp, ri, pv = ograph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    st_F = np.full(g.n, (1 - spec.d) / g.n)
+    st_H = np.zeros(g.n)
+    t0 = time.perf_counter()
+    r = odi.sweep_run(g.n, cp, ri, pv, spec.d, st_F, st_H, theta=1.0, tol=0.0, max_sweeps=sweeps)
+    dt = time.perf_counter() - t0
+    return r.edges, dt, (cp, ri, pv)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    spec = spec_for(args)
+    g = synth.generate(spec)
+    from oracle import di as odi
+    from oracle import graph as ograph
+    cp, ri, pv = ograph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    sweeps = 1 if g.m > 50_000_000 else 5
+    times, edges = [], []
+    for it in range(args.warmup + args.steps):
+        F = np.full(g.n, (1 - spec.d) / g.n)
+        H = np.zeros(g.n)
+        t0 = time.perf_counter()
+        r = odi.sweep_run(g.n, cp, ri, pv, spec.d, F, H, theta=1.0, tol=0.0, max_sweeps=sweeps)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            edges.append(r.edges)
+    tot = sum(times)
+    value = sum(edges) / tot
+    sample = (f"first {sweeps} frontier sweep(s) from the cold start per step, full graph "
+              f"n={g.n} m={g.m}; single-threaded C oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_name(spec, args.config), "n": g.n, "m": g.m},
+            "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def pinned_alloc(shape, dtype):
+    import torch
+    tdt = {np.int32: torch.int32, np.float32: torch.float32, np.int64: torch.int64,
+           np.float64: torch.float64}[dtype]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
+def load_traffic(workload, kernel):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            tr = json.load(fh)
+        return tr.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import paper_1501_06350_b200 as eng
+    from paper_1501_06350_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 or args.gpus > 1:
+        from paper_1501_06350_b200 import dist
+        return dist.bench_sharded(args, METRIC)
+    torch.cuda.set_device(0)
+    spec = spec_for(args)
+    tol = args.tol if args.tol is not None else spec.tol
+    t0 = time.perf_counter()
+    g = synth.generate(spec, pinned_alloc=pinned_alloc)
+    gen_s = time.perf_counter() - t0
+    row_ptr = pinned_alloc((g.n + 1,), np.int64)
+    row_ptr[:] = g.row_ptr
+    stream = torch.cuda.current_stream()
+    G = eng.DIGraph(g.n, row_ptr, g.col, g.w, stream=stream)
+    kw = dict(d=spec.d, tol=tol, theta=args.theta, variant=args.variant)
+    out = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        G.solve(out=out, **kw)
+    torch.cuda.synchronize()
+    _lib.di_profile_enable(G.handle, True)
+    prof_tot = {}
+    edges_tot = 0
+    sweeps = []
+    l0 = eng.di_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        results = []
+        for _ in range(args.steps):
+            _, res = G.solve(out=out, **kw)
+            results.append(res)
+            p = _lib.di_profile_get(G.handle)
+            for k, v in p.items():
+                prof_tot[k] = prof_tot.get(k, 0) + v
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = eng.di_kernel_launches() - l0
+    _lib.di_profile_enable(G.handle, False)
+    total_ms = ev0.elapsed_time(ev1)
+    for r in results:
+        edges_tot += r["diffused_edges"]
+        sweeps.append(r["sweeps"])
+    value = edges_tot / (total_ms / 1e3)
+    res = results[-1]
+    assert res["converged"], res
+    # roofline of the dominant kernel (largest summed device time)
+    peak, peak_kind = load_peaks()
+    kinds = ["select", "push", "pull", "reduce"]
+    dom = max(kinds, key=lambda k: prof_tot.get(f"{k}_ms", 0.0))
+    dom_ms = prof_tot[f"{dom}_ms"]
+    dom_launch = max(1, prof_tot[f"{dom}_launches"])
+    achieved = prof_tot[f"{dom}_bytes"] / (dom_ms / 1e3) / 1e9
+    share = {k: prof_tot.get(f"{k}_ms", 0.0) / max(1e-9, sum(prof_tot.get(f"{q}_ms", 0.0) for q in kinds))
+             for k in kinds}
+    traffic = load_traffic(spec.name, dom)
+    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_kind,
+                "traffic": traffic, "algorithmic_bytes_per_launch": prof_tot[f"{dom}_bytes"] / dom_launch,
+                "avg_launch_ms": dom_ms / dom_launch, "share_of_step": share,
+                "sweep_bytes_per_s_all_kernels": sum(prof_tot.get(f"{k}_bytes", 0) for k in kinds) /
+                (sum(prof_tot.get(f"{k}_ms", 0.0) for k in kinds) / 1e3) / 1e9}
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        Hh = pinned_alloc((g.n,), np.float64)
+        h2d = row_ptr.nbytes + g.col.nbytes + (g.w.nbytes if g.w is not None else 0)
+        e_edges, e_ms = 0, 0.0
+        for _ in range(args.e2e_steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            h = _lib.di_graph_create(g.n, row_ptr, g.col, g.w, device=0, stream=stream)
+            r = _lib.di_solve(h, spec.d, None, tol, Hh, theta=args.theta,
+                              variant=eng.VARIANTS[args.variant])
+            b.record(stream)
+            torch.cuda.synchronize()
+            _lib.di_graph_destroy(h)
+            e_ms += a.elapsed_time(b)
+            e_edges += r.diffused_edges
+        e2e = {"value": e_edges / (e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(Hh.nbytes), "ms_per_step": e_ms / args.e2e_steps}
+    # CPU oracle baseline (bounded sample)
+    cpu = None
+    if not args.no_cpu:
+        sw = 1 if g.m > 50_000_000 else 5
+        ce, cdt, _ = oracle_sweeps(spec, g, sw)
+        cpu = {"value": ce / cdt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {sw} frontier sweep(s) of the cold solve on the full graph "
+                         f"({ce} diffused edges, {cdt:.1f} s, single-threaded C oracle)"}
+    clocks = clk.summary()
+    line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "time_to_tol_s": total_ms / args.steps / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(spec, args.config), "n": g.n, "m": g.m, "d": spec.d, "tol": tol,
+                       "theta": args.theta, "variant": args.variant, "weighted": spec.weighted,
+                       "sweeps_per_solve": sweeps[-1], "diffused_edges_per_solve": results[-1]["diffused_edges"],
+                       "push_sweeps": res["push_sweeps"], "pull_sweeps": res["pull_sweeps"],
+                       "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",
+                       "generate_s": round(gen_s, 2)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks}
+    print(json.dumps(line), flush=True)
+    G.close()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

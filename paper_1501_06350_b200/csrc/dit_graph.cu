@@ -1,0 +1,503 @@
+// dit_graph.cu -- graph builder and dynamic update (B200, sm_100a).
+//
+// Builder (§2.1, Eq. (1)): the CSR by source IS the column structure
+// of P; the only derived per-node array needed by the sweep is
+//     inv(j) = 1 / sum_k w_{j,k}   (1/out(j) unweighted, 0 for a dangling j)
+// so that P_{i,j} = w_{j,i} inv(j) is formed on the fly from the raw weight.
+// Raw float64 weights are stored as float32 when every value converts exactly
+// (then the arithmetic is identical and the edge stream is 4 B smaller).
+//
+// Update (§3.5, Theorem 4): F'_0 = F + d (P' - P) H touches only the changed
+// columns: the old column of each changed source j is withdrawn
+// (F(t) -= d H(j) P_{t,j}), the CSR is rebuilt with the removals dropped and
+// the additions appended, the scales recomputed, and the new column injected
+// (F(t) += d H(j) P'_{t,j}).
+#include "dit_internal.cuh"
+
+#include <vector>
+
+namespace dit {
+
+// ---------------------------------------------------------------- validation
+__global__ void k_check_rows(const int64_t *__restrict__ row_ptr, int64_t n, int64_t m, int *__restrict__ bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = row_ptr[i];
+        if ((i == 0 && v != 0) || (i == n && v != m) || (i < n && row_ptr[i + 1] < v)) atomicOr(bad, 1);
+    }
+}
+
+template <typename Wt>
+__global__ void k_check_edges(const int32_t *__restrict__ col, const Wt *__restrict__ w, int64_t m, int64_t n,
+                              int *__restrict__ bad, int *__restrict__ not_f32) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = col[e];
+        if (c < 0 || (int64_t)c >= n) atomicOr(bad, 2);
+        if (w) {
+            const double x = (double)w[e];
+            if (!(x > 0.0) || !isfinite(x)) atomicOr(bad, 4);
+            if ((double)(float)x != x) atomicOr(not_f32, 1);
+        }
+    }
+}
+
+__global__ void k_f64_to_f32(const double *__restrict__ a, float *__restrict__ b, int64_t m) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        b[e] = (float)a[e];
+}
+
+// ---------------------------------------------------------------- scales (Eq. (1))
+template <typename Wt>
+__global__ void k_scales(const int64_t *__restrict__ row_ptr, const Wt *__restrict__ w, int64_t n,
+                         double *__restrict__ inv, const unsigned char *__restrict__ only) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        if (only && !only[j]) continue;
+        const int64_t b = row_ptr[j], e = row_ptr[j + 1];
+        if (b == e) {
+            inv[j] = 0.0;                     // dangling: null column of P
+            continue;
+        }
+        if (!w) {
+            inv[j] = 1.0 / (double)(e - b);   // P_{i,j} = 1/out(j)
+            continue;
+        }
+        double s = 0.0;                       // sum_k w_{j,k}, in edge order
+        for (int64_t k = b; k < e; ++k) s += (double)w[k];
+        inv[j] = 1.0 / s;
+    }
+}
+
+static void launch_scales(di_graph *h, const unsigned char *only) {
+    DevGraph &g = h->g;
+    if (g.n == 0) return;
+    const int grid = (int)std::min<int64_t>((g.n + 255) / 256, (int64_t)h->num_sms * 16);
+    if (g.w_kind == DI_W_F32)
+        k_scales<float><<<grid, 256, 0, h->stream>>>(g.row_ptr, (const float *)g.w, g.n, g.inv, only);
+    else if (g.w_kind == DI_W_F64)
+        k_scales<double><<<grid, 256, 0, h->stream>>>(g.row_ptr, (const double *)g.w, g.n, g.inv, only);
+    else
+        k_scales<float><<<grid, 256, 0, h->stream>>>(g.row_ptr, nullptr, g.n, g.inv, only);
+    count_launch();
+    DI_CUDA(cudaGetLastError());
+}
+
+void build_scales(di_graph *h) {
+    DevGraph &g = h->g;
+    if (!g.inv) DI_CUDA(cudaMalloc(&g.inv, (g.n > 0 ? g.n : 1) * sizeof(double)));
+    launch_scales(h, nullptr);
+}
+
+static int grid_for(di_graph *h, int64_t count) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)h->num_sms * 16));
+}
+
+static int read_flag(int *dflag, cudaStream_t st) {
+    int v = 0;
+    DI_CUDA(cudaMemcpyAsync(&v, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    return v;
+}
+
+// Copy + validate the caller's CSR into the handle.
+void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                  const void *weights, int w_dtype, int mem) {
+    DevGraph &g = h->g;
+    cudaStream_t st = h->stream;
+    g.n = n;
+    g.m = m;
+    const cudaMemcpyKind kind = mem == DI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    DI_CUDA(cudaMalloc(&g.row_ptr, (n + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMalloc(&g.col, (m > 0 ? m : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMemcpyAsync(g.row_ptr, row_ptr, (n + 1) * sizeof(int64_t), kind, st));
+    if (m > 0) DI_CUDA(cudaMemcpyAsync(g.col, col, m * sizeof(int32_t), kind, st));
+    void *wtmp = nullptr;
+    if (w_dtype != DI_W_NONE && m > 0) {
+        const size_t es = w_dtype == DI_W_F32 ? 4 : 8;
+        DI_CUDA(cudaMalloc(&wtmp, m * es));
+        DI_CUDA(cudaMemcpyAsync(wtmp, weights, m * es, kind, st));
+    }
+    int *flags = nullptr;
+    DI_CUDA(cudaMallocAsync(&flags, 2 * sizeof(int), st));
+    DI_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+    k_check_rows<<<grid_for(h, n + 1), 256, 0, st>>>(g.row_ptr, n, m, flags);
+    count_launch();
+    if (m > 0) {
+        if (w_dtype == DI_W_F32)
+            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, (const float *)wtmp, m, n, flags, flags + 1);
+        else if (w_dtype == DI_W_F64)
+            k_check_edges<double><<<grid_for(h, m), 256, 0, st>>>(g.col, (const double *)wtmp, m, n, flags, flags + 1);
+        else
+            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, nullptr, m, n, flags, flags + 1);
+        count_launch();
+    }
+    DI_CUDA(cudaGetLastError());
+    int fl[2] = {0, 0};
+    DI_CUDA(cudaMemcpyAsync(fl, flags, sizeof(fl), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaFreeAsync(flags, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    if (fl[0]) {
+        cudaFree(wtmp);
+        set_error(fl[0] & 1 ? "row_ptr must be non-decreasing with row_ptr[0]=0 and row_ptr[n]=m"
+                            : (fl[0] & 2 ? "col ids must be in [0, n)" : "weights must be finite and > 0"));
+        throw Fail{DI_ERR_INVALID};
+    }
+    if (w_dtype == DI_W_F32 && m > 0) {
+        g.w = wtmp;
+        g.w_kind = DI_W_F32;
+    } else if (w_dtype == DI_W_F64 && m > 0) {
+        if (fl[1]) {
+            g.w = wtmp;
+            g.w_kind = DI_W_F64;
+        } else {   // every weight is exactly a float: store 4 bytes per edge
+            DI_CUDA(cudaMalloc(&g.w, m * sizeof(float)));
+            k_f64_to_f32<<<grid_for(h, m), 256, 0, st>>>((const double *)wtmp, (float *)g.w, m);
+            count_launch();
+            DI_CUDA(cudaStreamSynchronize(st));
+            cudaFree(wtmp);
+            g.w_kind = DI_W_F32;
+        }
+    }
+    build_scales(h);
+}
+
+static void free_transpose(DevGraph &g) {
+    cudaFree(g.t_ptr);
+    cudaFree(g.t_src);
+    cudaFree(g.t_w);
+    cudaFree(g.pieces);
+    cudaFree(g.fix);
+    cudaFree(g.pbuf);
+    g.t_ptr = nullptr;
+    g.t_src = nullptr;
+    g.t_w = nullptr;
+    g.pieces = nullptr;
+    g.fix = nullptr;
+    g.pbuf = nullptr;
+    g.npieces = g.nfix = 0;
+    g.has_t = false;
+}
+
+void free_graph(DevGraph &g) {
+    free_transpose(g);
+    cudaFree(g.row_ptr);
+    cudaFree(g.col);
+    cudaFree(g.w);
+    cudaFree(g.inv);
+    g = DevGraph();
+}
+
+// ---------------------------------------------------------------- update (Theorem 4)
+__global__ void k_check_ids(const int32_t *__restrict__ a, const int32_t *__restrict__ b, int64_t cnt, int64_t n,
+                            int *__restrict__ bad) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x)
+        if (a[q] < 0 || a[q] >= n || b[q] < 0 || b[q] >= n) atomicOr(bad, 1);
+}
+
+// flags[0] |= invalid weight, flags[1] |= not exactly a float, flags[2] |= not 1
+__global__ void k_check_w(const double *__restrict__ w, int64_t cnt, int *__restrict__ fl) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x) {
+        const double x = w[q];
+        if (!(x > 0.0) || !isfinite(x)) atomicOr(fl, 1);
+        if ((double)(float)x != x) atomicOr(fl + 1, 1);
+        if (x != 1.0) atomicOr(fl + 2, 1);
+    }
+}
+
+// mark every CSR entry matched by a removal; count matches per removal / row
+__global__ void k_mark_removals(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                const int32_t *__restrict__ rs, const int32_t *__restrict__ rd, int64_t nrem,
+                                unsigned char *__restrict__ del, unsigned char *__restrict__ chg,
+                                int *__restrict__ notfound) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nrem; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = rs[q], t = rd[q];
+        int found = 0;
+        for (int64_t e = row_ptr[s]; e < row_ptr[s + 1]; ++e)
+            if (col[e] == t) {
+                del[e] = 1;
+                found = 1;
+            }
+        if (!found) atomicOr(notfound, 1);
+        chg[s] = 1;
+    }
+}
+
+__global__ void k_mark_adds(const int32_t *__restrict__ as, int64_t nadd, unsigned char *__restrict__ chg,
+                            int64_t *__restrict__ addcnt) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nadd; q += (int64_t)gridDim.x * blockDim.x) {
+        chg[as[q]] = 1;
+        atomicAdd((unsigned long long *)&addcnt[as[q]], 1ull);
+    }
+}
+
+// F(t) += sign * d * H(j) * w_{j,t} * inv(j) over the out-edges of changed sources j
+template <typename Wt>
+__global__ void k_column_fluid(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                               const Wt *__restrict__ w, const double *__restrict__ inv,
+                               const unsigned char *__restrict__ chg, const double *__restrict__ H,
+                               double *__restrict__ F, int64_t n, double dsign) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp; j < n; j += nw) {
+        if (!chg[j] || H[j] == 0.0) continue;
+        const double a = dsign * H[j] * inv[j];
+        for (int64_t e = row_ptr[j] + lane_id(); e < row_ptr[j + 1]; e += 32) {
+            const double v = w ? a * (double)w[e] : a;
+            red_add(F + col[e], v);
+        }
+    }
+}
+
+// new out-degree = old - removed + added
+__global__ void k_new_deg(const int64_t *__restrict__ row_ptr, const unsigned char *__restrict__ del,
+                          const unsigned char *__restrict__ chg, const int64_t *__restrict__ addcnt, int64_t n,
+                          int64_t *__restrict__ deg) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp; j < n; j += nw) {
+        const int64_t b = row_ptr[j], e = row_ptr[j + 1];
+        int64_t kept = e - b;
+        if (chg[j]) {
+            int64_t r = 0;
+            for (int64_t k = b + lane_id(); k < e; k += 32) r += del[k];
+            kept -= warp_sum(r);
+            kept += addcnt[j];
+        }
+        if (lane_id() == 0) deg[j] = kept;
+    }
+}
+
+// copy kept entries of every row in order (warp ballot compaction)
+template <typename Wt>
+__global__ void k_copy_kept(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            const Wt *__restrict__ w, const unsigned char *__restrict__ del,
+                            const unsigned char *__restrict__ chg, const int64_t *__restrict__ nrp, int64_t n,
+                            int32_t *__restrict__ ncol, Wt *__restrict__ nw_, int64_t *__restrict__ cursor) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (int64_t j = warp; j < n; j += nwp) {
+        const int64_t b = row_ptr[j], e = row_ptr[j + 1];
+        int64_t out = nrp[j];
+        const bool c = chg[j] != 0;
+        for (int64_t k0 = b; k0 < e; k0 += 32) {
+            const int64_t k = k0 + lane;
+            const bool keep = k < e && !(c && del[k]);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int64_t o = out + __popc(bal & ((1u << lane) - 1u));
+                ncol[o] = col[k];
+                if (w) nw_[o] = w[k];
+            }
+            out += __popc(bal);
+        }
+        if (lane == 0) cursor[j] = out;   // additions of row j go from here
+    }
+}
+
+template <typename Wt>
+__global__ void k_place_adds(const int32_t *__restrict__ as, const int32_t *__restrict__ ad,
+                             const double *__restrict__ aw, int64_t nadd, int64_t *__restrict__ cursor,
+                             int32_t *__restrict__ ncol, Wt *__restrict__ nw_) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nadd; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = (int64_t)atomicAdd((unsigned long long *)&cursor[as[q]], 1ull);
+        ncol[o] = ad[q];
+        if (nw_) nw_[o] = (Wt)(aw ? aw[q] : 1.0);
+    }
+}
+
+template <typename T>
+static T *to_device(const T *p, int64_t cnt, int mem, cudaStream_t st) {
+    if (cnt == 0 || !p) return nullptr;
+    T *d = nullptr;
+    DI_CUDA(cudaMallocAsync(&d, cnt * sizeof(T), st));
+    DI_CUDA(cudaMemcpyAsync(d, p, cnt * sizeof(T), mem == DI_MEM_HOST ? cudaMemcpyHostToDevice
+                                                                      : cudaMemcpyDeviceToDevice, st));
+    return d;
+}
+
+__global__ void k_f32_to_f64(const float *__restrict__ a, double *__restrict__ b, int64_t m) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        b[e] = (double)a[e];
+}
+
+template <typename Wt>
+static void column_fluid(di_graph *h, const unsigned char *chg, double dsign) {
+    DevGraph &g = h->g;
+    k_column_fluid<Wt><<<h->num_sms * 8, 256, 0, h->stream>>>(g.row_ptr, g.col, (const Wt *)g.w, g.inv, chg, h->s.H,
+                                                                h->s.F, g.n, dsign);
+    count_launch();
+}
+
+static void apply_column_fluid(di_graph *h, const unsigned char *chg, double dsign) {
+    if (h->g.w_kind == DI_W_F64) column_fluid<double>(h, chg, dsign);
+    else column_fluid<float>(h, chg, dsign);   // unweighted: g.w == nullptr
+}
+
+void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int32_t *add_dst, const void *add_w,
+                  int w_dtype, int64_t n_rem, const int32_t *rem_src, const int32_t *rem_dst, int mem) {
+    DevGraph &g = h->g;
+    cudaStream_t st = h->stream;
+    const int64_t n = g.n;
+    std::vector<void *> tmp;
+    auto track = [&](void *p) { tmp.push_back(p); return p; };
+    auto release = [&]() {
+        for (void *p : tmp) cudaFreeAsync(p, st);
+        tmp.clear();
+    };
+    try {
+        int32_t *as = (int32_t *)track(to_device(add_src, n_add, mem, st));
+        int32_t *ad = (int32_t *)track(to_device(add_dst, n_add, mem, st));
+        int32_t *rs = (int32_t *)track(to_device(rem_src, n_rem, mem, st));
+        int32_t *rd = (int32_t *)track(to_device(rem_dst, n_rem, mem, st));
+        double *aw = nullptr;
+        if (add_w && n_add > 0) {
+            if (w_dtype == DI_W_F64) {
+                aw = (double *)track(to_device((const double *)add_w, n_add, mem, st));
+            } else {
+                float *f = (float *)track(to_device((const float *)add_w, n_add, mem, st));
+                DI_CUDA(cudaMallocAsync(&aw, n_add * sizeof(double), st));
+                track(aw);
+                k_f32_to_f64<<<grid_for(h, n_add), 256, 0, st>>>(f, aw, n_add);
+                count_launch();
+            }
+        }
+        int *flags = nullptr;   // [0] bad id, [1..3] weight checks, [4] removal not found
+        DI_CUDA(cudaMallocAsync(&flags, 5 * sizeof(int), st));
+        track(flags);
+        DI_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
+        if (n_add) {
+            k_check_ids<<<grid_for(h, n_add), 256, 0, st>>>(as, ad, n_add, n, flags);
+            count_launch();
+        }
+        if (n_rem) {
+            k_check_ids<<<grid_for(h, n_rem), 256, 0, st>>>(rs, rd, n_rem, n, flags);
+            count_launch();
+        }
+        if (aw) {
+            k_check_w<<<grid_for(h, n_add), 256, 0, st>>>(aw, n_add, flags + 1);
+            count_launch();
+        }
+        int fl[5];
+        DI_CUDA(cudaMemcpyAsync(fl, flags, sizeof(fl), cudaMemcpyDeviceToHost, st));
+        DI_CUDA(cudaStreamSynchronize(st));
+        if (fl[0] || fl[1]) {
+            set_error("di_update_edges: node id out of range or weight not finite and > 0");
+            throw Fail{DI_ERR_INVALID};
+        }
+        if (aw && g.w_kind == DI_W_NONE && fl[3]) {   // the graph stays unweighted only for unit weights
+            set_error("di_update_edges: weighted additions on an unweighted graph");
+            throw Fail{DI_ERR_INVALID};
+        }
+        unsigned char *del = nullptr, *chg = nullptr;
+        int64_t *addcnt = nullptr;
+        DI_CUDA(cudaMallocAsync(&del, (g.m > 0 ? g.m : 1), st));
+        track(del);
+        DI_CUDA(cudaMallocAsync(&chg, (n > 0 ? n : 1), st));
+        track(chg);
+        DI_CUDA(cudaMallocAsync(&addcnt, (n > 0 ? n : 1) * sizeof(int64_t), st));
+        track(addcnt);
+        DI_CUDA(cudaMemsetAsync(del, 0, (g.m > 0 ? g.m : 1), st));
+        DI_CUDA(cudaMemsetAsync(chg, 0, (n > 0 ? n : 1), st));
+        DI_CUDA(cudaMemsetAsync(addcnt, 0, (n > 0 ? n : 1) * sizeof(int64_t), st));
+        if (n_rem) {
+            k_mark_removals<<<grid_for(h, n_rem), 256, 0, st>>>(g.row_ptr, g.col, rs, rd, n_rem, del, chg, flags + 4);
+            count_launch();
+        }
+        if (read_flag(flags + 4, st)) {
+            set_error("di_update_edges: a removal names an edge absent from the graph");
+            throw Fail{DI_ERR_EDGE_NOT_FOUND};
+        }
+        if (n_add) {
+            k_mark_adds<<<grid_for(h, n_add), 256, 0, st>>>(as, n_add, chg, addcnt);
+            count_launch();
+        }
+        const bool state = h->s.valid;
+        const double d = h->s.d;
+        // f32 weight storage must stay exact: promote to f64 if an added weight is not a float
+        if (g.w_kind == DI_W_F32 && aw && fl[2]) {
+            double *w64 = nullptr;
+            DI_CUDA(cudaMalloc(&w64, (g.m > 0 ? g.m : 1) * sizeof(double)));
+            if (g.m > 0) {
+                k_f32_to_f64<<<grid_for(h, g.m), 256, 0, st>>>((const float *)g.w, w64, g.m);
+                count_launch();
+            }
+            DI_CUDA(cudaStreamSynchronize(st));
+            cudaFree(g.w);
+            g.w = w64;
+            g.w_kind = DI_W_F64;
+        }
+        // Theorem 4, first half: withdraw d P H over the old changed columns
+        if (state && n > 0) apply_column_fluid(h, chg, -d);
+        // rebuild the CSR
+        int64_t *deg = nullptr, *nrp = nullptr, *cursor = nullptr;
+        DI_CUDA(cudaMallocAsync(&deg, (n > 0 ? n : 1) * sizeof(int64_t), st));
+        track(deg);
+        DI_CUDA(cudaMallocAsync(&cursor, (n > 0 ? n : 1) * sizeof(int64_t), st));
+        track(cursor);
+        DI_CUDA(cudaMalloc(&nrp, (n + 1) * sizeof(int64_t)));
+        if (n > 0) {
+            k_new_deg<<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, del, chg, addcnt, n, deg);
+            count_launch();
+        }
+        exclusive_scan_i64(deg, nrp, n, st);
+        int64_t m2 = 0;
+        DI_CUDA(cudaMemcpyAsync(&m2, nrp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        DI_CUDA(cudaStreamSynchronize(st));
+        int32_t *ncol = nullptr;
+        void *nwt = nullptr;
+        DI_CUDA(cudaMalloc(&ncol, (m2 > 0 ? m2 : 1) * sizeof(int32_t)));
+        const size_t es = g.w_kind == DI_W_F64 ? 8 : (g.w_kind == DI_W_F32 ? 4 : 0);
+        if (es) DI_CUDA(cudaMalloc(&nwt, (m2 > 0 ? m2 : 1) * es));
+        if (n > 0) {
+            if (g.w_kind == DI_W_F64)
+                k_copy_kept<double><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, del, chg,
+                                                                     nrp, n, ncol, (double *)nwt, cursor);
+            else
+                k_copy_kept<float><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const float *)g.w, del, chg, nrp,
+                                                                    n, ncol, (float *)nwt, cursor);
+            count_launch();
+        }
+        if (n_add) {
+            if (g.w_kind == DI_W_F64)
+                k_place_adds<double><<<grid_for(h, n_add), 256, 0, st>>>(as, ad, aw, n_add, cursor, ncol, (double *)nwt);
+            else
+                k_place_adds<float><<<grid_for(h, n_add), 256, 0, st>>>(as, ad, aw, n_add, cursor, ncol, (float *)nwt);
+            count_launch();
+        }
+        DI_CUDA(cudaGetLastError());
+        DI_CUDA(cudaStreamSynchronize(st));
+        // swap in the new CSR, recompute the scales of changed rows
+        free_transpose(g);
+        cudaFree(g.row_ptr);
+        cudaFree(g.col);
+        cudaFree(g.w);
+        g.row_ptr = nrp;
+        g.col = ncol;
+        g.w = nwt;
+        g.m = m2;
+        if (n > 0) launch_scales(h, chg);
+        // Theorem 4, second half: inject d P' H over the new changed columns
+        if (state && n > 0) apply_column_fluid(h, chg, d);
+        DI_CUDA(cudaGetLastError());
+        DI_CUDA(cudaStreamSynchronize(st));
+        // the entry buffer is sized by m
+        if (state) {
+            State &s = h->s;
+            const int64_t need = n + g.m / kSplit + 1;
+            if (need > s.ent_cap) {
+                cudaFree(s.ent);
+                s.ent = nullptr;
+                DI_CUDA(cudaMalloc(&s.ent, need * sizeof(uint4)));
+                s.ent_cap = need;
+            }
+            // l as a function of the state (R5): sum of H over the
+            // dangling nodes of the new graph
+            set_leak_from_history(h);
+        }
+        release();
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
+}  // namespace dit

@@ -1,0 +1,186 @@
+// dit_internal.cuh -- internal types and device helpers of libdit (B200, sm_100a).
+// The C ABI is include/dit.h; DESIGN.md describes the data layout and kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/dit.h"
+
+namespace dit {
+
+constexpr int kThreads = 256;           // block size of every grid-stride kernel
+constexpr int kWarps = kThreads / 32;
+constexpr int64_t kSplit = 512;         // a frontier row is split into entries of <= kSplit edges
+constexpr int kSplitShift = 9;
+constexpr int kLenBits = 24;            // entry: begin (40 bits) | len (24 bits)
+
+// One record per sweep, written by the last block of k_reduce.
+struct SweepRec {
+    unsigned long long entries, edges, nodes_cum;
+    int use_pull, pad;
+};
+constexpr int64_t kHistCap = 1 << 16;
+
+// Device-resident control block: the solver loop runs without host round
+// trips; the host polls `done` once per chunk of sweeps.
+struct Ctrl {
+    double resid;            // |F|_1 of the current F (from the last reduce)
+    double fmax;             // max_i |F(i)|
+    double T;                // frontier threshold of the next select
+    double leak;             // l, fluid consumed at dangling nodes
+    double d, theta, tol;
+    double pull_edges;       // AUTO: pull when frontier edges > pull_edges
+    unsigned long long n_entries;       // frontier entries written this sweep
+    unsigned long long sel_edges;       // out-edges of this sweep's frontier
+    unsigned long long sweeps;          // sweeps done in the current call
+    unsigned long long max_sweeps;
+    unsigned long long diffused_nodes;  // cumulative over the current call
+    unsigned long long diffused_edges;
+    unsigned long long push_sweeps, pull_sweeps;
+    SweepRec *hist;                     // per-sweep records (device), kHistCap entries
+    unsigned int done;
+    unsigned int sel_blocks;            // last-block counters
+    unsigned int red_blocks;
+    int variant;                        // DI_VARIANT_* requested
+    int use_pull;                       // decision for the current sweep
+    int pad;
+};
+
+// Per-node weight-scale storage and raw weights.
+struct DevGraph {
+    int64_t n = 0, m = 0;
+    int64_t *row_ptr = nullptr;    // [n+1]
+    int32_t *col = nullptr;        // [m]
+    void *w = nullptr;             // [m] float or double raw weights, or null
+    int w_kind = DI_W_NONE;        // storage: DI_W_NONE / DI_W_F32 / DI_W_F64
+    double *inv = nullptr;         // [n] 1/sum_k w_{j,k} (0: dangling)
+    // transpose (built lazily for the pull variant)
+    bool has_t = false;
+    int64_t *t_ptr = nullptr;      // [n+1]
+    int32_t *t_src = nullptr;      // [m] source of each in-edge
+    void *t_w = nullptr;           // [m] weight (same storage kind as w)
+    uint4 *pieces = nullptr;       // pull work list: target pieces of <= kPullSplit in-edges
+    int64_t npieces = 0;
+    int4 *fix = nullptr;           // targets cut into several pieces: {j, first piece (lo, hi), count}
+    int64_t nfix = 0;
+    double *pbuf = nullptr;        // [npieces] partial sums of split targets
+};
+
+struct State {
+    bool valid = false;
+    SweepRec *hist = nullptr;            // [kHistCap] device
+    bool profile = false;
+    std::vector<cudaEvent_t> events;     // profiling: 5 per sweep
+    di_profile last_prof{};
+    int64_t last_sweeps = 0;
+    double d = 0.85;
+    double *F = nullptr, *H = nullptr;   // [n]
+    double *A = nullptr;                 // [n] pull: outflow amount per node
+    uint4 *ent = nullptr;                // frontier entries (16 B each)
+    int64_t ent_cap = 0;
+    Ctrl *ctrl = nullptr;                // device
+    Ctrl *ctrl_host = nullptr;           // pinned mirror
+    double *part = nullptr;              // per-block partials (2 per block)
+    int grid = 0;                        // grid of the grid-stride kernels
+};
+
+}  // namespace dit
+
+struct di_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    dit::DevGraph g;
+    dit::State s;
+    int num_sms = 148;
+};
+
+namespace dit {
+
+// ---- error plumbing (thread-local message) ----
+void set_error(const std::string &msg);
+struct Fail {
+    int code;
+};
+void check_cuda(cudaError_t e, const char *what);   // throws Fail{DI_ERR_CUDA / DI_ERR_OOM}
+#define DI_CUDA(x) ::dit::check_cuda((x), #x)
+void count_launch(int k = 1);
+
+// ---- builders / solver (dit_graph.cu, dit_solve.cu) ----
+void build_scales(di_graph *h);
+void build_transpose(di_graph *h);
+void free_graph(DevGraph &g);
+void ensure_state(di_graph *h);
+void free_state(State &s);
+void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res);
+void init_state(di_graph *h, double d, const double *Z_dev);
+void write_H(di_graph *h, double factor, double *H_out, int mem);
+void set_leak_from_history(di_graph *h);
+void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                  const void *weights, int w_dtype, int mem);
+void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int32_t *add_dst,
+                  const void *add_w, int w_dtype, int64_t n_rem, const int32_t *rem_src,
+                  const int32_t *rem_dst, int mem);
+void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStream_t st);
+
+// ---- device helpers ----
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(0xffffffffu, v, o);
+        if ((int)lane_id() >= o) v += u;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Fire-and-forget float64 add at L2 (RED.E.ADD.F64).
+__device__ __forceinline__ void red_add(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Streaming 32-bit load that does not allocate in L1 (index/weight streams).
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+template <typename W>
+__device__ __forceinline__ double load_w(const W *w, int64_t e);
+template <>
+__device__ __forceinline__ double load_w<float>(const float *w, int64_t e) { return (double)ld_stream_f32(w + e); }
+template <>
+__device__ __forceinline__ double load_w<double>(const double *w, int64_t e) { return ld_stream_f64(w + e); }
+
+struct NoW {};
+
+}  // namespace dit

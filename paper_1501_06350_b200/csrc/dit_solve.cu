@@ -1,0 +1,520 @@
+// dit_solve.cu -- the D-Iteration sweep on B200 (sm_100a).
+//
+// One sweep (reading R1; §3.1 Eqs. (8), (10)) =
+//   k_select  frontier S = { i : F(i) != 0, |F(i)| >= T }: H(i) += F(i), F(i) = 0,
+//             emit (edge range, amount d F(i) / sum_k w_{i,k}) entries (push) or
+//             the dense outflow A(i) (pull); warp-ballot/scan compaction with one
+//             atomic per warp; dangling nodes add their fluid to the leak l (§3.3)
+//   k_push    edge-balanced scatter: a warp takes 32 entries, scans their lengths
+//             and walks the union of their edges 32 at a time, RED.ADD.F64 into F
+//   k_pull    (dit_pull.cu) deterministic gather over the transpose
+//   k_reduce  |F|_1 and max|F| (Theorem 1's remaining fluid), deterministic
+//             block partials; the last block sets the next threshold
+//             T = min(theta |F|_1 / n, max|F|) and the `done` flag.
+// Every kernel has a fixed grid and returns at once when ctrl->done is set, so
+// a chunk of sweeps can be enqueued (or graph-launched) without host syncs.
+#include "dit_internal.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace dit {
+
+// ---------------------------------------------------------------- init
+__global__ void __launch_bounds__(kThreads) k_init(double *__restrict__ F, double *__restrict__ H,
+                                                   const double *__restrict__ Z, int64_t n, double d) {
+    const double u = (1.0 - d) / (double)n;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+        F[i] = Z ? (1.0 - d) * Z[i] : u;     // Eq. (7): F_0 = (1-d) Z
+        H[i] = 0.0;                          //          H_0 = 0
+    }
+}
+
+// ---------------------------------------------------------------- select
+// Entry = { (begin << 24) | len , amount } in 16 bytes.
+__device__ __forceinline__ void store_entry(uint4 *p, int64_t begin, int64_t len, double a) {
+    unsigned long long packed = ((unsigned long long)begin << kLenBits) | (unsigned long long)len;
+    unsigned long long ab = (unsigned long long)__double_as_longlong(a);
+    *p = make_uint4((unsigned)packed, (unsigned)(packed >> 32), (unsigned)ab, (unsigned)(ab >> 32));
+}
+
+template <bool kPull>
+__global__ void __launch_bounds__(kThreads) k_select(const int64_t *__restrict__ row_ptr,
+                                                     const double *__restrict__ inv, double *__restrict__ F,
+                                                     double *__restrict__ H, double *__restrict__ A,
+                                                     uint4 *__restrict__ ent, int64_t n, Ctrl *__restrict__ ctrl,
+                                                     double *__restrict__ part_sel) {
+    __shared__ double s_leak[kWarps];
+    __shared__ unsigned long long s_cnt[kWarps][2];
+    if (ctrl->done) return;
+    if (kPull != (ctrl->use_pull != 0)) return;
+    const double T = ctrl->T, d = ctrl->d;
+    const unsigned lane = lane_id();
+    double leak = 0.0;
+    unsigned long long nodes = 0, edges = 0;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); base < n; base += stride) {
+        const int64_t i = base + lane;
+        const bool valid = i < n;
+        const double f = valid ? F[i] : 0.0;
+        const bool sel = valid && f != 0.0 && fabs(f) >= T;
+        int64_t b = 0, deg = 0;
+        double a = 0.0;
+        if (sel) {
+            H[i] += f;                       // Eq. (10)
+            F[i] = 0.0;                      // third term of Eq. (8)
+            b = row_ptr[i];
+            deg = row_ptr[i + 1] - b;
+            nodes += 1;
+            edges += (unsigned long long)deg;
+            if (deg == 0) leak += f;         // dangling: fluid leaves (§3.3 l_k)
+            else a = d * f * inv[i];         // d F(i) / sum_k w_{i,k}
+        }
+        if (kPull) {
+            if (valid) A[i] = a;
+        } else {
+            const unsigned nch = (unsigned)((deg + kSplit - 1) >> kSplitShift);
+            const unsigned incl = warp_incl_scan(nch);
+            const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (tot) {
+                unsigned long long pos = 0;
+                if (lane == 31) pos = atomicAdd(&ctrl->n_entries, (unsigned long long)tot);
+                pos = __shfl_sync(0xffffffffu, pos, 31) + (incl - nch);
+                for (unsigned c = 0; c < nch; ++c) {
+                    const int64_t cb = b + ((int64_t)c << kSplitShift);
+                    const int64_t len = min((int64_t)kSplit, deg - ((int64_t)c << kSplitShift));
+                    store_entry(ent + pos + c, cb, len, a);
+                }
+            }
+        }
+    }
+    // deterministic block reduction of the leak; integer counters by atomics
+    leak = warp_sum(leak);
+    nodes = warp_sum(nodes);
+    edges = warp_sum(edges);
+    const unsigned w = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_leak[w] = leak;
+        s_cnt[w][0] = nodes;
+        s_cnt[w][1] = edges;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double l = 0.0;
+        unsigned long long nn = 0, ee = 0;
+        for (int k = 0; k < kWarps; ++k) {
+            l += s_leak[k];
+            nn += s_cnt[k][0];
+            ee += s_cnt[k][1];
+        }
+        part_sel[blockIdx.x] = l;
+        if (nn) {
+            atomicAdd(&ctrl->diffused_nodes, nn);
+            atomicAdd(&ctrl->sel_edges, ee);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- push
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_push(const int32_t *__restrict__ col, const W *__restrict__ w,
+                                                   double *__restrict__ F, const uint4 *__restrict__ ent,
+                                                   const Ctrl *__restrict__ ctrl) {
+    if (ctrl->done || ctrl->use_pull) return;
+    const unsigned long long N = ctrl->n_entries;
+    const unsigned lane = lane_id();
+    const unsigned long long warp = ((unsigned long long)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * kThreads) >> 5;
+    for (unsigned long long cbase = warp * 32; cbase < N; cbase += nwarps * 32) {
+        const unsigned long long j = cbase + lane;
+        int len = 0;
+        long long beg = 0;
+        double a = 0.0;
+        if (j < N) {
+            const uint4 e = ent[j];
+            const unsigned long long packed = ((unsigned long long)e.y << 32) | e.x;
+            len = (int)(packed & ((1ull << kLenBits) - 1));
+            beg = (long long)(packed >> kLenBits);
+            a = __longlong_as_double((long long)(((unsigned long long)e.w << 32) | e.z));
+        }
+        const int incl = warp_incl_scan(len);
+        const int E = __shfl_sync(0xffffffffu, incl, 31);
+        for (int k0 = 0; k0 < E; k0 += 32) {
+            const int k = k0 + (int)lane;
+            // entry of edge k: number of lanes whose inclusive end is <= k
+            int pos = 0;
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, pos + s - 1);
+                if (v <= k) pos += s;
+            }
+            const int src = min(pos, 31);
+            const int excl = __shfl_sync(0xffffffffu, incl, src) - __shfl_sync(0xffffffffu, len, src);
+            const long long bL = __shfl_sync(0xffffffffu, beg, src);
+            const double aL = __shfl_sync(0xffffffffu, a, src);
+            if (k < E) {
+                const int64_t e = bL + (k - excl);
+                const int32_t t = ld_stream_i32(col + e);
+                double v = aL;
+                if constexpr (!std::is_same<W, NoW>::value) v *= load_w(w, e);   // P_{t,i} = w_{i,t} inv_i
+                red_add(F + t, v);                                                // Eq. (8) push
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- reduce
+__global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ F, int64_t n, int64_t m,
+                                                     Ctrl *__restrict__ ctrl, double *__restrict__ part,
+                                                     const double *__restrict__ part_sel, int is_init) {
+    __shared__ double s_sum[kWarps], s_max[kWarps];
+    __shared__ bool s_last;
+    if (ctrl->done) return;
+    double s = 0.0, mx = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+        const double a = fabs(F[i]);
+        s += a;
+        mx = fmax(mx, a);
+    }
+    s = warp_sum(s);
+    mx = warp_max(mx);
+    const unsigned w = threadIdx.x >> 5;
+    if (lane_id() == 0) {
+        s_sum[w] = s;
+        s_max[w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < kWarps; ++k) {
+            a += s_sum[k];
+            b = fmax(b, s_max[k]);
+        }
+        part[2 * blockIdx.x] = a;
+        part[2 * blockIdx.x + 1] = b;
+        __threadfence();
+        const unsigned v = atomicAdd(&ctrl->red_blocks, 1u);
+        s_last = (v == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    // last block: ordered final sums (deterministic), next-sweep control
+    __threadfence();
+    const volatile double *vp = part;
+    const volatile double *vs = part_sel;
+    double r = 0.0, fm = 0.0, lk = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+        r += vp[2 * b];
+        fm = fmax(fm, vp[2 * b + 1]);
+    }
+    if (!is_init) {
+        for (unsigned b = 0; b < gridDim.x; ++b) lk += vs[b];
+        ctrl->leak += lk;
+        if (ctrl->hist && ctrl->sweeps < (unsigned long long)kHistCap) {
+            SweepRec rec;
+            rec.entries = ctrl->n_entries;
+            rec.edges = ctrl->sel_edges;
+            rec.nodes_cum = ctrl->diffused_nodes;
+            rec.use_pull = ctrl->use_pull;
+            rec.pad = 0;
+            ctrl->hist[ctrl->sweeps] = rec;
+        }
+        ctrl->sweeps += 1;
+        ctrl->diffused_edges += ctrl->sel_edges;
+        if (ctrl->use_pull) ctrl->pull_sweeps += 1; else ctrl->push_sweeps += 1;
+    }
+    ctrl->resid = r;
+    ctrl->fmax = fm;
+    const double T = ctrl->theta * r / (double)n;
+    ctrl->T = T < fm ? T : fm;
+    ctrl->done = (r <= ctrl->tol || ctrl->sweeps >= ctrl->max_sweeps) ? 1u : 0u;
+    // direction choice for the next sweep (AUTO uses this sweep's frontier
+    // edges as the estimate of the next one's; the first sweep from a uniform
+    // F_0 takes every node, see init)
+    const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->sel_edges;
+    if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = 1;
+    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = 0;
+    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? 1 : 0;
+    ctrl->n_entries = 0;
+    ctrl->sel_edges = 0;
+    ctrl->red_blocks = 0;
+}
+
+// ---------------------------------------------------------------- output helpers
+__global__ void k_scale_copy(const double *__restrict__ H, double *__restrict__ out, int64_t n, double f) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = H[i] * f;
+}
+
+// sum of H over dangling nodes (l of §3.3 as a function of the state, R5)
+__global__ void __launch_bounds__(kThreads) k_dangling_hist(const int64_t *__restrict__ row_ptr,
+                                                            const double *__restrict__ H, int64_t n,
+                                                            double *__restrict__ part) {
+    __shared__ double s[kWarps];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+        if (row_ptr[i + 1] == row_ptr[i]) acc += H[i];
+    acc = warp_sum(acc);
+    if (lane_id() == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int k = 0; k < kWarps; ++k) a += s[k];
+        part[blockIdx.x] = a;
+    }
+}
+
+// pull-variant kernels live in dit_pull.cu
+void launch_pull(di_graph *h);
+
+// ---------------------------------------------------------------- host side
+void ensure_state(di_graph *h) {
+    State &s = h->s;
+    const int64_t n = h->g.n;
+    if (s.F) return;
+    const int64_t nn = n > 0 ? n : 1;
+    DI_CUDA(cudaMalloc(&s.F, nn * sizeof(double)));
+    DI_CUDA(cudaMalloc(&s.H, nn * sizeof(double)));
+    s.ent_cap = n + h->g.m / kSplit + 1;
+    DI_CUDA(cudaMalloc(&s.ent, s.ent_cap * sizeof(uint4)));
+    DI_CUDA(cudaMalloc(&s.ctrl, sizeof(Ctrl)));
+    DI_CUDA(cudaMallocHost(&s.ctrl_host, sizeof(Ctrl)));
+    std::memset(s.ctrl_host, 0, sizeof(Ctrl));
+    // fixed grid for every grid-stride kernel: 8 resident 256-thread blocks per SM
+    const int64_t want = (n + kThreads - 1) / kThreads;
+    s.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->num_sms * 8));
+    DI_CUDA(cudaMalloc(&s.part, (size_t)s.grid * 3 * sizeof(double)));
+    DI_CUDA(cudaMalloc(&s.hist, kHistCap * sizeof(SweepRec)));
+    DI_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(Ctrl), h->stream));
+}
+
+void free_state(State &s) {
+    for (cudaEvent_t e : s.events) cudaEventDestroy(e);
+    cudaFree(s.hist);
+    cudaFree(s.F);
+    cudaFree(s.H);
+    cudaFree(s.A);
+    cudaFree(s.ent);
+    cudaFree(s.ctrl);
+    cudaFree(s.part);
+    if (s.ctrl_host) cudaFreeHost(s.ctrl_host);
+    s = State();
+}
+
+void init_state(di_graph *h, double d, const double *Z_dev) {
+    ensure_state(h);
+    State &s = h->s;
+    const int64_t n = h->g.n;
+    if (n > 0) {
+        k_init<<<s.grid, kThreads, 0, h->stream>>>(s.F, s.H, Z_dev, n, d);
+        count_launch();
+        DI_CUDA(cudaGetLastError());
+    }
+    s.d = d;
+    s.valid = true;
+    // leak restarts with the state
+    DI_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(Ctrl), h->stream));
+}
+
+static void launch_select(di_graph *h, bool pull) {
+    State &s = h->s;
+    DevGraph &g = h->g;
+    if (pull)
+        k_select<true><<<s.grid, kThreads, 0, h->stream>>>(g.row_ptr, g.inv, s.F, s.H, s.A, s.ent, g.n, s.ctrl,
+                                                            s.part + 2 * s.grid);
+    else
+        k_select<false><<<s.grid, kThreads, 0, h->stream>>>(g.row_ptr, g.inv, s.F, s.H, s.A, s.ent, g.n, s.ctrl,
+                                                             s.part + 2 * s.grid);
+    count_launch();
+}
+
+static void launch_push(di_graph *h) {
+    State &s = h->s;
+    DevGraph &g = h->g;
+    const int grid = h->num_sms * 8;
+    switch (g.w_kind) {
+    case DI_W_F32:
+        k_push<float><<<grid, kThreads, 0, h->stream>>>(g.col, (const float *)g.w, s.F, s.ent, s.ctrl);
+        break;
+    case DI_W_F64:
+        k_push<double><<<grid, kThreads, 0, h->stream>>>(g.col, (const double *)g.w, s.F, s.ent, s.ctrl);
+        break;
+    default:
+        k_push<NoW><<<grid, kThreads, 0, h->stream>>>(g.col, nullptr, s.F, s.ent, s.ctrl);
+    }
+    count_launch();
+}
+
+static void launch_reduce(di_graph *h, int is_init) {
+    State &s = h->s;
+    k_reduce<<<s.grid, kThreads, 0, h->stream>>>(s.F, h->g.n, h->g.m, s.ctrl, s.part, s.part + 2 * s.grid, is_init);
+    count_launch();
+}
+
+// Algorithmic bytes per launch: every index / weight /
+// entry read once, every fluid read-modify-write counted as 16 B.
+static void collect_profile(di_graph *h, const Ctrl &r) {
+    State &s = h->s;
+    DevGraph &g = h->g;
+    di_profile p{};
+    const int64_t S = std::min<int64_t>((int64_t)r.sweeps, kHistCap);
+    std::vector<SweepRec> hs(S > 0 ? S : 1);
+    if (S > 0) {
+        DI_CUDA(cudaMemcpyAsync(hs.data(), s.hist, S * sizeof(SweepRec), cudaMemcpyDeviceToHost, h->stream));
+        DI_CUDA(cudaStreamSynchronize(h->stream));
+    }
+    const double n = (double)g.n, m = (double)g.m;
+    const double wb = g.w_kind == DI_W_F32 ? 4.0 : (g.w_kind == DI_W_F64 ? 8.0 : 0.0);
+    unsigned long long prev_nodes = 0;
+    for (int64_t k = 0; k < S; ++k) {
+        float t[4];
+        for (int q = 0; q < 4; ++q) DI_CUDA(cudaEventElapsedTime(&t[q], s.events[5 * k + q], s.events[5 * k + q + 1]));
+        const SweepRec &rc = hs[k];
+        const double nodes = (double)(rc.nodes_cum - prev_nodes);
+        prev_nodes = rc.nodes_cum;
+        p.select_ms += t[0];
+        p.select_bytes += 8.0 * n + 48.0 * nodes + (rc.use_pull ? 8.0 * n : 16.0 * (double)rc.entries);
+        p.select_launches += 1;
+        if (rc.use_pull) {
+            p.pull_ms += t[2];
+            p.pull_bytes += 32.0 * (double)g.npieces + m * (12.0 + wb);
+            p.pull_launches += 1;
+        } else {
+            p.push_ms += t[1];
+            p.push_bytes += 16.0 * (double)rc.entries + (double)rc.edges * (20.0 + wb);
+            p.push_launches += 1;
+        }
+        p.reduce_ms += t[3];
+        p.reduce_bytes += 8.0 * n;
+        p.reduce_launches += 1;
+    }
+    p.sweeps = S;
+    s.last_prof = p;
+}
+
+void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res) {
+    State &s = h->s;
+    DevGraph &g = h->g;
+    const bool want_pull = o.variant == DI_VARIANT_PULL || o.variant == DI_VARIANT_AUTO;
+    if (want_pull && g.n > 0) {
+        build_transpose(h);
+        if (!s.A) DI_CUDA(cudaMalloc(&s.A, g.n * sizeof(double)));
+    }
+    // per-call control fields (leak persists with the state)
+    DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+    DI_CUDA(cudaStreamSynchronize(h->stream));
+    Ctrl c = *s.ctrl_host;
+    const double leak = c.leak;
+    std::memset(&c, 0, sizeof(Ctrl));
+    c.leak = leak;
+    c.d = s.d;
+    c.theta = o.theta;
+    c.tol = tol;
+    c.max_sweeps = (unsigned long long)(o.max_sweeps > 0 ? o.max_sweeps : 10000000LL);
+    c.variant = g.has_t ? o.variant : DI_VARIANT_PUSH;
+    c.pull_edges = o.pull_frac * (double)g.m;
+    c.hist = s.hist;
+    *s.ctrl_host = c;
+    DI_CUDA(cudaMemcpyAsync(s.ctrl, s.ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+    int64_t launched = 0;
+    auto mark = [&](int64_t sweep, int k) {
+        if (!s.profile) return;
+        const size_t idx = (size_t)sweep * 5 + k;
+        while (s.events.size() <= idx) {
+            cudaEvent_t e;
+            DI_CUDA(cudaEventCreate(&e));
+            s.events.push_back(e);
+        }
+        DI_CUDA(cudaEventRecord(s.events[idx], h->stream));
+    };
+    if (g.n > 0) {
+        launch_reduce(h, 1);
+        int chunk = 2;
+        for (;;) {
+            for (int k = 0; k < chunk; ++k, ++launched) {
+                const bool rec = launched < kHistCap;
+                if (rec) mark(launched, 0);
+                launch_select(h, false);
+                if (g.has_t) launch_select(h, true);
+                if (rec) mark(launched, 1);
+                launch_push(h);
+                if (rec) mark(launched, 2);
+                if (g.has_t) launch_pull(h);
+                if (rec) mark(launched, 3);
+                launch_reduce(h, 0);
+                if (rec) mark(launched, 4);
+            }
+            DI_CUDA(cudaGetLastError());
+            DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+            DI_CUDA(cudaStreamSynchronize(h->stream));
+            if (s.ctrl_host->done) break;
+            chunk = std::min(chunk * 2, 64);
+        }
+    } else {
+        s.ctrl_host->done = 1;
+    }
+    const Ctrl &r = *s.ctrl_host;
+    s.last_sweeps = (int64_t)r.sweeps;
+    if (s.profile) collect_profile(h, r);
+    if (res) {
+        std::memset(res, 0, sizeof(*res));
+        res->residual_l1 = g.n > 0 ? r.resid : 0.0;
+        res->leak = r.leak;
+        const bool comp = o.dangling == DI_DANGLING_COMPLETE;
+        const double den = comp ? (1.0 - s.d - s.d * r.leak) : (1.0 - s.d);
+        res->bound = res->residual_l1 / den;
+        res->norm_factor = comp ? (1.0 - s.d) / den : 1.0;
+        res->sweeps = (int64_t)r.sweeps;
+        res->diffused_nodes = (int64_t)r.diffused_nodes;
+        res->diffused_edges = (int64_t)r.diffused_edges;
+        res->push_sweeps = (int64_t)r.push_sweeps;
+        res->pull_sweeps = (int64_t)r.pull_sweeps;
+        res->converged = res->residual_l1 <= tol ? 1 : 0;
+    }
+}
+
+void write_H(di_graph *h, double factor, double *H_out, int mem) {
+    const int64_t n = h->g.n;
+    if (!H_out || n == 0) return;
+    State &s = h->s;
+    double *dst = H_out;
+    double *tmp = nullptr;
+    if (mem == DI_MEM_HOST) {
+        if (factor == 1.0) {
+            DI_CUDA(cudaMemcpyAsync(H_out, s.H, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            DI_CUDA(cudaStreamSynchronize(h->stream));
+            return;
+        }
+        DI_CUDA(cudaMallocAsync(&tmp, n * sizeof(double), h->stream));
+        dst = tmp;
+    }
+    k_scale_copy<<<s.grid, kThreads, 0, h->stream>>>(s.H, dst, n, factor);
+    count_launch();
+    DI_CUDA(cudaGetLastError());
+    if (tmp) {
+        DI_CUDA(cudaMemcpyAsync(H_out, tmp, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        DI_CUDA(cudaFreeAsync(tmp, h->stream));
+    }
+    DI_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+// l := sum of H over dangling nodes, summed on the device in a fixed order
+__global__ void k_leak_final(const double *__restrict__ part, int nb, Ctrl *__restrict__ ctrl) {
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int b = 0; b < nb; ++b) a += part[b];
+        ctrl->leak = a;
+    }
+}
+
+void set_leak_from_history(di_graph *h) {
+    State &s = h->s;
+    const int64_t n = h->g.n;
+    if (n == 0) return;
+    k_dangling_hist<<<s.grid, kThreads, 0, h->stream>>>(h->g.row_ptr, s.H, n, s.part);
+    k_leak_final<<<1, 32, 0, h->stream>>>(s.part, s.grid, s.ctrl);
+    count_launch(2);
+    DI_CUDA(cudaGetLastError());
+}
+
+}  // namespace dit
