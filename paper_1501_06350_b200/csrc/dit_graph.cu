@@ -104,6 +104,8 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     cudaStream_t st = h->stream;
     g.n = n;
     g.m = m;
+    g.nt = n;
+    g.n_global = n;
     const cudaMemcpyKind kind = mem == DI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     DI_CUDA(cudaMalloc(&g.row_ptr, (n + 1) * sizeof(int64_t)));
     DI_CUDA(cudaMalloc(&g.col, (m > 0 ? m : 1) * sizeof(int32_t)));
@@ -166,6 +168,9 @@ static void free_transpose(DevGraph &g) {
     cudaFree(g.pieces);
     cudaFree(g.fix);
     cudaFree(g.pbuf);
+    cudaFree(g.tile_start);
+    g.tile_start = nullptr;
+    g.ntiles = 0;
     g.t_ptr = nullptr;
     g.t_src = nullptr;
     g.t_w = nullptr;
@@ -178,6 +183,8 @@ static void free_transpose(DevGraph &g) {
 
 void free_graph(DevGraph &g) {
     free_transpose(g);
+    cudaFree(g.ghost_ids);
+    cudaFree(g.recv_idx);
     cudaFree(g.row_ptr);
     cudaFree(g.col);
     cudaFree(g.w);

@@ -41,6 +41,10 @@ struct Ctrl {
     unsigned long long diffused_edges;
     unsigned long long push_sweeps, pull_sweeps;
     SweepRec *hist;                     // per-sweep records (device), kHistCap entries
+    double n_global;                    // n of the whole graph (threshold denominator)
+    double *stats_out;                  // shard mode: local {r, fmax, leak, sel_edges} go here
+    unsigned long long last_sel_edges;  // frontier out-edges of the last sweep
+    int stats_is_init;
     unsigned int done;
     unsigned int sel_blocks;            // last-block counters
     unsigned int red_blocks;
@@ -51,7 +55,14 @@ struct Ctrl {
 
 // Per-node weight-scale storage and raw weights.
 struct DevGraph {
-    int64_t n = 0, m = 0;
+    int64_t n = 0, m = 0;          // rows (owned nodes) and edges
+    int64_t nt = 0;                // fluid slots = n, + ghost slots for a shard
+    int64_t n_global = 0;          // nodes of the whole graph (= n unless shard)
+    int64_t lo = 0;                // shard: first owned global id
+    bool shard = false;
+    int32_t *ghost_ids = nullptr;  // shard: global id of each ghost slot (ascending)
+    int32_t *recv_idx = nullptr;   // shard: local target of each received value
+    std::vector<int64_t> recv_seg; // shard: received values per source rank
     int64_t *row_ptr = nullptr;    // [n+1]
     int32_t *col = nullptr;        // [m]
     void *w = nullptr;             // [m] float or double raw weights, or null
@@ -67,6 +78,8 @@ struct DevGraph {
     int4 *fix = nullptr;           // targets cut into several pieces: {j, first piece (lo, hi), count}
     int64_t nfix = 0;
     double *pbuf = nullptr;        // [npieces] partial sums of split targets
+    int64_t *tile_start = nullptr; // [ntiles+1] first piece of each pull tile
+    int64_t ntiles = 0;
 };
 
 struct State {
@@ -75,6 +88,7 @@ struct State {
     bool profile = false;
     std::vector<cudaEvent_t> events;     // profiling: 5 per sweep
     di_profile last_prof{};
+    int64_t launched = 0;                // sweeps enqueued in the current call
     int64_t last_sweeps = 0;
     double d = 0.85;
     double *F = nullptr, *H = nullptr;   // [n]
@@ -116,6 +130,15 @@ void free_graph(DevGraph &g);
 void ensure_state(di_graph *h);
 void free_state(State &s);
 void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res);
+void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats_out);
+void launch_sweep(di_graph *h);
+void launch_sweep_reduce(di_graph *h);
+void launch_reduce(di_graph *h, int is_init);
+void launch_select(di_graph *h, bool pull);
+void launch_push(di_graph *h);
+void launch_pull(di_graph *h);
+bool poll_done(di_graph *h);
+void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res);
 void init_state(di_graph *h, double d, const double *Z_dev);
 void write_H(di_graph *h, double factor, double *H_out, int mem);
 void set_leak_from_history(di_graph *h);

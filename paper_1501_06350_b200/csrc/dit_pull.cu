@@ -19,7 +19,8 @@ constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortItems = 16;                       // items per lane
 constexpr int kWarpItems = 32 * kSortItems;          // 512 items per warp
 constexpr int kSortTile = kWarps * kWarpItems;       // 4096 items per block
-constexpr int64_t kPullSplit = 256;
+constexpr int64_t kPullSplit = 64;     // max in-edges per piece (one thread sums a piece)
+constexpr int64_t kPullTile = 2048;    // edges staged in shared memory per pull tile
 
 // ---------------------------------------------------------------- radix sort
 __global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t *__restrict__ keys, int64_t count,
@@ -128,23 +129,41 @@ __global__ void k_gather_t(const V *__restrict__ sv, int64_t m, const int32_t *_
     }
 }
 
-__global__ void k_piece_count(const int64_t *__restrict__ t_ptr, int64_t n, int64_t *__restrict__ pc) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-        pc[j] = (t_ptr[j + 1] - t_ptr[j] + kPullSplit - 1) / kPullSplit;
+// Pieces: the in-edge range of each target cut at every kPullTile boundary of
+// the edge index and after kPullSplit edges, so that every pull tile (edges
+// [t kPullTile, (t+1) kPullTile)) is a whole number of pieces.
+__device__ __forceinline__ int64_t piece_end(int64_t b, int64_t e) {
+    const int64_t tile_end = (b / kPullTile + 1) * kPullTile;
+    return min(e, min(b + kPullSplit, tile_end));
 }
 
-// piece = { begin<<24 | len, target, first-piece-of-split-target index or -1 }
-__global__ void k_piece_write(const int64_t *__restrict__ t_ptr, int64_t n, const int64_t *__restrict__ po,
-                              uint4 *__restrict__ pieces, int4 *__restrict__ fix, unsigned long long *__restrict__ nfix) {
+__global__ void k_piece_count(const int64_t *__restrict__ t_ptr, int64_t n, int64_t *__restrict__ pc) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = t_ptr[j], deg = t_ptr[j + 1] - b;
+        int64_t b = t_ptr[j], c = 0;
+        const int64_t e = t_ptr[j + 1];
+        while (b < e) {
+            b = piece_end(b, e);
+            ++c;
+        }
+        pc[j] = c;
+    }
+}
+
+// piece = { begin<<24 | len, target, split flag }; tile_start[t] = first piece of tile t
+__global__ void k_piece_write(const int64_t *__restrict__ t_ptr, int64_t n, const int64_t *__restrict__ po,
+                              uint4 *__restrict__ pieces, int4 *__restrict__ fix, unsigned long long *__restrict__ nfix,
+                              int64_t *__restrict__ tile_start) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = t_ptr[j + 1];
         const int64_t np = po[j + 1] - po[j];
         const bool split = np > 1;
+        int64_t b = t_ptr[j];
         for (int64_t c = 0; c < np; ++c) {
-            const int64_t cb = b + c * kPullSplit;
-            const int64_t len = min(kPullSplit, deg - c * kPullSplit);
-            const unsigned long long packed = ((unsigned long long)cb << kLenBits) | (unsigned long long)len;
+            const int64_t pe = piece_end(b, e);
+            const unsigned long long packed = ((unsigned long long)b << kLenBits) | (unsigned long long)(pe - b);
             pieces[po[j] + c] = make_uint4((unsigned)packed, (unsigned)(packed >> 32), (unsigned)j, split ? 1u : 0u);
+            if (b % kPullTile == 0) tile_start[b / kPullTile] = po[j] + c;
+            b = pe;
         }
         if (split) {
             const unsigned long long q = atomicAdd(nfix, 1ull);
@@ -172,16 +191,16 @@ void build_transpose(di_graph *h) {
     DevGraph &g = h->g;
     if (g.has_t) return;
     cudaStream_t st = h->stream;
-    const int64_t n = g.n, m = g.m;
+    const int64_t n = g.n, m = g.m, nt = g.nt;   // rows = owned sources, targets = fluid slots
     const bool wide = m >= (int64_t)0xffffffffLL;
     const size_t vsz = wide ? 8 : 4;
-    DI_CUDA(cudaMalloc(&g.t_ptr, (n + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMalloc(&g.t_ptr, (nt + 1) * sizeof(int64_t)));
     DI_CUDA(cudaMalloc(&g.t_src, (m > 0 ? m : 1) * sizeof(int32_t)));
     const size_t wsz = g.w_kind == DI_W_F32 ? 4 : (g.w_kind == DI_W_F64 ? 8 : 0);
     if (wsz) DI_CUDA(cudaMalloc(&g.t_w, (m > 0 ? m : 1) * wsz));
     int64_t *cnt = nullptr;
-    DI_CUDA(cudaMallocAsync(&cnt, (n + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&cnt, (nt + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMemsetAsync(cnt, 0, (nt + 1) * sizeof(int64_t), st));
     if (m > 0) {
         uint32_t *k0, *k1;
         void *v0, *v1;
@@ -198,7 +217,7 @@ void build_transpose(di_graph *h) {
         DI_CUDA(cudaMallocAsync(&hc, (int64_t)kRadix * ntiles * sizeof(int64_t), st));
         DI_CUDA(cudaMallocAsync(&ho, ((int64_t)kRadix * ntiles + 1) * sizeof(int64_t), st));
         int bits = 1;
-        while (bits < 31 && ((int64_t)1 << bits) < n) ++bits;
+        while (bits < 31 && ((int64_t)1 << bits) < nt) ++bits;
         for (int shift = 0; shift < bits; shift += kRadixBits) {
             radix_sort_pass_launch(k0, v0, k1, v1, m, shift, ntiles, hc, ho, wide, st);
             std::swap(k0, k1);
@@ -230,30 +249,33 @@ void build_transpose(di_graph *h) {
         DI_CUDA(cudaFreeAsync(v0, st));
         DI_CUDA(cudaFreeAsync(v1, st));
     }
-    exclusive_scan_i64(cnt, g.t_ptr, n, st);
+    exclusive_scan_i64(cnt, g.t_ptr, nt, st);
     // pieces
     DevGraph &pd = g;
     int64_t *pc, *po;
-    DI_CUDA(cudaMallocAsync(&pc, (n + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMallocAsync(&po, (n + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&pc, (nt + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&po, (nt + 1) * sizeof(int64_t), st));
     const int grid = h->num_sms * 8;
-    if (n > 0) {
-        k_piece_count<<<grid, kThreads, 0, st>>>(g.t_ptr, n, pc);
+    if (nt > 0) {
+        k_piece_count<<<grid, kThreads, 0, st>>>(g.t_ptr, nt, pc);
         count_launch();
     }
-    exclusive_scan_i64(pc, po, n, st);
+    exclusive_scan_i64(pc, po, nt, st);
     int64_t np = 0;
-    DI_CUDA(cudaMemcpyAsync(&np, po + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaMemcpyAsync(&np, po + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     DI_CUDA(cudaStreamSynchronize(st));
     pd.npieces = np;
     DI_CUDA(cudaMalloc(&pd.pieces, (np > 0 ? np : 1) * sizeof(uint4)));
     DI_CUDA(cudaMalloc(&pd.pbuf, (np > 0 ? np : 1) * sizeof(double)));
-    DI_CUDA(cudaMalloc(&pd.fix, (n > 0 ? n : 1) * sizeof(int4)));
+    DI_CUDA(cudaMalloc(&pd.fix, (nt > 0 ? nt : 1) * sizeof(int4)));
+    pd.ntiles = (m + kPullTile - 1) / kPullTile;
+    DI_CUDA(cudaMalloc(&pd.tile_start, (pd.ntiles + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMemcpyAsync(pd.tile_start + pd.ntiles, &pd.npieces, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     unsigned long long *nf;
     DI_CUDA(cudaMallocAsync(&nf, sizeof(unsigned long long), st));
     DI_CUDA(cudaMemsetAsync(nf, 0, sizeof(unsigned long long), st));
-    if (n > 0) {
-        k_piece_write<<<grid, kThreads, 0, st>>>(g.t_ptr, n, po, pd.pieces, pd.fix, nf);
+    if (nt > 0) {
+        k_piece_write<<<grid, kThreads, 0, st>>>(g.t_ptr, nt, po, pd.pieces, pd.fix, nf, pd.tile_start);
         count_launch();
     }
     unsigned long long nfix = 0;
@@ -268,87 +290,78 @@ void build_transpose(di_graph *h) {
 }
 
 // ---------------------------------------------------------------- pull sweep
+// One CTA per tile of kPullTile consecutive in-edges (grid-stride):
+//   phase 1: v_e = A(src_e) w_e for the tile's edges -> shared memory
+//            (coalesced index/weight streams, gathers of A, no shuffles)
+//   phase 2: one thread per piece sums its slice of v in edge order and adds
+//            it to F(target), or parks it in pbuf for targets cut into pieces.
+// Fixed summation order everywhere: bitwise reproducible on a given graph.
 template <typename W>
 __global__ void __launch_bounds__(kThreads) k_pull(const int32_t *__restrict__ t_src, const W *__restrict__ t_w,
                                                    const double *__restrict__ A, double *__restrict__ F,
-                                                   const uint4 *__restrict__ pieces, int64_t npieces,
+                                                   const uint4 *__restrict__ pieces,
+                                                   const int64_t *__restrict__ tile_start, int64_t ntiles, int64_t m,
                                                    double *__restrict__ pbuf, const Ctrl *__restrict__ ctrl) {
-    __shared__ double acc[kWarps][33];
+    __shared__ double vals[kPullTile];
     if (ctrl->done || !ctrl->use_pull) return;
-    const unsigned lane = lane_id(), wi = threadIdx.x >> 5;
-    const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-    for (int64_t cbase = warp * 32; cbase < npieces; cbase += nwarps * 32) {
-        const int64_t pi = cbase + lane;
-        int len = 0;
-        long long beg = 0;
-        unsigned tgt = 0, split = 0;
-        if (pi < npieces) {
-            const uint4 p = pieces[pi];
-            const unsigned long long packed = ((unsigned long long)p.y << 32) | p.x;
-            len = (int)(packed & ((1ull << kLenBits) - 1));
-            beg = (long long)(packed >> kLenBits);
-            tgt = p.z;
-            split = p.w;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t e0 = t * kPullTile;
+        const int cnt = (int)min((int64_t)kPullTile, m - e0);
+#pragma unroll 8
+        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+            const int64_t e = e0 + k;
+            double v = A[ld_stream_i32(t_src + e)];
+            if constexpr (!std::is_same<W, NoW>::value) v *= load_w(t_w, e);
+            vals[k] = v;
         }
-        acc[wi][lane] = 0.0;
-        __syncwarp();
-        const int incl = warp_incl_scan(len);
-        const int E = __shfl_sync(0xffffffffu, incl, 31);
-        for (int k0 = 0; k0 < E; k0 += 32) {
-            const int k = k0 + (int)lane;
-            int pos = 0;
-#pragma unroll
-            for (int s = 16; s; s >>= 1) {
-                const int v = __shfl_sync(0xffffffffu, incl, pos + s - 1);
-                if (v <= k) pos += s;
-            }
-            const int excl = __shfl_sync(0xffffffffu, incl, pos) - __shfl_sync(0xffffffffu, len, pos);
-            const long long bL = __shfl_sync(0xffffffffu, beg, pos);
-            const bool ok = k < E;
-            const int seg = ok ? pos : 32;
-            double v = 0.0;
-            if (ok) {
-                const int64_t e = bL + (k - excl);
-                const int32_t s = ld_stream_i32(t_src + e);
-                v = A[s];
-                if constexpr (!std::is_same<W, NoW>::value) v *= load_w(t_w, e);
-            }
-            // segmented inclusive scan by piece (fixed order -> deterministic)
-            const int prev = __shfl_up_sync(0xffffffffu, seg, 1);
-            bool head = lane == 0 || prev != seg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double u = __shfl_up_sync(0xffffffffu, v, o);
-                const int hu = __shfl_up_sync(0xffffffffu, (int)head, o);
-                if ((int)lane >= o && !head) {
-                    v += u;
-                    head = hu != 0;
-                }
-            }
-            const int next = __shfl_down_sync(0xffffffffu, seg, 1);
-            const bool tail = lane == 31 || next != seg;
-            if (ok && tail) acc[wi][seg] += v;
-            __syncwarp();
+        __syncthreads();
+        const int64_t p1 = tile_start[t + 1];
+        for (int64_t p = tile_start[t] + threadIdx.x; p < p1; p += kThreads) {
+            const uint4 pc = pieces[p];
+            const unsigned long long packed = ((unsigned long long)pc.y << 32) | pc.x;
+            const int len = (int)(packed & ((1ull << kLenBits) - 1));
+            const int off = (int)((int64_t)(packed >> kLenBits) - e0);
+            double s = 0.0;
+            for (int k = 0; k < len; ++k) s += vals[off + k];
+            if (pc.w) pbuf[p] = s;
+            else F[pc.z] += s;
         }
-        if (pi < npieces) {
-            const double a = acc[wi][lane];
-            if (split) pbuf[pi] = a;
-            else F[tgt] += a;
-        }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
+// Targets cut into several pieces.  A warp takes 32 fix entries: entries with
+// fewer than 32 pieces are summed by their own lane (in piece order), the
+// others by the whole warp (lane-strided, then a fixed butterfly).  Every sum
+// has a fixed order: deterministic.
 __global__ void k_pull_fix(const int4 *__restrict__ fix, int64_t nfix, const double *__restrict__ pbuf,
                            double *__restrict__ F, const Ctrl *__restrict__ ctrl) {
     if (ctrl->done || !ctrl->use_pull) return;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nfix; q += (int64_t)gridDim.x * blockDim.x) {
-        const int4 f = fix[q];
+    const unsigned lane = lane_id();
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 32; base < nfix; base += nw * 32) {
+        const int64_t q = base + lane;
+        int4 f = make_int4(0, 0, 0, 0);
+        if (q < nfix) f = fix[q];
         const int64_t p0 = (int64_t)(unsigned)f.y | ((int64_t)f.z << 32);
-        double s = 0.0;
-        for (int c = 0; c < f.w; ++c) s += pbuf[p0 + c];
-        F[f.x] += s;
+        if (f.w > 0 && f.w < 32) {
+            double s = 0.0;
+            for (int c = 0; c < f.w; ++c) s += pbuf[p0 + c];
+            F[f.x] += s;
+        }
+        unsigned big = __ballot_sync(0xffffffffu, f.w >= 32);
+        while (big) {
+            const int b = __ffs(big) - 1;
+            big &= big - 1;
+            const int j = __shfl_sync(0xffffffffu, f.x, b);
+            const int np = __shfl_sync(0xffffffffu, f.w, b);
+            const int64_t pb = __shfl_sync(0xffffffffu, p0, b);
+            double s = 0.0;
+            for (int c = (int)lane; c < np; c += 32) s += pbuf[pb + c];
+            s = warp_sum(s);
+            if (lane == 0) F[j] += s;
+        }
     }
 }
 
@@ -357,25 +370,26 @@ void launch_pull(di_graph *h) {
     State &s = h->s;
     DevGraph &pd = g;
     const int grid = h->num_sms * 8;
-    if (pd.npieces > 0) {
+    if (pd.ntiles > 0) {
+        const unsigned grid = (unsigned)std::min<int64_t>(pd.ntiles, (int64_t)h->num_sms * 8);
         switch (g.w_kind) {
         case DI_W_F32:
             k_pull<float><<<grid, kThreads, 0, h->stream>>>(g.t_src, (const float *)g.t_w, s.A, s.F, pd.pieces,
-                                                             pd.npieces, pd.pbuf, s.ctrl);
+                                                             pd.tile_start, pd.ntiles, g.m, pd.pbuf, s.ctrl);
             break;
         case DI_W_F64:
             k_pull<double><<<grid, kThreads, 0, h->stream>>>(g.t_src, (const double *)g.t_w, s.A, s.F, pd.pieces,
-                                                              pd.npieces, pd.pbuf, s.ctrl);
+                                                              pd.tile_start, pd.ntiles, g.m, pd.pbuf, s.ctrl);
             break;
         default:
-            k_pull<NoW><<<grid, kThreads, 0, h->stream>>>(g.t_src, nullptr, s.A, s.F, pd.pieces, pd.npieces, pd.pbuf,
-                                                           s.ctrl);
+            k_pull<NoW><<<grid, kThreads, 0, h->stream>>>(g.t_src, nullptr, s.A, s.F, pd.pieces, pd.tile_start,
+                                                           pd.ntiles, g.m, pd.pbuf, s.ctrl);
         }
         count_launch();
     }
     if (pd.nfix > 0) {
-        k_pull_fix<<<(unsigned)std::min<int64_t>((pd.nfix + 255) / 256, 4096), 256, 0, h->stream>>>(pd.fix, pd.nfix,
-                                                                                                    pd.pbuf, s.F, s.ctrl);
+        k_pull_fix<<<(unsigned)std::min<int64_t>((pd.nfix + 255) / 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
+            pd.fix, pd.nfix, pd.pbuf, s.F, s.ctrl);
         count_launch();
     }
 }

@@ -22,11 +22,16 @@ namespace dit {
 
 // ---------------------------------------------------------------- init
 __global__ void __launch_bounds__(kThreads) k_init(double *__restrict__ F, double *__restrict__ H,
-                                                   const double *__restrict__ Z, int64_t n, double d) {
-    const double u = (1.0 - d) / (double)n;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        F[i] = Z ? (1.0 - d) * Z[i] : u;     // Eq. (7): F_0 = (1-d) Z
-        H[i] = 0.0;                          //          H_0 = 0
+                                                   const double *__restrict__ Z, int64_t n, int64_t nt,
+                                                   double n_global, double d) {
+    const double u = (1.0 - d) / n_global;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nt; i += (int64_t)gridDim.x * kThreads) {
+        if (i < n) {
+            F[i] = Z ? (1.0 - d) * Z[i] : u;     // Eq. (7): F_0 = (1-d) Z
+            H[i] = 0.0;                          //          H_0 = 0
+        } else {
+            F[i] = 0.0;                          // shard: ghost fluid slots
+        }
     }
 }
 
@@ -164,19 +169,50 @@ __global__ void __launch_bounds__(kThreads) k_push(const int32_t *__restrict__ c
 }
 
 // ---------------------------------------------------------------- reduce
+// Next-sweep control from the (global) residual r and max fluid fm.
+__device__ void finalize_control(Ctrl *ctrl, double r, double fm, int is_init, int64_t m) {
+    ctrl->resid = r;
+    ctrl->fmax = fm;
+    const double T = ctrl->theta * r / ctrl->n_global;
+    ctrl->T = T < fm ? T : fm;
+    ctrl->done = (r <= ctrl->tol || ctrl->sweeps >= ctrl->max_sweeps) ? 1u : 0u;
+    // direction of the next sweep: AUTO takes this sweep's frontier out-edges
+    // as the estimate of the next one's (the first sweep from a uniform F_0
+    // takes every node)
+    const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->last_sel_edges;
+    if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = 1;
+    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = 0;
+    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ F, int64_t n, int64_t m,
                                                      Ctrl *__restrict__ ctrl, double *__restrict__ part,
                                                      const double *__restrict__ part_sel, int is_init) {
     __shared__ double s_sum[kWarps], s_max[kWarps];
     __shared__ bool s_last;
     if (ctrl->done) return;
-    double s = 0.0, mx = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        const double a = fabs(F[i]);
-        s += a;
-        mx = fmax(mx, a);
+    // two independent 16-byte streams per thread (F is 256-byte aligned)
+    double s0 = 0.0, s1 = 0.0, mx = 0.0;
+    const int64_t n2 = n >> 1;
+    const double2 *F2 = reinterpret_cast<const double2 *>(F);
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    for (; i + stride < n2; i += 2 * stride) {
+        const double2 a = F2[i], b = F2[i + stride];
+        s0 += fabs(a.x) + fabs(a.y);
+        s1 += fabs(b.x) + fabs(b.y);
+        mx = fmax(mx, fmax(fmax(fabs(a.x), fabs(a.y)), fmax(fabs(b.x), fabs(b.y))));
     }
-    s = warp_sum(s);
+    for (; i < n2; i += stride) {
+        const double2 a = F2[i];
+        s0 += fabs(a.x) + fabs(a.y);
+        mx = fmax(mx, fmax(fabs(a.x), fabs(a.y)));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        s1 += fabs(F[n - 1]);
+        mx = fmax(mx, fabs(F[n - 1]));
+    }
+    double s = warp_sum(s0 + s1);
     mx = warp_max(mx);
     const unsigned w = threadIdx.x >> 5;
     if (lane_id() == 0) {
@@ -198,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
     }
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
-    // last block: ordered final sums (deterministic), next-sweep control
+    // last block: ordered final sums (deterministic), sweep bookkeeping
     __threadfence();
     const volatile double *vp = part;
     const volatile double *vs = part_sel;
@@ -222,22 +258,26 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
         ctrl->sweeps += 1;
         ctrl->diffused_edges += ctrl->sel_edges;
         if (ctrl->use_pull) ctrl->pull_sweeps += 1; else ctrl->push_sweeps += 1;
+        ctrl->last_sel_edges = ctrl->sel_edges;
     }
-    ctrl->resid = r;
-    ctrl->fmax = fm;
-    const double T = ctrl->theta * r / (double)n;
-    ctrl->T = T < fm ? T : fm;
-    ctrl->done = (r <= ctrl->tol || ctrl->sweeps >= ctrl->max_sweeps) ? 1u : 0u;
-    // direction choice for the next sweep (AUTO uses this sweep's frontier
-    // edges as the estimate of the next one's; the first sweep from a uniform
-    // F_0 takes every node, see init)
-    const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->sel_edges;
-    if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = 1;
-    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = 0;
-    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? 1 : 0;
     ctrl->n_entries = 0;
     ctrl->sel_edges = 0;
     ctrl->red_blocks = 0;
+    if (ctrl->stats_out) {              // shard: the global values come back through k_control
+        ctrl->stats_out[0] = r;
+        ctrl->stats_out[1] = fm;
+        ctrl->stats_out[2] = ctrl->leak;
+        ctrl->stats_out[3] = (double)ctrl->last_sel_edges;
+        ctrl->stats_is_init = is_init;
+        return;
+    }
+    finalize_control(ctrl, r, fm, is_init, m);
+}
+
+// shard mode: control from the all-reduced {sum r, max fm} (gstats[0], gstats[1])
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m) {
+    if (threadIdx.x != 0 || ctrl->done) return;
+    finalize_control(ctrl, gstats[0], gstats[1], ctrl->stats_is_init, m);
 }
 
 // ---------------------------------------------------------------- output helpers
@@ -273,7 +313,7 @@ void ensure_state(di_graph *h) {
     const int64_t n = h->g.n;
     if (s.F) return;
     const int64_t nn = n > 0 ? n : 1;
-    DI_CUDA(cudaMalloc(&s.F, nn * sizeof(double)));
+    DI_CUDA(cudaMalloc(&s.F, (h->g.nt > 0 ? h->g.nt : 1) * sizeof(double)));
     DI_CUDA(cudaMalloc(&s.H, nn * sizeof(double)));
     s.ent_cap = n + h->g.m / kSplit + 1;
     DI_CUDA(cudaMalloc(&s.ent, s.ent_cap * sizeof(uint4)));
@@ -306,7 +346,7 @@ void init_state(di_graph *h, double d, const double *Z_dev) {
     State &s = h->s;
     const int64_t n = h->g.n;
     if (n > 0) {
-        k_init<<<s.grid, kThreads, 0, h->stream>>>(s.F, s.H, Z_dev, n, d);
+        k_init<<<s.grid, kThreads, 0, h->stream>>>(s.F, s.H, Z_dev, n, h->g.nt, (double)h->g.n_global, d);
         count_launch();
         DI_CUDA(cudaGetLastError());
     }
@@ -316,7 +356,7 @@ void init_state(di_graph *h, double d, const double *Z_dev) {
     DI_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(Ctrl), h->stream));
 }
 
-static void launch_select(di_graph *h, bool pull) {
+void launch_select(di_graph *h, bool pull) {
     State &s = h->s;
     DevGraph &g = h->g;
     if (pull)
@@ -328,7 +368,7 @@ static void launch_select(di_graph *h, bool pull) {
     count_launch();
 }
 
-static void launch_push(di_graph *h) {
+void launch_push(di_graph *h) {
     State &s = h->s;
     DevGraph &g = h->g;
     const int grid = h->num_sms * 8;
@@ -345,7 +385,7 @@ static void launch_push(di_graph *h) {
     count_launch();
 }
 
-static void launch_reduce(di_graph *h, int is_init) {
+void launch_reduce(di_graph *h, int is_init) {
     State &s = h->s;
     k_reduce<<<s.grid, kThreads, 0, h->stream>>>(s.F, h->g.n, h->g.m, s.ctrl, s.part, s.part + 2 * s.grid, is_init);
     count_launch();
@@ -392,7 +432,8 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
     s.last_prof = p;
 }
 
-void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res) {
+// Per-call control block: leak persists with the state, everything else is reset.
+void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats_out) {
     State &s = h->s;
     DevGraph &g = h->g;
     const bool want_pull = o.variant == DI_VARIANT_PULL || o.variant == DI_VARIANT_AUTO;
@@ -400,7 +441,6 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
         build_transpose(h);
         if (!s.A) DI_CUDA(cudaMalloc(&s.A, g.n * sizeof(double)));
     }
-    // per-call control fields (leak persists with the state)
     DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     DI_CUDA(cudaStreamSynchronize(h->stream));
     Ctrl c = *s.ctrl_host;
@@ -414,45 +454,56 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
     c.variant = g.has_t ? o.variant : DI_VARIANT_PUSH;
     c.pull_edges = o.pull_frac * (double)g.m;
     c.hist = s.hist;
+    c.n_global = (double)(g.n_global > 0 ? g.n_global : 1);
+    c.stats_out = stats_out;
     *s.ctrl_host = c;
     DI_CUDA(cudaMemcpyAsync(s.ctrl, s.ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
-    int64_t launched = 0;
-    auto mark = [&](int64_t sweep, int k) {
-        if (!s.profile) return;
-        const size_t idx = (size_t)sweep * 5 + k;
-        while (s.events.size() <= idx) {
-            cudaEvent_t e;
-            DI_CUDA(cudaEventCreate(&e));
-            s.events.push_back(e);
-        }
-        DI_CUDA(cudaEventRecord(s.events[idx], h->stream));
-    };
-    if (g.n > 0) {
-        launch_reduce(h, 1);
-        int chunk = 2;
-        for (;;) {
-            for (int k = 0; k < chunk; ++k, ++launched) {
-                const bool rec = launched < kHistCap;
-                if (rec) mark(launched, 0);
-                launch_select(h, false);
-                if (g.has_t) launch_select(h, true);
-                if (rec) mark(launched, 1);
-                launch_push(h);
-                if (rec) mark(launched, 2);
-                if (g.has_t) launch_pull(h);
-                if (rec) mark(launched, 3);
-                launch_reduce(h, 0);
-                if (rec) mark(launched, 4);
-            }
-            DI_CUDA(cudaGetLastError());
-            DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
-            DI_CUDA(cudaStreamSynchronize(h->stream));
-            if (s.ctrl_host->done) break;
-            chunk = std::min(chunk * 2, 64);
-        }
-    } else {
-        s.ctrl_host->done = 1;
+    s.launched = 0;
+}
+
+void mark_event(di_graph *h, int64_t sweep, int k) {
+    State &s = h->s;
+    if (!s.profile || sweep >= kHistCap) return;
+    const size_t idx = (size_t)sweep * 5 + k;
+    while (s.events.size() <= idx) {
+        cudaEvent_t e;
+        DI_CUDA(cudaEventCreate(&e));
+        s.events.push_back(e);
     }
+    DI_CUDA(cudaEventRecord(s.events[idx], h->stream));
+}
+
+// select + diffusion of one sweep (events 0..3 of the sweep when profiling)
+void launch_sweep(di_graph *h) {
+    State &s = h->s;
+    const int64_t k = s.launched;
+    mark_event(h, k, 0);
+    launch_select(h, false);
+    if (h->g.has_t) launch_select(h, true);
+    mark_event(h, k, 1);
+    launch_push(h);
+    mark_event(h, k, 2);
+    if (h->g.has_t) launch_pull(h);
+    mark_event(h, k, 3);
+}
+
+void launch_sweep_reduce(di_graph *h) {
+    launch_reduce(h, 0);
+    mark_event(h, h->s.launched, 4);
+    h->s.launched += 1;
+}
+
+bool poll_done(di_graph *h) {
+    State &s = h->s;
+    DI_CUDA(cudaGetLastError());
+    DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+    DI_CUDA(cudaStreamSynchronize(h->stream));
+    return s.ctrl_host->done != 0;
+}
+
+void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res) {
+    State &s = h->s;
+    DevGraph &g = h->g;
     const Ctrl &r = *s.ctrl_host;
     s.last_sweeps = (int64_t)r.sweeps;
     if (s.profile) collect_profile(h, r);
@@ -471,6 +522,26 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
         res->pull_sweeps = (int64_t)r.pull_sweeps;
         res->converged = res->residual_l1 <= tol ? 1 : 0;
     }
+}
+
+void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res) {
+    State &s = h->s;
+    prepare_call(h, tol, o, nullptr);
+    if (h->g.n > 0) {
+        launch_reduce(h, 1);
+        int chunk = 2;
+        for (;;) {
+            for (int k = 0; k < chunk; ++k) {
+                launch_sweep(h);
+                launch_sweep_reduce(h);
+            }
+            if (poll_done(h)) break;
+            chunk = std::min(chunk * 2, 64);
+        }
+    } else {
+        s.ctrl_host->done = 1;
+    }
+    fill_result(h, o, tol, res);
 }
 
 void write_H(di_graph *h, double factor, double *H_out, int mem) {
