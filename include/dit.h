@@ -108,7 +108,8 @@ void di_solve_opts_default(di_solve_opts *o);
  *   weights  NULL (w_dtype DI_W_NONE) or w_dtype[m] raw weights, each > 0
  *   mem      DI_MEM_HOST / DI_MEM_DEVICE for row_ptr, col and weights
  *   device   CUDA device ordinal
- *   stream   cudaStream_t to run on (NULL: a stream owned by the handle)
+ *   stream   cudaStream_t every call on this handle runs on (NULL = the CUDA
+ *            default stream, the usual CUDA convention)
  * Builds on the device (Eq. (1)): the per-source scale
  * 1/sum_k w_{j,k} (1/out(j) unweighted; 0 marks a dangling node); the
  * transpose for the pull variant is built lazily on first use.
@@ -201,6 +202,51 @@ int di_profile_get(const di_graph *g, di_profile *out);
  */
 int di_sweep_history(const di_graph *g, int64_t cap, int64_t *nodes, int64_t *edges, int64_t *entries,
                      int32_t *variant, int64_t *count);
+
+/*
+ * ---- Multi-GPU shards ----
+ * One process per GPU owns the contiguous node range [lo, hi) of a graph with
+ * n_global nodes: its out-edges (CSR rows lo..hi-1, `col` holding GLOBAL ids)
+ * and the fluid / history of its nodes.  Fluid pushed to a node of another
+ * rank accumulates in a "ghost" slot (one per distinct remote target, in
+ * ascending global id); after every sweep the caller moves the ghost fluid
+ * to its owners (an all-to-all, e.g. NCCL over NVLink) and adds what it
+ * received with di_shard_apply; the residual and max fluid are all-reduced
+ * (sum / max) by the caller between di_shard_reduce and di_shard_control.
+ * Every di_shard_* call except create/info/ghost_ids/set_recv/poll/finish is
+ * asynchronous on the handle's stream.  DESIGN.md reading R1 covers why the
+ * exchange after the sweep is still an exact D-Iteration.
+ */
+int di_shard_create(int64_t n_global, int64_t lo, int64_t hi, int64_t m, const int64_t *row_ptr,
+                    const int32_t *col, const void *weights, int32_t w_dtype, int32_t mem, int32_t device,
+                    void *stream, di_graph **out);
+/* owned nodes (hi - lo), ghost slots, lo */
+int di_shard_info(const di_graph *g, int64_t *n_local, int64_t *n_ghost, int64_t *lo);
+/* global ids of the ghost slots, ascending (int32[n_ghost]) */
+int di_shard_ghost_ids(const di_graph *g, int32_t *ids, int32_t mem);
+/* receive map: local_idx[total] (owned ids - lo) in the order values arrive,
+ * cut into nseg consecutive segments of seg_counts[k] values (one per source
+ * rank; ids are distinct within a segment) */
+int di_shard_set_recv(di_graph *g, int64_t total, const int32_t *local_idx, int32_t nseg,
+                      const int64_t *seg_counts, int32_t mem);
+/* F_0 = (1-d) Z on owned nodes (Z: owned slice or NULL = 1/n_global), H_0 = 0;
+ * local {|F|_1, max|F|, leak, frontier edges} -> stats (device double[4],
+ * retained until di_shard_finish) */
+int di_shard_begin(di_graph *g, double d, const double *Z, int32_t Z_mem, double tol,
+                   const di_solve_opts *opts, double *stats);
+/* next threshold / done flag from the all-reduced gstats = {sum |F|_1, max |F|} (device) */
+int di_shard_control(di_graph *g, const double *gstats);
+/* one sweep (select + diffusion); ghost fluid moved to ghost_out (device double[n_ghost]) */
+int di_shard_sweep(di_graph *g, double *ghost_out);
+/* F[local_idx[q]] += recv[q] (device double[total]), segment by segment */
+int di_shard_apply(di_graph *g, const double *recv);
+/* local statistics of the current F into the stats buffer given to di_shard_begin */
+int di_shard_reduce(di_graph *g);
+/* host-synchronous: 1 once the control block says done */
+int di_shard_poll(di_graph *g, int32_t *done);
+/* local H (owned nodes) and local counters; residual_l1 / bound are global */
+int di_shard_finish(di_graph *g, double tol, const di_solve_opts *opts, double *H_out, int32_t H_mem,
+                    di_result *res);
 
 /* Text of the last error raised on the calling thread ("" if none). */
 const char *di_last_error(void);

@@ -246,3 +246,90 @@ def di_sweep_history(h, cap=1 << 16):
                                  var.ctypes.data, ctypes.byref(cnt)))
     k = cnt.value
     return nodes[:k], edges[:k], ent[:k], var[:k]
+
+
+# ------------------------------------------------------------------ shards (multi-GPU)
+EXPORTS += ["di_shard_create", "di_shard_info", "di_shard_ghost_ids", "di_shard_set_recv", "di_shard_begin",
+            "di_shard_control", "di_shard_sweep", "di_shard_apply", "di_shard_reduce", "di_shard_poll",
+            "di_shard_finish"]
+_lib.di_shard_create.argtypes = [_I64, _I64, _I64, _I64, _P, _P, _P, _I32, _I32, _I32, _P, ctypes.POINTER(_P)]
+_lib.di_shard_info.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
+_lib.di_shard_ghost_ids.argtypes = [_P, _P, _I32]
+_lib.di_shard_set_recv.argtypes = [_P, _I64, _P, _I32, _P, _I32]
+_lib.di_shard_begin.argtypes = [_P, _D, _P, _I32, _D, ctypes.POINTER(di_solve_opts), _P]
+_lib.di_shard_control.argtypes = [_P, _P]
+_lib.di_shard_sweep.argtypes = [_P, _P]
+_lib.di_shard_apply.argtypes = [_P, _P]
+_lib.di_shard_reduce.argtypes = [_P]
+_lib.di_shard_poll.argtypes = [_P, ctypes.POINTER(_I32)]
+_lib.di_shard_finish.argtypes = [_P, _D, ctypes.POINTER(di_solve_opts), _P, _I32, ctypes.POINTER(di_result)]
+for _name in EXPORTS[-11:]:
+    getattr(_lib, _name).restype = ctypes.c_int
+
+
+def di_shard_create(n_global, lo, hi, row_ptr, col, weights=None, device=0, stream=None):
+    m = int(row_ptr[-1]) if len(row_ptr) else 0
+    rp, mem, k1 = _ptr_mem(row_ptr, np.int64)
+    cp, mem2, k2 = _ptr_mem(col, np.int32)
+    wp, mem3, k3 = _ptr_mem(weights)
+    if len({mem, mem2} | ({mem3} if weights is not None else set())) != 1:
+        raise ValueError("row_ptr, col and weights must all be host or all be device")
+    h = _P()
+    _check(_lib.di_shard_create(n_global, lo, hi, m, rp, cp, wp, _wdtype(weights), mem, device,
+                                _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def di_shard_info(h):
+    a, b, c = _I64(), _I64(), _I64()
+    _check(_lib.di_shard_info(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return a.value, b.value, c.value
+
+
+def di_shard_ghost_ids(h, out):
+    p, mem, k = _ptr_mem(out)
+    _check(_lib.di_shard_ghost_ids(h, p, mem))
+    return out
+
+
+def di_shard_set_recv(h, local_idx, seg_counts):
+    p, mem, k = _ptr_mem(local_idx, np.int32)
+    seg = np.ascontiguousarray(seg_counts, dtype=np.int64)
+    _check(_lib.di_shard_set_recv(h, int(seg.sum()), p, len(seg), seg.ctypes.data, mem))
+
+
+def di_shard_begin(h, d, Z=None, tol=1e-12, stats=None, **opts):
+    zp, zmem, kz = _ptr_mem(Z, np.float64)
+    sp, smem, ks = _ptr_mem(stats)
+    o = _opts(**opts)
+    _check(_lib.di_shard_begin(h, d, zp, zmem, tol, ctypes.byref(o), sp))
+
+
+def di_shard_control(h, gstats):
+    _check(_lib.di_shard_control(h, _ptr_mem(gstats)[0]))
+
+
+def di_shard_sweep(h, ghost_out):
+    _check(_lib.di_shard_sweep(h, _ptr_mem(ghost_out)[0]))
+
+
+def di_shard_apply(h, recv):
+    _check(_lib.di_shard_apply(h, _ptr_mem(recv)[0]))
+
+
+def di_shard_reduce(h):
+    _check(_lib.di_shard_reduce(h))
+
+
+def di_shard_poll(h):
+    d = _I32()
+    _check(_lib.di_shard_poll(h, ctypes.byref(d)))
+    return bool(d.value)
+
+
+def di_shard_finish(h, tol=1e-12, H_out=None, **opts):
+    hp, hmem, kh = _ptr_mem(H_out)
+    res = di_result()
+    o = _opts(**opts)
+    _check(_lib.di_shard_finish(h, tol, ctypes.byref(o), hp, hmem, ctypes.byref(res)))
+    return res

@@ -99,13 +99,8 @@ int di_graph_create(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t 
         g->device = device;
         try {
             cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
-            if (stream) {
-                g->stream = (cudaStream_t)stream;
-            } else {
-                DI_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
-                g->own_stream = true;
-            }
-            create_graph(g, n, m, row_ptr, col, weights, w_dtype, mem);
+            g->stream = (cudaStream_t)stream;   // NULL = the CUDA default stream
+            create_graph(g, n, m, row_ptr, col, weights, w_dtype, mem, n);
         } catch (...) {
             free_graph(g->g);
             if (g->own_stream) cudaStreamDestroy(g->stream);
@@ -141,6 +136,7 @@ int di_solve(di_graph *g, double d, const double *Z, int32_t Z_mem, double tol, 
              double *H_out, int32_t H_mem, di_result *res) {
     return guarded([&] {
         if (!g) fail(DI_ERR_INVALID, "graph is NULL");
+        if (g->g.shard) fail(DI_ERR_INVALID, "di_solve on a shard handle: use the di_shard_* protocol");
         if (!(d > 0.0 && d < 1.0)) fail(DI_ERR_INVALID, "d must be in (0, 1)");
         if (!(tol >= 0.0)) fail(DI_ERR_INVALID, "tol must be >= 0");
         if ((Z || H_out) && (Z_mem != DI_MEM_HOST && Z_mem != DI_MEM_DEVICE)) fail(DI_ERR_INVALID, "Z_mem");
@@ -165,6 +161,7 @@ int di_solve(di_graph *g, double d, const double *Z, int32_t Z_mem, double tol, 
 int di_resume(di_graph *g, double tol, const di_solve_opts *opts, double *H_out, int32_t H_mem, di_result *res) {
     return guarded([&] {
         if (!g) fail(DI_ERR_INVALID, "graph is NULL");
+        if (g->g.shard) fail(DI_ERR_INVALID, "di_resume on a shard handle");
         if (!g->s.valid) fail(DI_ERR_STATE, "di_resume: no DI state (call di_solve or di_set_state first)");
         if (!(tol >= 0.0)) fail(DI_ERR_INVALID, "tol must be >= 0");
         if (H_out && H_mem != DI_MEM_HOST && H_mem != DI_MEM_DEVICE) fail(DI_ERR_INVALID, "H_mem");
@@ -178,6 +175,7 @@ int di_update_edges(di_graph *g, int64_t n_add, const int32_t *add_src, const in
                     int32_t w_dtype, int64_t n_rem, const int32_t *rem_src, const int32_t *rem_dst, int32_t mem) {
     return guarded([&] {
         if (!g) fail(DI_ERR_INVALID, "graph is NULL");
+        if (g->g.shard) fail(DI_ERR_INVALID, "di_update_edges is not supported on shards");
         if (n_add < 0 || n_rem < 0) fail(DI_ERR_INVALID, "negative counts");
         if (n_add > 0 && (!add_src || !add_dst)) fail(DI_ERR_INVALID, "add_src / add_dst is NULL");
         if (n_rem > 0 && (!rem_src || !rem_dst)) fail(DI_ERR_INVALID, "rem_src / rem_dst is NULL");
@@ -265,6 +263,176 @@ int di_sweep_history(const di_graph *gc, int64_t cap, int64_t *nodes, int64_t *e
             if (variant) variant[k] = hs[k].use_pull;
         }
         if (count) *count = S;
+    });
+}
+
+// ---------------------------------------------------------------- shards
+int di_shard_create(int64_t n_global, int64_t lo, int64_t hi, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                    const void *weights, int32_t w_dtype, int32_t mem, int32_t device, void *stream, di_graph **out) {
+    return guarded([&] {
+        if (!out) fail(DI_ERR_INVALID, "out is NULL");
+        if (n_global < 0 || n_global >= (1LL << 31) || lo < 0 || hi < lo || hi > n_global || m < 0)
+            fail(DI_ERR_INVALID, "need 0 <= lo <= hi <= n_global < 2^31, m >= 0");
+        if (!row_ptr || (m > 0 && !col)) fail(DI_ERR_INVALID, "row_ptr / col is NULL");
+        if (w_dtype != DI_W_NONE && w_dtype != DI_W_F32 && w_dtype != DI_W_F64) fail(DI_ERR_INVALID, "w_dtype");
+        if (w_dtype != DI_W_NONE && m > 0 && !weights) fail(DI_ERR_INVALID, "weights is NULL");
+        if (mem != DI_MEM_HOST && mem != DI_MEM_DEVICE) fail(DI_ERR_INVALID, "mem");
+        if (mem == DI_MEM_HOST && row_ptr[hi - lo] != m) fail(DI_ERR_INVALID, "row_ptr[hi-lo] != m");
+        if (m >= (1LL << 40)) fail(DI_ERR_INVALID, "m must be < 2^40");
+        DI_CUDA(cudaSetDevice(device));
+        di_graph *g = new di_graph();
+        g->device = device;
+        try {
+            cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+            g->stream = (cudaStream_t)stream;   // NULL = the CUDA default stream
+            create_shard(g, n_global, lo, hi, m, row_ptr, col, weights, w_dtype, mem);
+        } catch (...) {
+            free_graph(g->g);
+            if (g->own_stream) cudaStreamDestroy(g->stream);
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+static void need_shard(const di_graph *g) {
+    if (!g) fail(DI_ERR_INVALID, "graph is NULL");
+    if (!g->g.shard) fail(DI_ERR_INVALID, "not a shard handle (use di_shard_create)");
+}
+
+int di_shard_info(const di_graph *g, int64_t *n_local, int64_t *n_ghost, int64_t *lo) {
+    return guarded([&] {
+        need_shard(g);
+        if (n_local) *n_local = g->g.n;
+        if (n_ghost) *n_ghost = g->g.nt - g->g.n;
+        if (lo) *lo = g->g.lo;
+    });
+}
+
+int di_shard_ghost_ids(const di_graph *gc, int32_t *ids, int32_t mem) {
+    return guarded([&] {
+        need_shard(gc);
+        di_graph *g = const_cast<di_graph *>(gc);
+        if (mem != DI_MEM_HOST && mem != DI_MEM_DEVICE) fail(DI_ERR_INVALID, "mem");
+        use_device(g);
+        const int64_t ng = g->g.nt - g->g.n;
+        if (ng > 0) {
+            if (!ids) fail(DI_ERR_INVALID, "ids is NULL");
+            DI_CUDA(cudaMemcpyAsync(ids, g->g.ghost_ids, ng * sizeof(int32_t),
+                                    mem == DI_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                    g->stream));
+        }
+        DI_CUDA(cudaStreamSynchronize(g->stream));
+    });
+}
+
+int di_shard_set_recv(di_graph *g, int64_t total, const int32_t *local_idx, int32_t nseg, const int64_t *seg_counts,
+                      int32_t mem) {
+    return guarded([&] {
+        need_shard(g);
+        if (total < 0 || nseg < 0 || (nseg > 0 && !seg_counts) || (total > 0 && !local_idx))
+            fail(DI_ERR_INVALID, "bad receive map");
+        int64_t sum = 0;
+        for (int k = 0; k < nseg; ++k) {
+            if (seg_counts[k] < 0) fail(DI_ERR_INVALID, "negative segment");
+            sum += seg_counts[k];
+        }
+        if (sum != total) fail(DI_ERR_INVALID, "segment counts do not add up to total");
+        if (mem != DI_MEM_HOST && mem != DI_MEM_DEVICE) fail(DI_ERR_INVALID, "mem");
+        use_device(g);
+        shard_set_recv(g, total, local_idx, nseg, seg_counts, mem);
+    });
+}
+
+int di_shard_begin(di_graph *g, double d, const double *Z, int32_t Z_mem, double tol, const di_solve_opts *opts,
+                   double *stats) {
+    return guarded([&] {
+        need_shard(g);
+        if (!(d > 0.0 && d < 1.0)) fail(DI_ERR_INVALID, "d must be in (0, 1)");
+        if (!(tol >= 0.0)) fail(DI_ERR_INVALID, "tol must be >= 0");
+        if (!stats) fail(DI_ERR_INVALID, "stats is NULL");
+        const di_solve_opts o = resolve(opts);
+        use_device(g);
+        double *Zd = nullptr;
+        if (Z && g->g.n > 0) {
+            if (Z_mem == DI_MEM_HOST) {
+                DI_CUDA(cudaMallocAsync(&Zd, g->g.n * sizeof(double), g->stream));
+                DI_CUDA(cudaMemcpyAsync(Zd, Z, g->g.n * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+            } else {
+                Zd = const_cast<double *>(Z);
+            }
+        }
+        init_state(g, d, Zd);
+        if (Zd && Z_mem == DI_MEM_HOST) DI_CUDA(cudaFreeAsync(Zd, g->stream));
+        prepare_call(g, tol, o, stats);
+        launch_reduce(g, 1);
+        DI_CUDA(cudaGetLastError());
+    });
+}
+
+int di_shard_control(di_graph *g, const double *gstats) {
+    return guarded([&] {
+        need_shard(g);
+        if (!gstats) fail(DI_ERR_INVALID, "gstats is NULL");
+        use_device(g);
+        shard_control(g, gstats);
+    });
+}
+
+int di_shard_sweep(di_graph *g, double *ghost_out) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        if (g->g.nt > g->g.n && !ghost_out) fail(DI_ERR_INVALID, "ghost_out is NULL");
+        use_device(g);
+        shard_sweep(g, ghost_out);
+    });
+}
+
+int di_shard_apply(di_graph *g, const double *recv) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        int64_t tot = 0;
+        for (int64_t c : g->g.recv_seg) tot += c;
+        if (tot > 0 && !recv) fail(DI_ERR_INVALID, "recv is NULL");
+        use_device(g);
+        shard_apply(g, recv);
+    });
+}
+
+int di_shard_reduce(di_graph *g) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        use_device(g);
+        launch_sweep_reduce(g);
+        DI_CUDA(cudaGetLastError());
+    });
+}
+
+int di_shard_poll(di_graph *g, int32_t *done) {
+    return guarded([&] {
+        need_shard(g);
+        use_device(g);
+        const bool d = poll_done(g);
+        if (done) *done = d ? 1 : 0;
+    });
+}
+
+int di_shard_finish(di_graph *g, double tol, const di_solve_opts *opts, double *H_out, int32_t H_mem,
+                    di_result *res) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        const di_solve_opts o = resolve(opts);
+        use_device(g);
+        poll_done(g);
+        di_result r;
+        fill_result(g, o, tol, &r);
+        write_H(g, r.norm_factor, H_out, H_mem);
+        if (res) *res = r;
     });
 }
 

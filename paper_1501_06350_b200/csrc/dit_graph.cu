@@ -86,7 +86,7 @@ void build_scales(di_graph *h) {
     launch_scales(h, nullptr);
 }
 
-static int grid_for(di_graph *h, int64_t count) {
+int grid_for(di_graph *h, int64_t count) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)h->num_sms * 16));
 }
 
@@ -99,7 +99,7 @@ static int read_flag(int *dflag, cudaStream_t st) {
 
 // Copy + validate the caller's CSR into the handle.
 void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
-                  const void *weights, int w_dtype, int mem) {
+                  const void *weights, int w_dtype, int mem, int64_t col_bound) {
     DevGraph &g = h->g;
     cudaStream_t st = h->stream;
     g.n = n;
@@ -124,11 +124,11 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     count_launch();
     if (m > 0) {
         if (w_dtype == DI_W_F32)
-            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, (const float *)wtmp, m, n, flags, flags + 1);
+            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, (const float *)wtmp, m, col_bound, flags, flags + 1);
         else if (w_dtype == DI_W_F64)
-            k_check_edges<double><<<grid_for(h, m), 256, 0, st>>>(g.col, (const double *)wtmp, m, n, flags, flags + 1);
+            k_check_edges<double><<<grid_for(h, m), 256, 0, st>>>(g.col, (const double *)wtmp, m, col_bound, flags, flags + 1);
         else
-            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, nullptr, m, n, flags, flags + 1);
+            k_check_edges<float><<<grid_for(h, m), 256, 0, st>>>(g.col, nullptr, m, col_bound, flags, flags + 1);
         count_launch();
     }
     DI_CUDA(cudaGetLastError());
@@ -139,7 +139,7 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     if (fl[0]) {
         cudaFree(wtmp);
         set_error(fl[0] & 1 ? "row_ptr must be non-decreasing with row_ptr[0]=0 and row_ptr[n]=m"
-                            : (fl[0] & 2 ? "col ids must be in [0, n)" : "weights must be finite and > 0"));
+                            : (fl[0] & 2 ? "col ids must be in [0, n) (n_global for a shard)" : "weights must be finite and > 0"));
         throw Fail{DI_ERR_INVALID};
     }
     if (w_dtype == DI_W_F32 && m > 0) {

@@ -143,7 +143,15 @@ void init_state(di_graph *h, double d, const double *Z_dev);
 void write_H(di_graph *h, double factor, double *H_out, int mem);
 void set_leak_from_history(di_graph *h);
 void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
-                  const void *weights, int w_dtype, int mem);
+                  const void *weights, int w_dtype, int mem, int64_t col_bound);
+int grid_for(di_graph *h, int64_t count);
+void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t m, const int64_t *row_ptr,
+                  const int32_t *col, const void *weights, int w_dtype, int mem);
+void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int nseg, const int64_t *seg_counts,
+                    int mem);
+void shard_sweep(di_graph *h, double *ghost_out);
+void shard_apply(di_graph *h, const double *recv);
+void shard_control(di_graph *h, const double *gstats);
 void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int32_t *add_dst,
                   const void *add_w, int w_dtype, int64_t n_rem, const int32_t *rem_src,
                   const int32_t *rem_dst, int mem);

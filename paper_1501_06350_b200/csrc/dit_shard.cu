@@ -1,0 +1,159 @@
+// dit_shard.cu -- one rank of the multi-GPU D-Iteration.
+//
+// A shard owns nodes [lo, hi) of an n_global-node graph and their out-edges.
+// Targets outside [lo, hi) are renumbered to ghost slots n_local + g, g the
+// rank of the target among the distinct remote targets (ascending global id,
+// found with a bitmap over n_global ids and a popcount prefix sum), so the
+// sweep kernels run unchanged on n_local + n_ghost fluid slots.  After a
+// sweep the ghost fluid is handed to the caller's all-to-all and the fluid
+// received from the other ranks is added to the owned nodes.
+#include "dit_internal.cuh"
+
+namespace dit {
+
+__global__ void k_mark_remote(const int32_t *__restrict__ col, int64_t m, int64_t lo, int64_t hi,
+                              unsigned *__restrict__ bm) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = col[e];
+        if (t < lo || t >= hi) atomicOr(&bm[t >> 5], 1u << (t & 31));
+    }
+}
+
+__global__ void k_word_pop(const unsigned *__restrict__ bm, int64_t nw, int64_t *__restrict__ pc) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x)
+        pc[w] = __popc(bm[w]);
+}
+
+__global__ void k_remap(int32_t *__restrict__ col, int64_t m, int64_t lo, int64_t hi, const unsigned *__restrict__ bm,
+                        const int64_t *__restrict__ wpre, int64_t n_local) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = col[e];
+        if (t >= lo && t < hi) {
+            col[e] = (int32_t)(t - lo);
+        } else {
+            const unsigned below = bm[t >> 5] & ((1u << (t & 31)) - 1u);
+            col[e] = (int32_t)(n_local + wpre[t >> 5] + __popc(below));
+        }
+    }
+}
+
+__global__ void k_ghost_ids(const unsigned *__restrict__ bm, const int64_t *__restrict__ wpre, int64_t nw,
+                            int32_t *__restrict__ ids) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        unsigned bits = bm[w];
+        int64_t pos = wpre[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            ids[pos++] = (int32_t)(w * 32 + b);
+        }
+    }
+}
+
+void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t m, const int64_t *row_ptr,
+                  const int32_t *col, const void *weights, int w_dtype, int mem) {
+    const int64_t n_local = hi - lo;
+    create_graph(h, n_local, m, row_ptr, col, weights, w_dtype, mem, n_global);
+    DevGraph &g = h->g;
+    cudaStream_t st = h->stream;
+    const int64_t nw = (n_global + 31) / 32;
+    unsigned *bm = nullptr;
+    int64_t *pc = nullptr, *wpre = nullptr;
+    DI_CUDA(cudaMallocAsync(&bm, (nw > 0 ? nw : 1) * sizeof(unsigned), st));
+    DI_CUDA(cudaMallocAsync(&pc, (nw > 0 ? nw : 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&wpre, (nw + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMemsetAsync(bm, 0, (nw > 0 ? nw : 1) * sizeof(unsigned), st));
+    if (m > 0) {
+        k_mark_remote<<<grid_for(h, m), 256, 0, st>>>(g.col, m, lo, hi, bm);
+        count_launch();
+    }
+    if (nw > 0) {
+        k_word_pop<<<grid_for(h, nw), 256, 0, st>>>(bm, nw, pc);
+        count_launch();
+    }
+    exclusive_scan_i64(pc, wpre, nw, st);
+    int64_t n_ghost = 0;
+    DI_CUDA(cudaMemcpyAsync(&n_ghost, wpre + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    if (m > 0) {
+        k_remap<<<grid_for(h, m), 256, 0, st>>>(g.col, m, lo, hi, bm, wpre, n_local);
+        count_launch();
+    }
+    DI_CUDA(cudaMalloc(&g.ghost_ids, (n_ghost > 0 ? n_ghost : 1) * sizeof(int32_t)));
+    if (nw > 0) {
+        k_ghost_ids<<<grid_for(h, nw), 256, 0, st>>>(bm, wpre, nw, g.ghost_ids);
+        count_launch();
+    }
+    DI_CUDA(cudaFreeAsync(bm, st));
+    DI_CUDA(cudaFreeAsync(pc, st));
+    DI_CUDA(cudaFreeAsync(wpre, st));
+    DI_CUDA(cudaGetLastError());
+    DI_CUDA(cudaStreamSynchronize(st));
+    g.nt = n_local + n_ghost;
+    g.n_global = n_global;
+    g.lo = lo;
+    g.shard = true;
+}
+
+void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int nseg, const int64_t *seg_counts,
+                    int mem) {
+    DevGraph &g = h->g;
+    cudaFree(g.recv_idx);
+    g.recv_idx = nullptr;
+    DI_CUDA(cudaMalloc(&g.recv_idx, (total > 0 ? total : 1) * sizeof(int32_t)));
+    if (total > 0)
+        DI_CUDA(cudaMemcpyAsync(g.recv_idx, local_idx, total * sizeof(int32_t),
+                                mem == DI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+    g.recv_seg.assign(seg_counts, seg_counts + nseg);
+    DI_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+// ghost fluid -> caller's send buffer; ghost slots cleared for the next sweep
+__global__ void k_take_ghosts(double *__restrict__ Fg, int64_t ng, double *__restrict__ out,
+                              const Ctrl *__restrict__ ctrl) {
+    if (ctrl->done) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
+        out[i] = Fg[i];
+        Fg[i] = 0.0;
+    }
+}
+
+// one source rank's segment: its ghost ids are distinct, so plain adds
+__global__ void k_apply_seg(double *__restrict__ F, const int32_t *__restrict__ idx, const double *__restrict__ v,
+                            int64_t cnt, const Ctrl *__restrict__ ctrl) {
+    if (ctrl->done) return;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x)
+        F[idx[q]] += v[q];
+}
+
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m);
+
+void shard_sweep(di_graph *h, double *ghost_out) {
+    launch_sweep(h);
+    const int64_t ng = h->g.nt - h->g.n;
+    if (ng > 0) {
+        k_take_ghosts<<<grid_for(h, ng), 256, 0, h->stream>>>(h->s.F + h->g.n, ng, ghost_out, h->s.ctrl);
+        count_launch();
+    }
+    DI_CUDA(cudaGetLastError());
+}
+
+void shard_apply(di_graph *h, const double *recv) {
+    int64_t off = 0;
+    for (int64_t c : h->g.recv_seg) {   // source ranks in order: deterministic
+        if (c > 0) {
+            k_apply_seg<<<grid_for(h, c), 256, 0, h->stream>>>(h->s.F, h->g.recv_idx + off, recv + off, c, h->s.ctrl);
+            count_launch();
+        }
+        off += c;
+    }
+    DI_CUDA(cudaGetLastError());
+}
+
+void shard_control(di_graph *h, const double *gstats) {
+    k_control<<<1, 32, 0, h->stream>>>(h->s.ctrl, gstats, h->g.m);
+    count_launch();
+    DI_CUDA(cudaGetLastError());
+}
+
+}  // namespace dit

@@ -1,0 +1,227 @@
+"""Multi-GPU D-Iteration: one process per GPU, contiguous node ranges.
+
+Rank r owns nodes [lo_r, hi_r) = [r n / R, (r+1) n / R) and their out-edges.
+Every sweep of every rank runs in libdit (di_shard_sweep: frontier select +
+diffusion, fluid for other ranks accumulating in ghost slots); between sweeps
+the ranks exchange ghost fluid with one NCCL all-to-all over NVLink and
+all-reduce the residual (sum) and the max fluid (max) that set the next
+frontier threshold and the stop test.  This module only sequences those calls
+(argument marshalling and collectives); it does no arithmetic of the method.
+
+The protocol is written against a `collectives` object so that the same code
+drives torch.distributed (NCCL on GPUs, gloo in the CPU tests) and, in the
+tests, several shards of one process on one GPU run in lock step.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def node_ranges(n, world):
+    """Contiguous, balanced node ranges: bounds[r] .. bounds[r+1]."""
+    return [n * r // world for r in range(world + 1)]
+
+
+class CudaShard:
+    """One rank's libdit shard handle plus its device exchange buffers."""
+
+    def __init__(self, n_global, lo, hi, row_ptr, col, weights=None, device=0, stream=None):
+        self.n_global, self.lo, self.hi = int(n_global), int(lo), int(hi)
+        self.dev = torch.device("cuda", device)
+        self.h = _lib.di_shard_create(n_global, lo, hi, row_ptr, col, weights, device=device, stream=stream)
+        self.n_local, self.n_ghost, _ = _lib.di_shard_info(self.h)
+        self.ghost_ids = torch.empty(self.n_ghost, dtype=torch.int32, device=self.dev)
+        if self.n_ghost:
+            _lib.di_shard_ghost_ids(self.h, self.ghost_ids)
+        self.send = torch.zeros(max(self.n_ghost, 1), dtype=torch.float64, device=self.dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=self.dev)
+        self.gstats = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        self.recv = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.send_counts = None
+        self.recv_counts = None
+
+    # --- exchange plan
+    def set_recv(self, local_idx, seg_counts):
+        _lib.di_shard_set_recv(self.h, local_idx, seg_counts)
+        self.recv = torch.zeros(max(int(sum(seg_counts)), 1), dtype=torch.float64, device=self.dev)
+        self.recv_counts = [int(c) for c in seg_counts]
+
+    # --- protocol steps (asynchronous on the shard's stream)
+    def begin(self, d, tol, **opts):
+        _lib.di_shard_begin(self.h, d, None, tol, self.stats, **opts)
+
+    def control(self):
+        _lib.di_shard_control(self.h, self.gstats)
+
+    def sweep(self):
+        _lib.di_shard_sweep(self.h, self.send)
+
+    def apply(self):
+        _lib.di_shard_apply(self.h, self.recv)
+
+    def reduce(self):
+        _lib.di_shard_reduce(self.h)
+
+    def poll(self):
+        return _lib.di_shard_poll(self.h)
+
+    def finish(self, tol, out=None, **opts):
+        if out is None:
+            out = torch.empty(self.n_local, dtype=torch.float64, device=self.dev)
+        res = _lib.di_shard_finish(self.h, tol, out, **opts)
+        return out, res.as_dict()
+
+    def close(self):
+        if self.h:
+            _lib.di_graph_destroy(self.h)
+            self.h = None
+
+
+class TorchCollectives:
+    """torch.distributed collectives for a single local shard (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def plan(self, shards, bounds):
+        (s,) = shards
+        ids = s.ghost_ids.cpu().numpy().astype(np.int64)
+        owner = np.searchsorted(np.asarray(bounds), ids, side="right") - 1
+        send_counts = np.bincount(owner, minlength=self.world).astype(np.int64)
+        dev = s.send.device
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = rc.cpu().numpy()
+        recv_ids = torch.empty(int(recv_counts.sum()), dtype=torch.int32, device=dev)
+        self.dist.all_to_all_single(recv_ids, s.ghost_ids.to(dev), output_split_sizes=recv_counts.tolist(),
+                                    input_split_sizes=send_counts.tolist(), group=self.group)
+        s.send_counts = send_counts.tolist()
+        s.set_recv((recv_ids - s.lo).to(torch.int32), recv_counts.tolist())
+
+    def allreduce_stats(self, shards):
+        (s,) = shards
+        s.gstats.copy_(s.stats[:2])
+        self.dist.all_reduce(s.gstats[0:1], op=self.dist.ReduceOp.SUM, group=self.group)
+        self.dist.all_reduce(s.gstats[1:2], op=self.dist.ReduceOp.MAX, group=self.group)
+
+    def alltoall(self, shards):
+        (s,) = shards
+        if self.world == 1:
+            return
+        self.dist.all_to_all_single(s.recv[:sum(s.recv_counts)], s.send[:sum(s.send_counts)],
+                                    output_split_sizes=s.recv_counts, input_split_sizes=s.send_counts,
+                                    group=self.group)
+
+    def allreduce_sum(self, values, device):
+        t = torch.tensor(values, dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().tolist()
+
+    def allreduce_max(self, values, device):
+        t = torch.tensor(values, dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t.cpu().tolist()
+
+
+def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
+    """Cold sharded solve; returns (list of local H tensors, list of local result dicts).
+
+    Per sweep: sweep -> all-to-all(ghost fluid) -> apply -> reduce -> all-reduce
+    (sum |F|_1, max |F|) -> control.  The host polls `done` once per chunk."""
+    for s in shards:
+        s.begin(d, tol, **opts)
+    coll.allreduce_stats(shards)
+    for s in shards:
+        s.control()
+    chunk = 2
+    while True:
+        for _ in range(chunk):
+            for s in shards:
+                s.sweep()
+            coll.alltoall(shards)
+            for s in shards:
+                s.apply()
+                s.reduce()
+            coll.allreduce_stats(shards)
+            for s in shards:
+                s.control()
+        done = [s.poll() for s in shards]
+        if all(done):
+            break
+        if any(done):
+            raise RuntimeError("ranks disagree on convergence")
+        chunk = min(chunk * 2, max_chunk)
+    outs = [s.finish(tol, **opts) for s in shards]
+    return [o[0] for o in outs], [o[1] for o in outs]
+
+
+# ------------------------------------------------------------------ bench (torchrun)
+def bench_sharded(args, metric):
+    """bench.py --gpus N under torchrun: weak scaling, each rank owns the rows of
+    a configs[2]-shaped slice (50M nodes, ~1B edges per GPU)."""
+    import json
+    import os
+    import time
+
+    import torch.distributed as dist
+
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    base = synth.CONFIGS[args.config]
+    per = args.scale_n or base.n
+    spec = base.scaled(per * world)
+    tol = args.tol if args.tol is not None else spec.tol
+    bounds = node_ranges(spec.n, world)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    g = synth.generate(spec, lo, hi)
+    stream = torch.cuda.current_stream()
+    sh = CudaShard(spec.n, lo, hi, g.row_ptr, g.col, g.w, device=local, stream=stream)
+    coll = TorchCollectives()
+    coll.plan([sh], bounds)
+    kw = dict(theta=args.theta, variant={"auto": 0, "push": 1, "pull": 2}[args.variant])
+    for _ in range(args.warmup):
+        solve([sh], coll, d=spec.d, tol=tol, **kw)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.di_kernel_launches()
+    e0.record(stream)
+    res = []
+    for _ in range(args.steps):
+        _, r = solve([sh], coll, d=spec.d, tol=tol, **kw)
+        res.append(r[0])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.di_kernel_launches() - l0
+    ms_max = coll.allreduce_max([ms], stream.device)[0]
+    edges = coll.allreduce_sum([float(sum(r["diffused_edges"] for r in res))], stream.device)[0]
+    cross = coll.allreduce_sum([float(sh.n_ghost), float(g.m)], stream.device)
+    if rank == 0:
+        line = {"metric": metric, "value": edges / (ms_max / 1e3), "unit": "edges/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "time_to_tol_s": ms_max / args.steps / 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{spec.name} sharded, {per} nodes per GPU (weak scaling)", "n": spec.n,
+                           "m": int(cross[1]), "tol": tol, "theta": args.theta, "variant": args.variant,
+                           "ghost_slots_total": int(cross[0]), "sweeps_per_solve": res[-1]["sweeps"],
+                           "parallelism": f"node-range partition x{world}, NCCL all-to-all + all-reduce"},
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
+                "clocks": None}
+        print(json.dumps(line), flush=True)
+    sh.close()
+    dist.destroy_process_group()
+    return 0

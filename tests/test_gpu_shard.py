@@ -1,0 +1,129 @@
+"""GPU tests of the sharded path (libdit di_shard_* through paper_1501_06350_b200/dist.py).
+
+Only one GPU is available, so R ranks are emulated in one process: R shard
+handles on cuda:0 driven in lock step by the same dist.solve() protocol, with
+the all-to-all / all-reduce done by device copies (LockstepCollectives below,
+test infrastructure).  No kernel ever waits on another rank.  A world_size=1
+NCCL run checks the torch.distributed collectives themselves.
+"""
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import di, graph
+
+pytestmark = pytest.mark.gpu
+D = 0.85
+
+
+class LockstepCollectives:
+    """All ranks in one process: collectives as device copies (same stream)."""
+
+    def plan(self, shards, bounds):
+        world = len(shards)
+        per_send = []
+        for s in shards:
+            ids = s.ghost_ids.cpu().numpy().astype(np.int64)
+            owner = np.searchsorted(np.asarray(bounds), ids, side="right") - 1
+            s.send_counts = np.bincount(owner, minlength=world).astype(np.int64).tolist()
+            per_send.append((ids, owner))
+        self.soff = [np.concatenate([[0], np.cumsum(s.send_counts)]) for s in shards]
+        for r, s in enumerate(shards):
+            idx = [per_send[q][0][per_send[q][1] == r] - s.lo for q in range(world)]
+            s.set_recv(torch.tensor(np.concatenate(idx).astype(np.int32), device=s.dev),
+                       [len(x) for x in idx])
+        self.roff = [np.concatenate([[0], np.cumsum(s.recv_counts)]) for s in shards]
+
+    def allreduce_stats(self, shards):
+        tot = sum(s.stats[0] for s in shards)
+        mx = torch.stack([s.stats[1] for s in shards]).max()
+        for s in shards:
+            s.gstats[0] = tot
+            s.gstats[1] = mx
+
+    def alltoall(self, shards):
+        for r, s in enumerate(shards):
+            for q, sq in enumerate(shards):
+                c = sq.send_counts[r]
+                if c:
+                    a, b = int(self.roff[r][q]), int(self.soff[q][r])
+                    s.recv[a:a + c].copy_(sq.send[b:b + c])
+
+
+def _shards(spec, world):
+    from paper_1501_06350_b200.dist import CudaShard, node_ranges
+    bounds = node_ranges(spec.n, world)
+    out = []
+    for r in range(world):
+        g = synth.generate(spec, bounds[r], bounds[r + 1])
+        out.append(CudaShard(spec.n, bounds[r], bounds[r + 1], g.row_ptr, g.col, g.w,
+                             stream=torch.cuda.current_stream()))
+    return out, bounds
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1501_06350_b200  # noqa: F401
+    return True
+
+
+@pytest.mark.parametrize("world,variant", [(2, 0), (4, 1), (3, 2)])
+def test_lockstep_shards_match_oracle(gpu, world, variant):
+    from paper_1501_06350_b200 import dist
+    spec = synth.CONFIGS[1].scaled(200_000, seed=8, weighted=True)
+    shards, bounds = _shards(spec, world)
+    coll = LockstepCollectives()
+    coll.plan(shards, bounds)
+    Hs, res = dist.solve(shards, coll, d=D, tol=1e-12, variant=variant)
+    H = torch.cat(Hs).cpu().numpy()
+    g = synth.generate(spec)
+    ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12)
+    assert np.abs(H - ref.H).sum() <= 1e-9
+    assert len({r["sweeps"] for r in res}) == 1 and all(r["residual_l1"] <= 1e-12 for r in res)
+    assert sum(s.n_ghost for s in shards) > 0
+    for s in shards:
+        s.close()
+
+
+def test_lockstep_theta0_sweeps_elementwise(gpu):
+    from paper_1501_06350_b200 import dist
+    spec = synth.CONFIGS[0].scaled(5000, seed=4, weighted=True)
+    shards, bounds = _shards(spec, 2)
+    coll = LockstepCollectives()
+    coll.plan(shards, bounds)
+    Hs, res = dist.solve(shards, coll, d=D, tol=0.0, theta=0.0, max_sweeps=5)
+    g = synth.generate(spec)
+    cp, ri, pv = graph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    st = di.di_init(g.n, D)
+    r = di.sweep_run(g.n, cp, ri, pv, D, st.F, st.H, theta=0.0, tol=0, max_sweeps=5)
+    assert all(x["sweeps"] == 5 for x in res)
+    assert np.allclose(torch.cat(Hs).cpu().numpy(), r.H, rtol=1e-13, atol=1e-18)
+
+
+def test_nccl_world1(gpu):
+    import torch.distributed as tdist
+
+    from paper_1501_06350_b200 import dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                             device_id=torch.device("cuda", 0))
+    try:
+        spec = synth.CONFIGS[0].scaled(4000, seed=3)
+        shards, bounds = _shards(spec, 1)
+        coll = dist.TorchCollectives()
+        coll.plan(shards, bounds)
+        Hs, res = dist.solve(shards, coll, d=D, tol=1e-12)
+        g = synth.generate(spec)
+        ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12)
+        assert np.abs(Hs[0].cpu().numpy() - ref.H).sum() <= 1e-9
+        shards[0].close()
+    finally:
+        tdist.destroy_process_group()
