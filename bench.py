@@ -39,7 +39,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2)
-    p.add_argument("--variant", default="auto", choices=["auto", "push", "pull"])
+    p.add_argument("--variant", default="auto", choices=["auto", "push", "pull", "tiled"])
+    p.add_argument("--rounds", type=int, default=4, help="local rounds per sweep (variant tiled)")
     p.add_argument("--theta", type=float, default=1.0)
     p.add_argument("--tol", type=float, default=None)
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -201,7 +202,7 @@ def run_ours(args):
     row_ptr[:] = g.row_ptr
     stream = torch.cuda.current_stream()
     G = eng.DIGraph(g.n, row_ptr, g.col, g.w, stream=stream)
-    kw = dict(d=spec.d, tol=tol, theta=args.theta, variant=args.variant)
+    kw = dict(d=spec.d, tol=tol, theta=args.theta, variant=args.variant, local_rounds=args.rounds)
     out = torch.empty(g.n, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
         G.solve(out=out, **kw)
@@ -235,7 +236,7 @@ def run_ours(args):
     assert res["converged"], res
     # roofline of the dominant kernel (largest summed device time)
     peak, peak_kind = load_peaks()
-    kinds = ["select", "push", "pull", "reduce"]
+    kinds = ["select", "push", "pull", "reduce", "tile"]
     dom = max(kinds, key=lambda k: prof_tot.get(f"{k}_ms", 0.0))
     dom_ms = prof_tot[f"{dom}_ms"]
     dom_launch = max(1, prof_tot[f"{dom}_launches"])
@@ -261,7 +262,7 @@ def run_ours(args):
             a.record(stream)
             h = _lib.di_graph_create(g.n, row_ptr, g.col, g.w, device=0, stream=stream)
             r = _lib.di_solve(h, spec.d, None, tol, Hh, theta=args.theta,
-                              variant=eng.VARIANTS[args.variant])
+                              variant=eng.VARIANTS[args.variant], local_rounds=args.rounds)
             b.record(stream)
             torch.cuda.synchronize()
             _lib.di_graph_destroy(h)
@@ -282,7 +283,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "time_to_tol_s": total_ms / args.steps / 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(spec, args.config), "n": g.n, "m": g.m, "d": spec.d, "tol": tol,
-                       "theta": args.theta, "variant": args.variant, "weighted": spec.weighted,
+                       "theta": args.theta, "variant": args.variant, "local_rounds": args.rounds,
+                       "weighted": spec.weighted,
                        "sweeps_per_solve": sweeps[-1], "diffused_edges_per_solve": results[-1]["diffused_edges"],
                        "push_sweeps": res["push_sweeps"], "pull_sweeps": res["pull_sweeps"],
                        "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",

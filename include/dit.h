@@ -66,6 +66,11 @@ extern "C" {
 #define DI_VARIANT_AUTO 0         /* per sweep: pull when the frontier is dense, else push */
 #define DI_VARIANT_PUSH 1         /* push-scatter over the CSR with float64 atomic adds */
 #define DI_VARIANT_PULL 2         /* deterministic pull-gather over the transpose (CSC) */
+#define DI_VARIANT_TILED 3        /* tile-local schedule (R12): per node tile of 1024
+                                     ids, `local_rounds` diffusion rounds in shared memory over
+                                     the tile's internal edges, then one deterministic pull of
+                                     the diffused amounts over the remaining edges; every node
+                                     holding fluid diffuses (theta is not used) */
 
 typedef struct di_graph di_graph;  /* opaque: device CSR + derived arrays + DI state */
 
@@ -76,7 +81,9 @@ typedef struct {
     int32_t variant;     /* DI_VARIANT_*, default DI_VARIANT_AUTO */
     int32_t dangling;    /* DI_DANGLING_*, default DI_DANGLING_DROP */
     int64_t max_sweeps;  /* stop after this many sweeps even if |F|_1 > tol; <= 0: 10^7 */
-    double  pull_frac;   /* AUTO: use pull when frontier out-edges > pull_frac * m; default 0.5 */
+    double  pull_frac;   /* AUTO: use pull when frontier out-edges > pull_frac * m; default 0.25 */
+    int32_t local_rounds;/* TILED: diffusion rounds per tile per sweep (>= 1), default 4 */
+    int32_t reserved;
 } di_solve_opts;
 
 typedef struct {
@@ -189,6 +196,8 @@ typedef struct {
     double  select_bytes, push_bytes, pull_bytes, reduce_bytes;
     int64_t select_launches, push_launches, pull_launches, reduce_launches;
     int64_t sweeps;
+    double  tile_ms, tile_bytes;      /* TILED: the tile-local kernel (pull_* = remote pull) */
+    int64_t tile_launches;
 } di_profile;
 
 int di_profile_enable(di_graph *g, int32_t on);

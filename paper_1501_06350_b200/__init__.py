@@ -12,7 +12,7 @@ from ._lib import (DI_DANGLING_COMPLETE, DI_DANGLING_DROP, DI_MEM_DEVICE, DI_MEM
                    DIError, di_get_state, di_graph_create, di_graph_destroy, di_graph_info,
                    di_kernel_launches, di_last_error, di_resume, di_set_state, di_solve, di_update_edges)
 
-VARIANTS = {"auto": DI_VARIANT_AUTO, "push": DI_VARIANT_PUSH, "pull": DI_VARIANT_PULL}
+VARIANTS = {"auto": DI_VARIANT_AUTO, "push": DI_VARIANT_PUSH, "pull": DI_VARIANT_PULL, "tiled": _lib.DI_VARIANT_TILED}
 DANGLING = {"drop": DI_DANGLING_DROP, "complete": DI_DANGLING_COMPLETE}
 
 
@@ -39,17 +39,19 @@ class DIGraph:
         return out
 
     def solve(self, d=0.85, Z=None, tol=1e-12, out=None, theta=1.0, variant="auto", dangling="drop",
-              max_sweeps=0, pull_frac=0.5):
+              max_sweeps=0, pull_frac=0.25, local_rounds=4):
         out = self._out(out)
         res = di_solve(self.handle, d, Z, tol, out, theta=theta, variant=VARIANTS[variant],
-                       dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac)
+                       dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac,
+                       local_rounds=local_rounds)
         return out, res.as_dict()
 
     def resume(self, tol=1e-12, out=None, theta=1.0, variant="auto", dangling="drop", max_sweeps=0,
-               pull_frac=0.5):
+               pull_frac=0.25, local_rounds=4):
         out = self._out(out)
         res = di_resume(self.handle, tol, out, theta=theta, variant=VARIANTS[variant],
-                        dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac)
+                        dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac,
+                        local_rounds=local_rounds)
         return out, res.as_dict()
 
     def update_edges(self, add_src=None, add_dst=None, add_w=None, rem_src=None, rem_dst=None):

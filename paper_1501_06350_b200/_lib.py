@@ -27,7 +27,7 @@ DI_OK, DI_ERR_INVALID, DI_ERR_CUDA, DI_ERR_OOM, DI_ERR_EDGE_NOT_FOUND, DI_ERR_ST
 DI_MEM_HOST, DI_MEM_DEVICE = 0, 1
 DI_W_NONE, DI_W_F32, DI_W_F64 = 0, 1, 2
 DI_DANGLING_DROP, DI_DANGLING_COMPLETE = 0, 1
-DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL = 0, 1, 2
+DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL, DI_VARIANT_TILED = 0, 1, 2, 3
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",
@@ -38,7 +38,8 @@ class di_profile(ctypes.Structure):
     _fields_ = [(k, ctypes.c_double) for k in ("select_ms", "push_ms", "pull_ms", "reduce_ms", "select_bytes",
                                                "push_bytes", "pull_bytes", "reduce_bytes")] + \
                [(k, ctypes.c_int64) for k in ("select_launches", "push_launches", "pull_launches",
-                                              "reduce_launches", "sweeps")]
+                                              "reduce_launches", "sweeps")] + \
+               [("tile_ms", ctypes.c_double), ("tile_bytes", ctypes.c_double), ("tile_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -46,7 +47,8 @@ class di_profile(ctypes.Structure):
 
 class di_solve_opts(ctypes.Structure):
     _fields_ = [("theta", ctypes.c_double), ("variant", ctypes.c_int32), ("dangling", ctypes.c_int32),
-                ("max_sweeps", ctypes.c_int64), ("pull_frac", ctypes.c_double)]
+                ("max_sweeps", ctypes.c_int64), ("pull_frac", ctypes.c_double), ("local_rounds", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class di_result(ctypes.Structure):
@@ -166,9 +168,11 @@ def di_graph_info(h):
     return n.value, m.value, w.value
 
 
-def _opts(theta=1.0, variant=DI_VARIANT_AUTO, dangling=DI_DANGLING_DROP, max_sweeps=0, pull_frac=0.5):
+def _opts(theta=1.0, variant=DI_VARIANT_AUTO, dangling=DI_DANGLING_DROP, max_sweeps=0, pull_frac=0.25,
+          local_rounds=4):
     o = di_solve_opts_default()
     o.theta, o.variant, o.dangling, o.max_sweeps, o.pull_frac = theta, variant, dangling, max_sweeps, pull_frac
+    o.local_rounds = local_rounds
     return o
 
 

@@ -50,7 +50,8 @@ static di_solve_opts resolve(const di_solve_opts *o) {
     di_solve_opts_default(&r);
     if (o) r = *o;
     if (!(r.theta >= 0.0 && r.theta <= 1.0)) fail(DI_ERR_INVALID, "opts.theta must be in [0, 1]");
-    if (r.variant < DI_VARIANT_AUTO || r.variant > DI_VARIANT_PULL) fail(DI_ERR_INVALID, "opts.variant");
+    if (r.variant < DI_VARIANT_AUTO || r.variant > DI_VARIANT_TILED) fail(DI_ERR_INVALID, "opts.variant");
+    if (r.local_rounds < 1 || r.local_rounds > 1000) fail(DI_ERR_INVALID, "opts.local_rounds must be in [1, 1000]");
     if (r.dangling != DI_DANGLING_DROP && r.dangling != DI_DANGLING_COMPLETE) fail(DI_ERR_INVALID, "opts.dangling");
     if (!(r.pull_frac >= 0.0)) fail(DI_ERR_INVALID, "opts.pull_frac must be >= 0");
     return r;
@@ -76,7 +77,8 @@ void di_solve_opts_default(di_solve_opts *o) {
     o->variant = DI_VARIANT_AUTO;
     o->dangling = DI_DANGLING_DROP;
     o->max_sweeps = 10000000;
-    o->pull_frac = 0.5;
+    o->pull_frac = 0.25;
+    o->local_rounds = 4;
 }
 
 const char *di_last_error(void) { return t_err.c_str(); }

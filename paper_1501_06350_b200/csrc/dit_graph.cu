@@ -162,23 +162,8 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
 }
 
 static void free_transpose(DevGraph &g) {
-    cudaFree(g.t_ptr);
-    cudaFree(g.t_src);
-    cudaFree(g.t_w);
-    cudaFree(g.pieces);
-    cudaFree(g.fix);
-    cudaFree(g.pbuf);
-    cudaFree(g.tile_start);
-    g.tile_start = nullptr;
-    g.ntiles = 0;
-    g.t_ptr = nullptr;
-    g.t_src = nullptr;
-    g.t_w = nullptr;
-    g.pieces = nullptr;
-    g.fix = nullptr;
-    g.pbuf = nullptr;
-    g.npieces = g.nfix = 0;
-    g.has_t = false;
+    free_plan(g.t);
+    free_tiles(g.tl);
 }
 
 void free_graph(DevGraph &g) {

@@ -16,6 +16,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int64_t kSplit = 512;         // a frontier row is split into entries of <= kSplit edges
 constexpr int kSplitShift = 9;
 constexpr int kLenBits = 24;            // entry: begin (40 bits) | len (24 bits)
+constexpr int64_t kNodeTile = 1024;     // TILED: node ids per tile
+// ctrl->use_pull: which diffusion kernels run this sweep
+constexpr int kUsePush = 0, kUsePull = 1, kUseTiled = 2;
 
 // One record per sweep, written by the last block of k_reduce.
 struct SweepRec {
@@ -53,6 +56,38 @@ struct Ctrl {
     int pad;
 };
 
+// A CSC (targets -> in-edges, ascending source) and its pull work plan:
+// pieces of <= 64 in-edges that never cross a 2048-edge tile, split targets.
+struct PullPlan {
+    bool built = false;
+    int64_t nt = 0, m = 0;         // targets, edges
+    int64_t *ptr = nullptr;        // [nt+1]
+    int32_t *src = nullptr;        // [m] source row of each in-edge
+    void *w = nullptr;             // [m] raw weight (graph storage kind) or null
+    uint4 *pieces = nullptr;       // {begin<<24 | len, target, split}
+    int64_t npieces = 0;
+    int4 *fix = nullptr;           // split targets: {j, first piece lo, hi, count}
+    int64_t nfix = 0;
+    double *pbuf = nullptr;        // [npieces] partial sums of split targets
+    int64_t *tile_start = nullptr; // [ntiles+1] first piece of each 2048-edge tile
+    int64_t ntiles = 0;
+};
+
+// Tile-local schedule (R12): node tiles of kNodeTile ids; in-edges
+// whose source is in the target's tile are "local" (kept as u16 offsets),
+// the others form the remote CSC pulled once per sweep.
+struct TilePlan {
+    bool built = false;
+    int64_t ntile = 0;             // node tiles
+    int64_t *lptr = nullptr;       // [nt+1] local in-edges of target t
+    uint16_t *lsrc = nullptr;      // [mloc] source - tile base
+    void *lw = nullptr;            // [mloc] weight or null
+    int64_t mloc = 0;
+    int32_t *deg = nullptr;        // [n] out-degree (diffused-edge accounting)
+    PullPlan rem;                  // remote in-edges
+    int64_t max_tile_edges = 0;
+};
+
 // Per-node weight-scale storage and raw weights.
 struct DevGraph {
     int64_t n = 0, m = 0;          // rows (owned nodes) and edges
@@ -69,17 +104,9 @@ struct DevGraph {
     int w_kind = DI_W_NONE;        // storage: DI_W_NONE / DI_W_F32 / DI_W_F64
     double *inv = nullptr;         // [n] 1/sum_k w_{j,k} (0: dangling)
     // transpose (built lazily for the pull variant)
-    bool has_t = false;
-    int64_t *t_ptr = nullptr;      // [n+1]
-    int32_t *t_src = nullptr;      // [m] source of each in-edge
-    void *t_w = nullptr;           // [m] weight (same storage kind as w)
-    uint4 *pieces = nullptr;       // pull work list: target pieces of <= kPullSplit in-edges
-    int64_t npieces = 0;
-    int4 *fix = nullptr;           // targets cut into several pieces: {j, first piece (lo, hi), count}
-    int64_t nfix = 0;
-    double *pbuf = nullptr;        // [npieces] partial sums of split targets
-    int64_t *tile_start = nullptr; // [ntiles+1] first piece of each pull tile
-    int64_t ntiles = 0;
+    PullPlan t;
+    // tile-local schedule (built lazily for DI_VARIANT_TILED)
+    TilePlan tl;
 };
 
 struct State {
@@ -89,6 +116,8 @@ struct State {
     std::vector<cudaEvent_t> events;     // profiling: 5 per sweep
     di_profile last_prof{};
     int64_t launched = 0;                // sweeps enqueued in the current call
+    int rounds = 4;                      // TILED local rounds of the current call
+    bool tiled_call = false;
     int64_t last_sweeps = 0;
     double d = 0.85;
     double *F = nullptr, *H = nullptr;   // [n]
@@ -137,6 +166,12 @@ void launch_reduce(di_graph *h, int is_init);
 void launch_select(di_graph *h, bool pull);
 void launch_push(di_graph *h);
 void launch_pull(di_graph *h);
+void launch_pull_plan(di_graph *h, const PullPlan &p, const double *A, int want);
+void build_plan_pieces(di_graph *h, PullPlan &p);
+void free_plan(PullPlan &p);
+void build_tiles(di_graph *h);
+void free_tiles(TilePlan &t);
+void launch_tile_local(di_graph *h, int rounds);
 bool poll_done(di_graph *h);
 void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res);
 void init_state(di_graph *h, double d, const double *Z_dev);

@@ -187,17 +187,71 @@ static void radix_sort_pass_launch(const uint32_t *k, const void *v, uint32_t *o
     DI_CUDA(cudaGetLastError());
 }
 
+// Work plan of a CSC (pieces, tiles, split-target fixups) for k_pull.
+void build_plan_pieces(di_graph *h, PullPlan &pd) {
+    cudaStream_t st = h->stream;
+    const int64_t nt = pd.nt, m = pd.m;
+    int64_t *pc, *po;
+    DI_CUDA(cudaMallocAsync(&pc, (nt + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&po, (nt + 1) * sizeof(int64_t), st));
+    const int grid = h->num_sms * 8;
+    if (nt > 0) {
+        k_piece_count<<<grid, kThreads, 0, st>>>(pd.ptr, nt, pc);
+        count_launch();
+    }
+    exclusive_scan_i64(pc, po, nt, st);
+    int64_t np = 0;
+    DI_CUDA(cudaMemcpyAsync(&np, po + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    pd.npieces = np;
+    DI_CUDA(cudaMalloc(&pd.pieces, (np > 0 ? np : 1) * sizeof(uint4)));
+    DI_CUDA(cudaMalloc(&pd.pbuf, (np > 0 ? np : 1) * sizeof(double)));
+    DI_CUDA(cudaMalloc(&pd.fix, (nt > 0 ? nt : 1) * sizeof(int4)));
+    pd.ntiles = (m + kPullTile - 1) / kPullTile;
+    DI_CUDA(cudaMalloc(&pd.tile_start, (pd.ntiles + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMemcpyAsync(pd.tile_start + pd.ntiles, &pd.npieces, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    unsigned long long *nf;
+    DI_CUDA(cudaMallocAsync(&nf, sizeof(unsigned long long), st));
+    DI_CUDA(cudaMemsetAsync(nf, 0, sizeof(unsigned long long), st));
+    if (nt > 0) {
+        k_piece_write<<<grid, kThreads, 0, st>>>(pd.ptr, nt, po, pd.pieces, pd.fix, nf, pd.tile_start);
+        count_launch();
+    }
+    unsigned long long nfix = 0;
+    DI_CUDA(cudaMemcpyAsync(&nfix, nf, sizeof(nfix), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaFreeAsync(nf, st));
+    DI_CUDA(cudaFreeAsync(pc, st));
+    DI_CUDA(cudaFreeAsync(po, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    pd.nfix = (int64_t)nfix;
+    pd.built = true;
+}
+
+void free_plan(PullPlan &p) {
+    cudaFree(p.ptr);
+    cudaFree(p.src);
+    cudaFree(p.w);
+    cudaFree(p.pieces);
+    cudaFree(p.fix);
+    cudaFree(p.pbuf);
+    cudaFree(p.tile_start);
+    p = PullPlan();
+}
+
 void build_transpose(di_graph *h) {
     DevGraph &g = h->g;
-    if (g.has_t) return;
+    PullPlan &T = g.t;
+    if (T.built) return;
     cudaStream_t st = h->stream;
     const int64_t n = g.n, m = g.m, nt = g.nt;   // rows = owned sources, targets = fluid slots
+    T.nt = nt;
+    T.m = m;
     const bool wide = m >= (int64_t)0xffffffffLL;
     const size_t vsz = wide ? 8 : 4;
-    DI_CUDA(cudaMalloc(&g.t_ptr, (nt + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMalloc(&g.t_src, (m > 0 ? m : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMalloc(&T.ptr, (nt + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMalloc(&T.src, (m > 0 ? m : 1) * sizeof(int32_t)));
     const size_t wsz = g.w_kind == DI_W_F32 ? 4 : (g.w_kind == DI_W_F64 ? 8 : 0);
-    if (wsz) DI_CUDA(cudaMalloc(&g.t_w, (m > 0 ? m : 1) * wsz));
+    if (wsz) DI_CUDA(cudaMalloc(&T.w, (m > 0 ? m : 1) * wsz));
     int64_t *cnt = nullptr;
     DI_CUDA(cudaMallocAsync(&cnt, (nt + 1) * sizeof(int64_t), st));
     DI_CUDA(cudaMemsetAsync(cnt, 0, (nt + 1) * sizeof(int64_t), st));
@@ -225,7 +279,7 @@ void build_transpose(di_graph *h) {
         }
         DI_CUDA(cudaFreeAsync(hc, st));
         DI_CUDA(cudaFreeAsync(ho, st));
-        // in-degrees -> t_ptr
+        // in-degrees -> ptr
         k_run_bounds<<<grid, kThreads, 0, st>>>(k0, m, cnt);
         count_launch();
         DI_CUDA(cudaMallocAsync(&esrc, m * 4, st));
@@ -233,14 +287,14 @@ void build_transpose(di_graph *h) {
         count_launch();
         if (wide) {
             if (g.w_kind == DI_W_F64)
-                k_gather_t<uint64_t, double><<<grid, kThreads, 0, st>>>((const uint64_t *)v0, m, esrc, (const double *)g.w, g.t_src, (double *)g.t_w);
+                k_gather_t<uint64_t, double><<<grid, kThreads, 0, st>>>((const uint64_t *)v0, m, esrc, (const double *)g.w, T.src, (double *)T.w);
             else
-                k_gather_t<uint64_t, float><<<grid, kThreads, 0, st>>>((const uint64_t *)v0, m, esrc, (const float *)g.w, g.t_src, (float *)g.t_w);
+                k_gather_t<uint64_t, float><<<grid, kThreads, 0, st>>>((const uint64_t *)v0, m, esrc, (const float *)g.w, T.src, (float *)T.w);
         } else {
             if (g.w_kind == DI_W_F64)
-                k_gather_t<uint32_t, double><<<grid, kThreads, 0, st>>>((const uint32_t *)v0, m, esrc, (const double *)g.w, g.t_src, (double *)g.t_w);
+                k_gather_t<uint32_t, double><<<grid, kThreads, 0, st>>>((const uint32_t *)v0, m, esrc, (const double *)g.w, T.src, (double *)T.w);
             else
-                k_gather_t<uint32_t, float><<<grid, kThreads, 0, st>>>((const uint32_t *)v0, m, esrc, (const float *)g.w, g.t_src, (float *)g.t_w);
+                k_gather_t<uint32_t, float><<<grid, kThreads, 0, st>>>((const uint32_t *)v0, m, esrc, (const float *)g.w, T.src, (float *)T.w);
         }
         count_launch();
         DI_CUDA(cudaFreeAsync(esrc, st));
@@ -249,44 +303,9 @@ void build_transpose(di_graph *h) {
         DI_CUDA(cudaFreeAsync(v0, st));
         DI_CUDA(cudaFreeAsync(v1, st));
     }
-    exclusive_scan_i64(cnt, g.t_ptr, nt, st);
-    // pieces
-    DevGraph &pd = g;
-    int64_t *pc, *po;
-    DI_CUDA(cudaMallocAsync(&pc, (nt + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMallocAsync(&po, (nt + 1) * sizeof(int64_t), st));
-    const int grid = h->num_sms * 8;
-    if (nt > 0) {
-        k_piece_count<<<grid, kThreads, 0, st>>>(g.t_ptr, nt, pc);
-        count_launch();
-    }
-    exclusive_scan_i64(pc, po, nt, st);
-    int64_t np = 0;
-    DI_CUDA(cudaMemcpyAsync(&np, po + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    DI_CUDA(cudaStreamSynchronize(st));
-    pd.npieces = np;
-    DI_CUDA(cudaMalloc(&pd.pieces, (np > 0 ? np : 1) * sizeof(uint4)));
-    DI_CUDA(cudaMalloc(&pd.pbuf, (np > 0 ? np : 1) * sizeof(double)));
-    DI_CUDA(cudaMalloc(&pd.fix, (nt > 0 ? nt : 1) * sizeof(int4)));
-    pd.ntiles = (m + kPullTile - 1) / kPullTile;
-    DI_CUDA(cudaMalloc(&pd.tile_start, (pd.ntiles + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMemcpyAsync(pd.tile_start + pd.ntiles, &pd.npieces, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    unsigned long long *nf;
-    DI_CUDA(cudaMallocAsync(&nf, sizeof(unsigned long long), st));
-    DI_CUDA(cudaMemsetAsync(nf, 0, sizeof(unsigned long long), st));
-    if (nt > 0) {
-        k_piece_write<<<grid, kThreads, 0, st>>>(g.t_ptr, nt, po, pd.pieces, pd.fix, nf, pd.tile_start);
-        count_launch();
-    }
-    unsigned long long nfix = 0;
-    DI_CUDA(cudaMemcpyAsync(&nfix, nf, sizeof(nfix), cudaMemcpyDeviceToHost, st));
-    DI_CUDA(cudaFreeAsync(nf, st));
-    DI_CUDA(cudaFreeAsync(pc, st));
-    DI_CUDA(cudaFreeAsync(po, st));
+    exclusive_scan_i64(cnt, T.ptr, nt, st);
     DI_CUDA(cudaFreeAsync(cnt, st));
-    DI_CUDA(cudaStreamSynchronize(st));
-    pd.nfix = (int64_t)nfix;
-    g.has_t = true;
+    build_plan_pieces(h, T);
 }
 
 // ---------------------------------------------------------------- pull sweep
@@ -301,9 +320,10 @@ __global__ void __launch_bounds__(kThreads) k_pull(const int32_t *__restrict__ t
                                                    const double *__restrict__ A, double *__restrict__ F,
                                                    const uint4 *__restrict__ pieces,
                                                    const int64_t *__restrict__ tile_start, int64_t ntiles, int64_t m,
-                                                   double *__restrict__ pbuf, const Ctrl *__restrict__ ctrl) {
+                                                   double *__restrict__ pbuf, const Ctrl *__restrict__ ctrl,
+                                                   int want) {
     __shared__ double vals[kPullTile];
-    if (ctrl->done || !ctrl->use_pull) return;
+    if (ctrl->done || ctrl->use_pull != want) return;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t e0 = t * kPullTile;
         const int cnt = (int)min((int64_t)kPullTile, m - e0);
@@ -335,8 +355,8 @@ __global__ void __launch_bounds__(kThreads) k_pull(const int32_t *__restrict__ t
 // others by the whole warp (lane-strided, then a fixed butterfly).  Every sum
 // has a fixed order: deterministic.
 __global__ void k_pull_fix(const int4 *__restrict__ fix, int64_t nfix, const double *__restrict__ pbuf,
-                           double *__restrict__ F, const Ctrl *__restrict__ ctrl) {
-    if (ctrl->done || !ctrl->use_pull) return;
+                           double *__restrict__ F, const Ctrl *__restrict__ ctrl, int want) {
+    if (ctrl->done || ctrl->use_pull != want) return;
     const unsigned lane = lane_id();
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -365,33 +385,33 @@ __global__ void k_pull_fix(const int4 *__restrict__ fix, int64_t nfix, const dou
     }
 }
 
-void launch_pull(di_graph *h) {
+void launch_pull_plan(di_graph *h, const PullPlan &pd, const double *A, int want) {
     DevGraph &g = h->g;
     State &s = h->s;
-    DevGraph &pd = g;
-    const int grid = h->num_sms * 8;
     if (pd.ntiles > 0) {
         const unsigned grid = (unsigned)std::min<int64_t>(pd.ntiles, (int64_t)h->num_sms * 8);
         switch (g.w_kind) {
         case DI_W_F32:
-            k_pull<float><<<grid, kThreads, 0, h->stream>>>(g.t_src, (const float *)g.t_w, s.A, s.F, pd.pieces,
-                                                             pd.tile_start, pd.ntiles, g.m, pd.pbuf, s.ctrl);
+            k_pull<float><<<grid, kThreads, 0, h->stream>>>(pd.src, (const float *)pd.w, A, s.F, pd.pieces,
+                                                             pd.tile_start, pd.ntiles, pd.m, pd.pbuf, s.ctrl, want);
             break;
         case DI_W_F64:
-            k_pull<double><<<grid, kThreads, 0, h->stream>>>(g.t_src, (const double *)g.t_w, s.A, s.F, pd.pieces,
-                                                              pd.tile_start, pd.ntiles, g.m, pd.pbuf, s.ctrl);
+            k_pull<double><<<grid, kThreads, 0, h->stream>>>(pd.src, (const double *)pd.w, A, s.F, pd.pieces,
+                                                              pd.tile_start, pd.ntiles, pd.m, pd.pbuf, s.ctrl, want);
             break;
         default:
-            k_pull<NoW><<<grid, kThreads, 0, h->stream>>>(g.t_src, nullptr, s.A, s.F, pd.pieces, pd.tile_start,
-                                                           pd.ntiles, g.m, pd.pbuf, s.ctrl);
+            k_pull<NoW><<<grid, kThreads, 0, h->stream>>>(pd.src, nullptr, A, s.F, pd.pieces, pd.tile_start,
+                                                           pd.ntiles, pd.m, pd.pbuf, s.ctrl, want);
         }
         count_launch();
     }
     if (pd.nfix > 0) {
         k_pull_fix<<<(unsigned)std::min<int64_t>((pd.nfix + 255) / 256, (int64_t)h->num_sms * 8), 256, 0, h->stream>>>(
-            pd.fix, pd.nfix, pd.pbuf, s.F, s.ctrl);
+            pd.fix, pd.nfix, pd.pbuf, s.F, s.ctrl, want);
         count_launch();
     }
 }
+
+void launch_pull(di_graph *h) { launch_pull_plan(h, h->g.t, h->s.A, kUsePull); }
 
 }  // namespace dit

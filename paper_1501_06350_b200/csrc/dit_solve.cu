@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) k_select(const int64_t *__restrict__
     __shared__ double s_leak[kWarps];
     __shared__ unsigned long long s_cnt[kWarps][2];
     if (ctrl->done) return;
-    if (kPull != (ctrl->use_pull != 0)) return;
+    if (ctrl->use_pull != (kPull ? kUsePull : kUsePush)) return;
     const double T = ctrl->T, d = ctrl->d;
     const unsigned lane = lane_id();
     double leak = 0.0;
@@ -125,7 +125,7 @@ template <typename W>
 __global__ void __launch_bounds__(kThreads) k_push(const int32_t *__restrict__ col, const W *__restrict__ w,
                                                    double *__restrict__ F, const uint4 *__restrict__ ent,
                                                    const Ctrl *__restrict__ ctrl) {
-    if (ctrl->done || ctrl->use_pull) return;
+    if (ctrl->done || ctrl->use_pull != kUsePush) return;
     const unsigned long long N = ctrl->n_entries;
     const unsigned lane = lane_id();
     const unsigned long long warp = ((unsigned long long)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -180,9 +180,10 @@ __device__ void finalize_control(Ctrl *ctrl, double r, double fm, int is_init, i
     // as the estimate of the next one's (the first sweep from a uniform F_0
     // takes every node)
     const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->last_sel_edges;
-    if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = 1;
-    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = 0;
-    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? 1 : 0;
+    if (ctrl->variant == DI_VARIANT_TILED) ctrl->use_pull = kUseTiled;
+    else if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = kUsePull;
+    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = kUsePush;
+    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? kUsePull : kUsePush;
 }
 
 __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ F, int64_t n, int64_t m,
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
         }
         ctrl->sweeps += 1;
         ctrl->diffused_edges += ctrl->sel_edges;
-        if (ctrl->use_pull) ctrl->pull_sweeps += 1; else ctrl->push_sweeps += 1;
+        if (ctrl->use_pull == kUsePush) ctrl->push_sweeps += 1; else ctrl->pull_sweeps += 1;
         ctrl->last_sel_edges = ctrl->sel_edges;
     }
     ctrl->n_entries = 0;
@@ -412,12 +413,26 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
         const SweepRec &rc = hs[k];
         const double nodes = (double)(rc.nodes_cum - prev_nodes);
         prev_nodes = rc.nodes_cum;
+        if (rc.use_pull == kUseTiled) {
+            // tile kernel: F, inv, deg, lptr read + F, H, A written per node, local
+            // edges (u16 source + weight) read once; remote pull over the remote CSC
+            p.tile_ms += t[0];
+            p.tile_bytes += 52.0 * n + (double)g.tl.mloc * (2.0 + wb);
+            p.tile_launches += 1;
+            p.pull_ms += t[2];
+            p.pull_bytes += 32.0 * (double)g.tl.rem.npieces + (double)g.tl.rem.m * (12.0 + wb);
+            p.pull_launches += 1;
+            p.reduce_ms += t[3];
+            p.reduce_bytes += 8.0 * n;
+            p.reduce_launches += 1;
+            continue;
+        }
         p.select_ms += t[0];
         p.select_bytes += 8.0 * n + 48.0 * nodes + (rc.use_pull ? 8.0 * n : 16.0 * (double)rc.entries);
         p.select_launches += 1;
         if (rc.use_pull) {
             p.pull_ms += t[2];
-            p.pull_bytes += 32.0 * (double)g.npieces + m * (12.0 + wb);
+            p.pull_bytes += 32.0 * (double)g.t.npieces + m * (12.0 + wb);
             p.pull_launches += 1;
         } else {
             p.push_ms += t[1];
@@ -436,11 +451,13 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
 void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats_out) {
     State &s = h->s;
     DevGraph &g = h->g;
-    const bool want_pull = o.variant == DI_VARIANT_PULL || o.variant == DI_VARIANT_AUTO;
+    const bool want_pull = o.variant != DI_VARIANT_PUSH;
     if (want_pull && g.n > 0) {
         build_transpose(h);
+        if (o.variant == DI_VARIANT_TILED) build_tiles(h);
         if (!s.A) DI_CUDA(cudaMalloc(&s.A, g.n * sizeof(double)));
     }
+    s.rounds = o.local_rounds > 0 ? o.local_rounds : 4;
     DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     DI_CUDA(cudaStreamSynchronize(h->stream));
     Ctrl c = *s.ctrl_host;
@@ -451,7 +468,8 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     c.theta = o.theta;
     c.tol = tol;
     c.max_sweeps = (unsigned long long)(o.max_sweeps > 0 ? o.max_sweeps : 10000000LL);
-    c.variant = g.has_t ? o.variant : DI_VARIANT_PUSH;
+    c.variant = g.t.built ? o.variant : DI_VARIANT_PUSH;
+    if (o.variant == DI_VARIANT_TILED && !g.tl.built) c.variant = DI_VARIANT_PUSH;
     c.pull_edges = o.pull_frac * (double)g.m;
     c.hist = s.hist;
     c.n_global = (double)(g.n_global > 0 ? g.n_global : 1);
@@ -459,6 +477,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     *s.ctrl_host = c;
     DI_CUDA(cudaMemcpyAsync(s.ctrl, s.ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     s.launched = 0;
+    s.tiled_call = c.variant == DI_VARIANT_TILED;
 }
 
 void mark_event(di_graph *h, int64_t sweep, int k) {
@@ -478,12 +497,20 @@ void launch_sweep(di_graph *h) {
     State &s = h->s;
     const int64_t k = s.launched;
     mark_event(h, k, 0);
+    if (s.tiled_call) {
+        launch_tile_local(h, s.rounds);              // select + local rounds ("select" slot)
+        mark_event(h, k, 1);
+        mark_event(h, k, 2);
+        launch_pull_plan(h, h->g.tl.rem, s.A, kUseTiled);
+        mark_event(h, k, 3);
+        return;
+    }
     launch_select(h, false);
-    if (h->g.has_t) launch_select(h, true);
+    if (h->g.t.built) launch_select(h, true);
     mark_event(h, k, 1);
     launch_push(h);
     mark_event(h, k, 2);
-    if (h->g.has_t) launch_pull(h);
+    if (h->g.t.built) launch_pull(h);
     mark_event(h, k, 3);
 }
 

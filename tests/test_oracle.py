@@ -340,3 +340,46 @@ def test_apply_delta_rejects_absent_edge_and_roundtrips():
     assert list(rp2) == [0, 1, 2, 2] and list(c2) == [2, 2] and list(ch) == [0]
     rp3, c3, _, _ = graph.apply_delta(3, rp2, c2, None, [0], [1], None, [0], [2])
     assert list(rp3) == list(rp) and list(c3) == list(c)
+
+
+# ------------------------------------------------- tile-local sweeps (R12)
+def test_tiled_sweep_chain_exact_in_one_sweep():
+    # 3-chain inside one tile, 3 local rounds: D = (0.05, 0.05+0.0425, 0.05+0.0425+0.036125)
+    ch = load("chain3.txt")
+    rp, c, _ = csr_from_edges(3, ch["edges"])
+    cp, ri, pv = graph.column_entries(3, rp, c)
+    st = di.di_init(3, ch["d"])
+    r = di.tiled_sweep_run(3, cp, ri, pv, ch["d"], st.F, st.H, tile=4, rounds=3, tol=0, max_sweeps=1)
+    assert np.allclose(r.H, ch["x"], rtol=0, atol=1e-17) and np.all(r.F == 0)
+    assert r.leak == pytest.approx(ch["leak"], abs=1e-17)
+
+
+def test_tiled_one_round_equals_theta0_sweep():
+    g = small_graph(300, 12, weighted=True)
+    cp, ri, pv = cols_of(g)
+    st = di.di_init(g.n, D)
+    for k in (1, 3, 8):
+        a = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=32, rounds=1, tol=0, max_sweeps=k)
+        b = di.sweep_run(g.n, cp, ri, pv, D, st.F, st.H, theta=0.0, tol=0, max_sweeps=k)
+        assert np.allclose(a.H, b.H, rtol=1e-14, atol=0) and np.allclose(a.F, b.F, rtol=1e-13, atol=1e-20)
+        assert a.edges == b.edges and a.nodes == b.nodes
+
+
+@pytest.mark.parametrize("tile,rounds", [(16, 2), (64, 5), (1024, 3)])
+def test_tiled_conservation_and_convergence(tile, rounds):
+    g = small_graph(200, 13)
+    cp, ri, pv = cols_of(g)
+    P = graph.dense_P(g.n, cp, ri, pv)
+    st = di.di_init(g.n, D)
+    F, H, lk = st.F, st.H, 0.0
+    for _ in range(6):
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, F, H, tile=tile, rounds=rounds, tol=0, max_sweeps=1, leak=lk)
+        F, H, lk = r.F, r.H, r.leak
+        assert np.abs(H + F - st.F0 - D * (P @ H)).max() <= 1e-15           # Eq. (12)
+        assert lk == pytest.approx(H[graph.dangling_mask(g.n, g.row_ptr)].sum(), abs=1e-15)
+    x = dense.dense_solve(P, D, synth.uniform_Z(g.n))
+    r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=rounds, tol=1e-13)
+    assert np.abs(r.H - x).sum() <= 1e-12
+    # more local rounds never need more sweeps than one round
+    r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13)
+    assert r.steps <= r1.steps
