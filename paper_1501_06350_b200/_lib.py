@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libdit.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"libdit.so not found at {LIB_PATH}: build the CUDA engine first "
-        "(python -m paper_1501_06350_b200.build or __graft_entry__.build()). "
+        "(python paper_1501_06350_b200/build.py or __graft_entry__.build()). "
         "There is no CPU fallback.")
 
 _lib = ctypes.CDLL(LIB_PATH)

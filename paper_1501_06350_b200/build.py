@@ -1,6 +1,6 @@
 """Build libdit.so (the C-ABI engine) in-tree for sm_100a with nvcc.
 
-    python -m paper_1501_06350_b200.build [--force] [--verbose]
+    python paper_1501_06350_b200/build.py [--force] [--verbose]
 
 Object files go to paper_1501_06350_b200/build/, the shared library to
 paper_1501_06350_b200/libdit.so (both git-ignored; the .so travels to the GPU
