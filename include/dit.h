@@ -66,11 +66,13 @@ extern "C" {
 #define DI_VARIANT_AUTO 0         /* per sweep: pull when the frontier is dense, else push */
 #define DI_VARIANT_PUSH 1         /* push-scatter over the CSR with float64 atomic adds */
 #define DI_VARIANT_PULL 2         /* deterministic pull-gather over the transpose (CSC) */
-#define DI_VARIANT_TILED 3        /* tile-local schedule (R12): per node tile of 1024
-                                     ids, `local_rounds` diffusion rounds in shared memory over
-                                     the tile's internal edges, then one deterministic pull of
-                                     the diffused amounts over the remaining edges; every node
-                                     holding fluid diffuses (theta is not used) */
+#define DI_VARIANT_TILED 3        /* tile-local schedule (R12): per node tile of
+                                     DI_TILE_NODES ids, `local_rounds` diffusion rounds in shared
+                                     memory over the tile's internal edges; the pushes along the
+                                     other edges are gathered by their targets at the start of
+                                     the next sweep (deterministic); every node holding fluid
+                                     diffuses (theta is not used).  Not available on shards. */
+#define DI_TILE_NODES 512         /* node ids per tile of DI_VARIANT_TILED */
 
 typedef struct di_graph di_graph;  /* opaque: device CSR + derived arrays + DI state */
 

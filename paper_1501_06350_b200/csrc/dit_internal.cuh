@@ -16,7 +16,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int64_t kSplit = 512;         // a frontier row is split into entries of <= kSplit edges
 constexpr int kSplitShift = 9;
 constexpr int kLenBits = 24;            // entry: begin (40 bits) | len (24 bits)
-constexpr int64_t kNodeTile = 1024;     // TILED: node ids per tile
+constexpr int64_t kNodeTile = 512;      // TILED: node ids per tile (= DI_TILE_NODES)
 // ctrl->use_pull: which diffusion kernels run this sweep
 constexpr int kUsePush = 0, kUsePull = 1, kUseTiled = 2;
 
@@ -53,7 +53,7 @@ struct Ctrl {
     unsigned int red_blocks;
     int variant;                        // DI_VARIANT_* requested
     int use_pull;                       // decision for the current sweep
-    int pad;
+    int gather;                         // TILED: remote pushes of the last sweep are pending in A
 };
 
 // A CSC (targets -> in-edges, ascending source) and its pull work plan:
@@ -73,19 +73,44 @@ struct PullPlan {
     int64_t ntiles = 0;
 };
 
-// Tile-local schedule (R12): node tiles of kNodeTile ids; in-edges
-// whose source is in the target's tile are "local" (kept as u16 offsets),
-// the others form the remote CSC pulled once per sweep.
+// Tile-local schedule (R12, §5): node tiles of kNodeTile ids.  An
+// in-edge is LOCAL when its source is in the target's tile (u16 tile-relative
+// source), otherwise REMOTE.  Remote in-edges of "light" targets sit per tile
+// in a {source, weight} record array that the tile kernel stages with TMA and
+// gathers itself; "heavy" targets (many remote in-edges, or tiles whose light
+// records would overflow kLightCap) are gathered by k_heavy over fixed chunks
+// of the heavy edge array (segments = target ∩ chunk), deterministic.
+constexpr int64_t kLightCap = 2048;     // light remote records per tile (shared memory)
+constexpr int64_t kHeavyTh = 16;        // remote in-degree above which a target is heavy
+constexpr int64_t kHeavyChunk = 2048;   // heavy edges per k_heavy chunk
+
 struct TilePlan {
     bool built = false;
     int64_t ntile = 0;             // node tiles
-    int64_t *lptr = nullptr;       // [nt+1] local in-edges of target t
+    // per node [n]
+    uint32_t *lrel = nullptr;      // local in-edge start, relative to ltile[tile]
+    uint32_t *rrel = nullptr;      // light remote in-edge start, relative to rtile[tile]
+    int32_t *hidx = nullptr;       // heavy index of the target or -1
+    float *wr = nullptr;           // share of node i's outflow that leaves its tile: sum_remote w * inv
+    int32_t *deg = nullptr;        // out-degree (diffused-edge accounting)
+    // per tile [ntile+1]
+    int64_t *ltile = nullptr, *rtile = nullptr;
+    // local in-edges (CSC order, padded by 16 B for aligned TMA supersets)
     uint16_t *lsrc = nullptr;      // [mloc] source - tile base
-    void *lw = nullptr;            // [mloc] weight or null
+    void *lw = nullptr;            // [mloc] raw weight (graph storage kind) or null
     int64_t mloc = 0;
-    int32_t *deg = nullptr;        // [n] out-degree (diffused-edge accounting)
-    PullPlan rem;                  // remote in-edges
-    int64_t max_tile_edges = 0;
+    // light remote records {int32 src, weight} (8 B for f32/unweighted, 16 B for f64)
+    void *rrec = nullptr;
+    int64_t mlight = 0;
+    // heavy targets
+    int64_t nh = 0, mh = 0, nseg = 0, nchunk = 0;
+    void *hrec = nullptr;          // [mh] records, by heavy target then source
+    int64_t *seg_start = nullptr;  // [nseg+1] first heavy edge of each segment
+    int64_t *cfirst = nullptr;     // [nchunk+1] first segment of each chunk
+    int64_t *hfirst = nullptr;     // [nh+1] first segment of each heavy target
+    double *part = nullptr;        // [nseg] segment partial sums
+    double *hsum = nullptr;        // [nh] remote inflow of each heavy target
+    int64_t max_tile_edges = 0;    // most local in-edges of one tile
 };
 
 // Per-node weight-scale storage and raw weights.
@@ -122,6 +147,7 @@ struct State {
     double d = 0.85;
     double *F = nullptr, *H = nullptr;   // [n]
     double *A = nullptr;                 // [n] pull: outflow amount per node
+    double *A2 = nullptr;                // [n] TILED: second outflow buffer (ping-pong by sweep parity)
     uint4 *ent = nullptr;                // frontier entries (16 B each)
     int64_t ent_cap = 0;
     Ctrl *ctrl = nullptr;                // device
@@ -171,7 +197,10 @@ void build_plan_pieces(di_graph *h, PullPlan &p);
 void free_plan(PullPlan &p);
 void build_tiles(di_graph *h);
 void free_tiles(TilePlan &t);
-void launch_tile_local(di_graph *h, int rounds);
+void launch_tile_sweep(di_graph *h, int rounds);
+void launch_tile_flush(di_graph *h);
+void launch_reduce_exact(di_graph *h);
+void mark_event(di_graph *h, int64_t sweep, int k);
 bool poll_done(di_graph *h);
 void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res);
 void init_state(di_graph *h, double d, const double *Z_dev);
@@ -248,5 +277,41 @@ template <>
 __device__ __forceinline__ double load_w<double>(const double *w, int64_t e) { return ld_stream_f64(w + e); }
 
 struct NoW {};
+
+// Next-sweep control from the (global) residual r and max fluid fm.
+__device__ __forceinline__ void finalize_control(Ctrl *ctrl, double r, double fm, int is_init, int64_t m) {
+    ctrl->resid = r;
+    ctrl->fmax = fm;
+    const double T = ctrl->theta * r / ctrl->n_global;
+    ctrl->T = T < fm ? T : fm;
+    ctrl->done = (r <= ctrl->tol || ctrl->sweeps >= ctrl->max_sweeps) ? 1u : 0u;
+    // direction of the next sweep: AUTO takes this sweep's frontier out-edges
+    // as the estimate of the next one's (the first sweep from a uniform F_0
+    // takes every node)
+    const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->last_sel_edges;
+    if (ctrl->variant == DI_VARIANT_TILED) ctrl->use_pull = kUseTiled;
+    else if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = kUsePull;
+    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = kUsePush;
+    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? kUsePull : kUsePush;
+}
+
+// End-of-sweep bookkeeping (last block of the sweep's final kernel): leak,
+// per-sweep record, counters, per-sweep accumulators reset.
+__device__ __forceinline__ void end_sweep(Ctrl *ctrl, double lk) {
+    ctrl->leak += lk;
+    if (ctrl->hist && ctrl->sweeps < (unsigned long long)kHistCap) {
+        SweepRec rec;
+        rec.entries = ctrl->n_entries;
+        rec.edges = ctrl->sel_edges;
+        rec.nodes_cum = ctrl->diffused_nodes;
+        rec.use_pull = ctrl->use_pull;
+        rec.pad = 0;
+        ctrl->hist[ctrl->sweeps] = rec;
+    }
+    ctrl->sweeps += 1;
+    ctrl->diffused_edges += ctrl->sel_edges;
+    if (ctrl->use_pull == kUsePush) ctrl->push_sweeps += 1; else ctrl->pull_sweeps += 1;
+    ctrl->last_sel_edges = ctrl->sel_edges;
+}
 
 }  // namespace dit

@@ -169,29 +169,13 @@ __global__ void __launch_bounds__(kThreads) k_push(const int32_t *__restrict__ c
 }
 
 // ---------------------------------------------------------------- reduce
-// Next-sweep control from the (global) residual r and max fluid fm.
-__device__ void finalize_control(Ctrl *ctrl, double r, double fm, int is_init, int64_t m) {
-    ctrl->resid = r;
-    ctrl->fmax = fm;
-    const double T = ctrl->theta * r / ctrl->n_global;
-    ctrl->T = T < fm ? T : fm;
-    ctrl->done = (r <= ctrl->tol || ctrl->sweeps >= ctrl->max_sweeps) ? 1u : 0u;
-    // direction of the next sweep: AUTO takes this sweep's frontier out-edges
-    // as the estimate of the next one's (the first sweep from a uniform F_0
-    // takes every node)
-    const unsigned long long fe = is_init ? (unsigned long long)m : ctrl->last_sel_edges;
-    if (ctrl->variant == DI_VARIANT_TILED) ctrl->use_pull = kUseTiled;
-    else if (ctrl->variant == DI_VARIANT_PULL) ctrl->use_pull = kUsePull;
-    else if (ctrl->variant == DI_VARIANT_PUSH) ctrl->use_pull = kUsePush;
-    else ctrl->use_pull = ((double)fe > ctrl->pull_edges) ? kUsePull : kUsePush;
-}
-
 __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ F, int64_t n, int64_t m,
                                                      Ctrl *__restrict__ ctrl, double *__restrict__ part,
-                                                     const double *__restrict__ part_sel, int is_init) {
+                                                     const double *__restrict__ part_sel, int is_init,
+                                                     int force) {
     __shared__ double s_sum[kWarps], s_max[kWarps];
     __shared__ bool s_last;
-    if (ctrl->done) return;
+    if (ctrl->done && !force) return;
     // two independent 16-byte streams per thread (F is 256-byte aligned)
     double s0 = 0.0, s1 = 0.0, mx = 0.0;
     const int64_t n2 = n >> 1;
@@ -246,21 +230,9 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
     }
     if (!is_init) {
         for (unsigned b = 0; b < gridDim.x; ++b) lk += vs[b];
-        ctrl->leak += lk;
-        if (ctrl->hist && ctrl->sweeps < (unsigned long long)kHistCap) {
-            SweepRec rec;
-            rec.entries = ctrl->n_entries;
-            rec.edges = ctrl->sel_edges;
-            rec.nodes_cum = ctrl->diffused_nodes;
-            rec.use_pull = ctrl->use_pull;
-            rec.pad = 0;
-            ctrl->hist[ctrl->sweeps] = rec;
-        }
-        ctrl->sweeps += 1;
-        ctrl->diffused_edges += ctrl->sel_edges;
-        if (ctrl->use_pull == kUsePush) ctrl->push_sweeps += 1; else ctrl->pull_sweeps += 1;
-        ctrl->last_sel_edges = ctrl->sel_edges;
+        end_sweep(ctrl, lk);
     }
+    if (force) ctrl->gather = 0;        // TILED flush: the pending remote pushes are now in F
     ctrl->n_entries = 0;
     ctrl->sel_edges = 0;
     ctrl->red_blocks = 0;
@@ -335,6 +307,7 @@ void free_state(State &s) {
     cudaFree(s.F);
     cudaFree(s.H);
     cudaFree(s.A);
+    cudaFree(s.A2);
     cudaFree(s.ent);
     cudaFree(s.ctrl);
     cudaFree(s.part);
@@ -388,7 +361,16 @@ void launch_push(di_graph *h) {
 
 void launch_reduce(di_graph *h, int is_init) {
     State &s = h->s;
-    k_reduce<<<s.grid, kThreads, 0, h->stream>>>(s.F, h->g.n, h->g.m, s.ctrl, s.part, s.part + 2 * s.grid, is_init);
+    k_reduce<<<s.grid, kThreads, 0, h->stream>>>(s.F, h->g.n, h->g.m, s.ctrl, s.part, s.part + 2 * s.grid, is_init,
+                                                 0);
+    count_launch();
+}
+
+// exact |F|_1 / max|F| of the current F even when `done` is set (after a TILED
+// flush): no sweep is counted; `done` is re-derived from the exact residual
+void launch_reduce_exact(di_graph *h) {
+    State &s = h->s;
+    k_reduce<<<s.grid, kThreads, 0, h->stream>>>(s.F, h->g.n, h->g.m, s.ctrl, s.part, s.part + 2 * s.grid, 1, 1);
     count_launch();
 }
 
@@ -414,17 +396,17 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
         const double nodes = (double)(rc.nodes_cum - prev_nodes);
         prev_nodes = rc.nodes_cum;
         if (rc.use_pull == kUseTiled) {
-            // tile kernel: F, inv, deg, lptr read + F, H, A written per node, local
-            // edges (u16 source + weight) read once; remote pull over the remote CSC
-            p.tile_ms += t[0];
-            p.tile_bytes += 52.0 * n + (double)g.tl.mloc * (2.0 + wb);
-            p.tile_launches += 1;
-            p.pull_ms += t[2];
-            p.pull_bytes += 32.0 * (double)g.tl.rem.npieces + (double)g.tl.rem.m * (12.0 + wb);
+            // heavy remote gather (k_heavy + fix) in slot 0, the fused tile kernel in slot 2
+            // (per node 68 B, per local edge 2 + w, per light record rec + 8)
+            const TilePlan &tp = g.tl;
+            const double rec = g.w_kind == DI_W_F64 ? 16.0 : 8.0;
+            p.pull_ms += t[0];
+            p.pull_bytes += (double)tp.mh * (rec + 8.0) + 32.0 * (double)tp.nseg + 16.0 * (double)tp.nh;
             p.pull_launches += 1;
-            p.reduce_ms += t[3];
-            p.reduce_bytes += 8.0 * n;
-            p.reduce_launches += 1;
+            p.tile_ms += t[2];
+            p.tile_bytes += 68.0 * n + (double)tp.mloc * (2.0 + wb) + (double)tp.mlight * (rec + 8.0) +
+                            8.0 * (double)tp.nh;
+            p.tile_launches += 1;
             continue;
         }
         p.select_ms += t[0];
@@ -454,7 +436,10 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     const bool want_pull = o.variant != DI_VARIANT_PUSH;
     if (want_pull && g.n > 0) {
         build_transpose(h);
-        if (o.variant == DI_VARIANT_TILED) build_tiles(h);
+        if (o.variant == DI_VARIANT_TILED) {
+            build_tiles(h);
+            if (!s.A2) DI_CUDA(cudaMalloc(&s.A2, g.n * sizeof(double)));
+        }
         if (!s.A) DI_CUDA(cudaMalloc(&s.A, g.n * sizeof(double)));
     }
     s.rounds = o.local_rounds > 0 ? o.local_rounds : 4;
@@ -480,7 +465,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     s.tiled_call = c.variant == DI_VARIANT_TILED;
 }
 
-void mark_event(di_graph *h, int64_t sweep, int k) {
+void mark_event(di_graph *h, int64_t sweep, int k) {  // profiling events (declared in dit_internal.cuh)
     State &s = h->s;
     if (!s.profile || sweep >= kHistCap) return;
     const size_t idx = (size_t)sweep * 5 + k;
@@ -498,11 +483,7 @@ void launch_sweep(di_graph *h) {
     const int64_t k = s.launched;
     mark_event(h, k, 0);
     if (s.tiled_call) {
-        launch_tile_local(h, s.rounds);              // select + local rounds ("select" slot)
-        mark_event(h, k, 1);
-        mark_event(h, k, 2);
-        launch_pull_plan(h, h->g.tl.rem, s.A, kUseTiled);
-        mark_event(h, k, 3);
+        launch_tile_sweep(h, s.rounds);              // heavy gather (0..1), fused tile kernel (2..3)
         return;
     }
     launch_select(h, false);
@@ -515,7 +496,7 @@ void launch_sweep(di_graph *h) {
 }
 
 void launch_sweep_reduce(di_graph *h) {
-    launch_reduce(h, 0);
+    if (!h->s.tiled_call) launch_reduce(h, 0);   // the tile kernel ends its own sweep
     mark_event(h, h->s.launched, 4);
     h->s.launched += 1;
 }
@@ -562,7 +543,14 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
                 launch_sweep(h);
                 launch_sweep_reduce(h);
             }
-            if (poll_done(h)) break;
+            if (poll_done(h)) {
+                if (!s.tiled_call || !s.ctrl_host->gather) break;
+                // TILED: the last sweep's remote pushes are still pending in A;
+                // gather them into F and take the exact residual
+                launch_tile_flush(h);
+                launch_reduce_exact(h);
+                if (poll_done(h)) break;
+            }
             chunk = std::min(chunk * 2, 64);
         }
     } else {
