@@ -288,7 +288,8 @@ def run_ours(args):
                        "sweeps_per_solve": sweeps[-1], "diffused_edges_per_solve": results[-1]["diffused_edges"],
                        "push_sweeps": res["push_sweeps"], "pull_sweeps": res["pull_sweeps"],
                        "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",
-                       "generate_s": round(gen_s, 2)},
+                       "generate_s": round(gen_s, 2),
+                       "tiled_plan": _lib.di_plan_stats(G.handle) if args.variant == "tiled" else None},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks}
     print(json.dumps(line), flush=True)

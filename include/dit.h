@@ -259,6 +259,16 @@ int di_shard_poll(di_graph *g, int32_t *done);
 int di_shard_finish(di_graph *g, double tol, const di_solve_opts *opts, double *H_out, int32_t H_mem,
                     di_result *res);
 
+/*
+ * Sizes of the graph's DI_VARIANT_TILED plan (built by the first tiled solve;
+ * DESIGN.md §5), written to stats[0 .. min(cap, DI_PLAN_STATS)-1] in this order:
+ * node tiles, local in-edges, sliced-ELL slots (local edges + padding), light
+ * remote in-edges, heavy remote in-edges, heavy targets, heavy segments, heavy
+ * runs, heavy chunks, source stripes.  All zero before the plan exists.
+ */
+#define DI_PLAN_STATS 10
+int di_plan_stats(const di_graph *g, int64_t *stats, int32_t cap);
+
 /* Text of the last error raised on the calling thread ("" if none). */
 const char *di_last_error(void);
 

@@ -32,7 +32,7 @@ DI_TILE_NODES = 512   # include/dit.h
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",
-           "di_kernel_launches", "di_profile_enable", "di_profile_get", "di_sweep_history"]
+           "di_kernel_launches", "di_profile_enable", "di_profile_get", "di_sweep_history", "di_plan_stats"]
 
 
 class di_profile(ctypes.Structure):
@@ -79,6 +79,7 @@ _lib.di_set_state.argtypes = [_P, _D, _P, _P, _I32, _D]
 _lib.di_profile_enable.argtypes = [_P, _I32]
 _lib.di_profile_get.argtypes = [_P, ctypes.POINTER(di_profile)]
 _lib.di_sweep_history.argtypes = [_P, _I64, _P, _P, _P, _P, ctypes.POINTER(_I64)]
+_lib.di_plan_stats.argtypes = [_P, _P, ctypes.c_int32]
 _lib.di_last_error.restype = ctypes.c_char_p
 _lib.di_kernel_launches.restype = _I64
 for _name in EXPORTS:
@@ -251,6 +252,17 @@ def di_sweep_history(h, cap=1 << 16):
                                  var.ctypes.data, ctypes.byref(cnt)))
     k = cnt.value
     return nodes[:k], edges[:k], ent[:k], var[:k]
+
+
+PLAN_STATS = ("tiles", "local_edges", "ell_slots", "light_edges", "heavy_edges", "heavy_targets", "heavy_segments",
+              "heavy_runs", "heavy_chunks", "stripes")
+
+
+def di_plan_stats(h):
+    """Sizes of the tiled plan (include/dit.h di_plan_stats) as a dict."""
+    v = np.zeros(len(PLAN_STATS), np.int64)
+    _check(_lib.di_plan_stats(h, v.ctypes.data, len(PLAN_STATS)))
+    return {k: int(x) for k, x in zip(PLAN_STATS, v)}
 
 
 # ------------------------------------------------------------------ shards (multi-GPU)

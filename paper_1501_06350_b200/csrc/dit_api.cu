@@ -243,6 +243,16 @@ int di_profile_get(const di_graph *g, di_profile *out) {
     });
 }
 
+int di_plan_stats(const di_graph *g, int64_t *stats, int32_t cap) {
+    return guarded([&] {
+        if (!g || !stats || cap < 0) fail(DI_ERR_INVALID, "bad argument");
+        const TilePlan &t = g->g.tl;
+        const int64_t v[DI_PLAN_STATS] = {t.ntile, t.mloc, t.mpad, t.mlight, t.mh, t.nh, t.nseg, t.nrun, t.nchunk,
+                                          t.built ? (int64_t)t.s_chunk.size() - 1 : 0};
+        for (int k = 0; k < cap && k < DI_PLAN_STATS; ++k) stats[k] = t.built ? v[k] : 0;
+    });
+}
+
 int di_sweep_history(const di_graph *gc, int64_t cap, int64_t *nodes, int64_t *edges, int64_t *entries,
                      int32_t *variant, int64_t *count) {
     return guarded([&] {

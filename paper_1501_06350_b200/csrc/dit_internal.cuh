@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/dit.h"
@@ -88,26 +89,38 @@ struct TilePlan {
     bool built = false;
     int64_t ntile = 0;             // node tiles
     // per node [n]
-    uint32_t *lrel = nullptr;      // local in-edge start, relative to ltile[tile]
     uint32_t *rrel = nullptr;      // light remote in-edge start, relative to rtile[tile]
     int32_t *hidx = nullptr;       // heavy index of the target or -1
     float *wr = nullptr;           // share of node i's outflow that leaves its tile: sum_remote w * inv
     int32_t *deg = nullptr;        // out-degree (diffused-edge accounting)
     // per tile [ntile+1]
     int64_t *ltile = nullptr, *rtile = nullptr;
-    // local in-edges (CSC order, padded by 16 B for aligned TMA supersets)
-    uint16_t *lsrc = nullptr;      // [mloc] source - tile base
-    void *lw = nullptr;            // [mloc] raw weight (graph storage kind) or null
-    int64_t mloc = 0;
-    // light remote records {int32 src, weight} (8 B for f32/unweighted, 16 B for f64)
-    void *rrec = nullptr;
+    // local in-edges in a sliced-ELL layout per tile: the tile's targets are
+    // ranked by local in-degree (lperm: rank -> node, descending degree); warp w
+    // of the tile kernel takes ranks [32w, 32w+32) and slot s of lane l sits at
+    // ltile[t] + wofs[t*17+w] + 32 s + l (padding: source kNodeTile, weight 0)
+    uint16_t *lperm = nullptr;     // [ntile*kNodeTile]
+    uint32_t *wofs = nullptr;      // [ntile*17] slot offset of each warp, relative to ltile[t]
+    uint16_t *lsrc = nullptr;      // [mpad] source - tile base (+16 B for aligned TMA supersets)
+    void *lw = nullptr;            // [mpad] raw weight (graph storage kind) or null
+    int64_t mloc = 0, mpad = 0;    // local in-edges, padded slots
+    // light remote in-edges: per target tile, CSC order, {int32 src, weight}
+    // records (8 B for f32/unweighted, 16 B for f64), gathered by the tile kernel
+    void *rrec = nullptr;          // [mlight] (+16 B)
     int64_t mlight = 0;
-    // heavy targets
-    int64_t nh = 0, mh = 0, nseg = 0, nchunk = 0;
-    void *hrec = nullptr;          // [mh] records, by heavy target then source
+    // heavy targets: remote in-edges sorted by (source stripe, target, source);
+    // one stripe's slice of the outflow A stays in L2 while its edges are
+    // gathered.  Segments = (stripe, target) runs cut at the stripe's 2048-edge
+    // chunks; hsum(h) accumulates the runs stripe by stripe (fixed order).
+    int64_t nh = 0, mh = 0, nseg = 0, nchunk = 0, nrun = 0;
+    int64_t stripe_nodes = 0;
+    void *hrec = nullptr;          // [mh] records
+    int64_t *chunk_start = nullptr;  // [nchunk+1] first heavy edge of each chunk
     int64_t *seg_start = nullptr;  // [nseg+1] first heavy edge of each segment
     int64_t *cfirst = nullptr;     // [nchunk+1] first segment of each chunk
-    int64_t *hfirst = nullptr;     // [nh+1] first segment of each heavy target
+    int32_t *run_h = nullptr;      // [nrun] heavy index of each run (high bit: first run of the target)
+    int64_t *run_seg = nullptr;    // [nrun+1] first segment of each run
+    std::vector<int64_t> s_chunk, s_run;   // per stripe [S+1]: first chunk, first run
     double *part = nullptr;        // [nseg] segment partial sums
     double *hsum = nullptr;        // [nh] remote inflow of each heavy target
     int64_t max_tile_edges = 0;    // most local in-edges of one tile
@@ -220,6 +233,8 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
                   const void *add_w, int w_dtype, int64_t n_rem, const int32_t *rem_src,
                   const int32_t *rem_dst, int mem);
 void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStream_t st);
+std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1,
+                                                 int64_t count, int bits, cudaStream_t st);
 
 // ---- device helpers ----
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

@@ -11,6 +11,8 @@
 // bitwise reproducible run to run on a given graph.
 #include "dit_internal.cuh"
 
+#include <utility>
+
 
 namespace dit {
 
@@ -185,6 +187,26 @@ static void radix_sort_pass_launch(const uint32_t *k, const void *v, uint32_t *o
                                                                            ok, (uint32_t *)ov);
     count_launch();
     DI_CUDA(cudaGetLastError());
+}
+
+// Stable LSD radix sort of (keys, u32 values) on the low `bits` bits of the
+// keys; k1/v1 are scratch of the same size.  Returns the buffers holding the
+// result (either the inputs or the scratch).
+std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1,
+                                                 int64_t count, int bits, cudaStream_t st) {
+    if (count <= 0) return {k0, v0};
+    const int64_t ntiles = (count + kSortTile - 1) / kSortTile;
+    int64_t *hc, *ho;
+    DI_CUDA(cudaMallocAsync(&hc, (int64_t)kRadix * ntiles * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&ho, ((int64_t)kRadix * ntiles + 1) * sizeof(int64_t), st));
+    for (int shift = 0; shift < bits; shift += kRadixBits) {
+        radix_sort_pass_launch(k0, v0, k1, v1, count, shift, ntiles, hc, ho, false, st);
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+    }
+    DI_CUDA(cudaFreeAsync(hc, st));
+    DI_CUDA(cudaFreeAsync(ho, st));
+    return {k0, v0};
 }
 
 // Work plan of a CSC (pieces, tiles, split-target fixups) for k_pull.

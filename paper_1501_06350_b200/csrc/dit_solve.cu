@@ -16,6 +16,7 @@
 #include "dit_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace dit {
@@ -396,15 +397,16 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
         const double nodes = (double)(rc.nodes_cum - prev_nodes);
         prev_nodes = rc.nodes_cum;
         if (rc.use_pull == kUseTiled) {
-            // heavy remote gather (k_heavy + fix) in slot 0, the fused tile kernel in slot 2
-            // (per node 68 B, per local edge 2 + w, per light record rec + 8)
+            // heavy remote gather (stripe kernels) in slot 0, the fused tile kernel in slot 2
+            // (per node 66 B, per local edge 2 + w, per light record rec + 8,
+            // per heavy edge rec + 8, per heavy segment 24 B)
             const TilePlan &tp = g.tl;
             const double rec = g.w_kind == DI_W_F64 ? 16.0 : 8.0;
             p.pull_ms += t[0];
-            p.pull_bytes += (double)tp.mh * (rec + 8.0) + 32.0 * (double)tp.nseg + 16.0 * (double)tp.nh;
+            p.pull_bytes += (double)tp.mh * (rec + 8.0) + 24.0 * (double)tp.nseg + 24.0 * (double)tp.nrun;
             p.pull_launches += 1;
             p.tile_ms += t[2];
-            p.tile_bytes += 68.0 * n + (double)tp.mloc * (2.0 + wb) + (double)tp.mlight * (rec + 8.0) +
+            p.tile_bytes += 66.0 * n + (double)tp.mloc * (2.0 + wb) + (double)tp.mlight * (rec + 8.0) +
                             8.0 * (double)tp.nh;
             p.tile_launches += 1;
             continue;
@@ -532,8 +534,15 @@ void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res
     }
 }
 
+// L2 fetch granularity for the sweep's random 8-byte gathers (experiment knob)
+static void set_l2_fetch() {
+    const char *e = getenv("DIT_L2_FETCH");
+    if (e && *e) DI_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
+}
+
 void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res) {
     State &s = h->s;
+    set_l2_fetch();
     prepare_call(h, tol, o, nullptr);
     if (h->g.n > 0) {
         launch_reduce(h, 1);

@@ -6,28 +6,36 @@
 // SM's shared memory.  Node ids are cut into tiles of kNodeTile; per sweep:
 //
 //   1. every tile first takes in the remote pushes of the previous sweep
-//      (F(t) += d D(i) P_{t,i} for i outside t's tile: a gather of the
-//      previous sweep's outflow A(i) = d D(i) / sum_k w_{i,k} over t's remote
-//      in-edges, Eq. (8) being linear in the diffused amount);
+//      (F(t) += d D(i) P_{t,i} for i outside t's tile, Eq. (8) being linear in
+//      the diffused amount D);
 //   2. then runs `rounds` Jacobi diffusion rounds over its LOCAL in-edges
 //      (source and target in the tile) in shared memory: every node holding
 //      fluid is diffused (Eqs. (8), (10)), local pushes applied at once;
-//   3. writes F (what is left in the tile), H += D and the new outflow A.
+//   3. writes F (what is left in the tile) and H += D, and emits the remote
+//      pushes d D(i) P_{t,i} of its sources.
 //
 // Step 1 of sweep k+1 completes the remote pushes of sweep k, so the sequence
 // of Eq. (8) updates is exactly the oracle's (orc_tiled_sweep_run: rounds in
 // every tile, then the remote pushes).  The stop test after sweep k uses
-// |F|_1 = sum_t |f_t| + sum_i |A(i)| wr(i) (wr = share of i's outflow that leaves
-// its tile): exact for non-negative fluid, an upper bound for signed fluid
-// (§3.5), so stopping on it keeps Theorem 1's guarantee; after the last sweep
-// the pending pushes are flushed into F and the exact |F|_1 is taken.
+// |F|_1 = sum_t |f_t| + sum_i |d D(i) inv(i)| wr(i) (wr = share of i's out-weight
+// that leaves its tile): exact for non-negative fluid, an upper bound for
+// signed fluid (§3.5), so stopping on it keeps Theorem 1's guarantee; after the
+// last sweep the pending pushes are flushed into F and the exact |F|_1 taken.
 //
-// Kernels (B200): k_tile -- one 512-thread CTA per tile, 2 CTAs per SM,
-// the tile's local edges and light remote records staged by TMA bulk copies
-// (cp.async.bulk + mbarrier) while the per-node state streams into registers;
-// k_heavy / k_heavy_fix -- the remote gather of heavy targets over fixed
-// 2048-edge chunks, warp-per-segment sums and warp-per-target fix-ups.  Every
-// summation has a fixed order: bitwise reproducible run to run.
+// Remote pushes are gathered by their targets.  Light targets (few remote
+// in-edges) are gathered inside the tile kernel from the previous sweep's
+// outflow A(i) = d D(i) inv(i), over {source, weight} records staged by TMA.
+// Heavy targets' in-edges are sorted by (source stripe, target, source) and
+// gathered stripe by stripe, so that the slice of A being read stays in L2
+// (a random 8-byte read from HBM costs a 64-byte DRAM access on B200).
+//
+// Kernels (B200): k_tile -- one 512-thread CTA per tile, 2 CTAs per SM; the
+// tile's light records and its local edges (sliced-ELL, coalesced across the
+// warp) staged by TMA bulk copies (cp.async.bulk + mbarrier) while the
+// per-node state streams into registers.  k_heavy_s -- per stripe: CTA per
+// 2048-edge chunk, warp per segment; then the stripe's runs folded into
+// hsum in stripe order.  Every summation has a fixed order: bitwise
+// reproducible run to run.
 #include "dit_internal.cuh"
 
 #include <algorithm>
@@ -37,6 +45,9 @@ namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // thread i owns node i of the tile
 constexpr int kTileWarps = kTileThreads / 32;
+
+template <typename W>
+using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
 
 // remote record: source and raw weight of one remote in-edge
 template <typename W>
@@ -53,8 +64,7 @@ struct RemRec<double> {
 template <typename W>
 __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w; }
 
-template <typename W>
-using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
+constexpr int64_t kStripeBytes = 48ll << 20;   // outflow slice per heavy stripe (L2-resident)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -86,6 +96,11 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+
+// bulk prefetch of a global range into L2 (the TMA engine; no completion tracking)
+__device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // ---------------------------------------------------------------- build
@@ -125,39 +140,81 @@ __global__ void k_classify(const int64_t *__restrict__ rc, int64_t n, int64_t nt
     }
 }
 
-// tile-relative offsets, tile bases, heavy index, out-degree
-__global__ void k_tile_rel(const int64_t *__restrict__ lptr, const int64_t *__restrict__ rptr,
-                           const int64_t *__restrict__ hpos, const int64_t *__restrict__ hflag,
-                           const int64_t *__restrict__ row_ptr, int64_t n, int64_t ntile, uint32_t *__restrict__ lrel,
-                           uint32_t *__restrict__ rrel, int32_t *__restrict__ hidx, int32_t *__restrict__ hj,
-                           int32_t *__restrict__ deg, int64_t *__restrict__ ltile, int64_t *__restrict__ rtile) {
+// rank the tile's targets by local in-degree (descending, ties by id) and
+// lay out the sliced-ELL warp offsets; CTA per tile
+__global__ void __launch_bounds__(kTileThreads) k_tile_rank(const int64_t *__restrict__ lc, int64_t n, int64_t ntile,
+                                                             uint16_t *__restrict__ lperm, int32_t *__restrict__ rank,
+                                                             uint32_t *__restrict__ wofs, int64_t *__restrict__ pcnt) {
+    __shared__ int64_t deg_s[kNodeTile];
+    __shared__ uint16_t perm_s[kNodeTile];
+    const int k = threadIdx.x;
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const int64_t a0 = t * kNodeTile;
+        const int nn = (int)min(kNodeTile, n - a0);
+        const int64_t dk = k < nn ? lc[a0 + k] : 0;
+        deg_s[k] = dk;
+        __syncthreads();
+        int r = 0;
+        for (int j = 0; j < (int)kNodeTile; ++j) {
+            const int64_t dj = deg_s[j];
+            r += (dj > dk) || (dj == dk && j < k);
+        }
+        perm_s[r] = (uint16_t)k;
+        if (k < nn) rank[a0 + k] = r;
+        __syncthreads();
+        lperm[a0 + k] = perm_s[k];
+        if (k == 0) {
+            uint32_t off = 0;
+            for (int w = 0; w < kTileWarps; ++w) {
+                wofs[t * (kTileWarps + 1) + w] = off;
+                off += 32u * (uint32_t)deg_s[perm_s[32 * w]];   // the warp's largest degree
+            }
+            wofs[t * (kTileWarps + 1) + kTileWarps] = off;
+            pcnt[t] = off;
+        }
+        __syncthreads();
+    }
+}
+
+// light offsets relative to the tile, tile bases, heavy index, out-degree
+__global__ void k_tile_rel(const int64_t *__restrict__ rptr, const int64_t *__restrict__ hpos,
+                           const int64_t *__restrict__ hflag, const int64_t *__restrict__ row_ptr, int64_t n,
+                           int64_t ntile, uint32_t *__restrict__ rrel, int32_t *__restrict__ hidx,
+                           int32_t *__restrict__ deg, int64_t *__restrict__ rtile) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += (int64_t)gridDim.x * blockDim.x) {
         if (j < n) {
             const int64_t b = (j / kNodeTile) * kNodeTile;
-            lrel[j] = (uint32_t)(lptr[j] - lptr[b]);
             rrel[j] = (uint32_t)(rptr[j] - rptr[b]);
             const int32_t h = hflag[j] ? (int32_t)hpos[j] : -1;
             hidx[j] = h;
-            if (h >= 0) hj[h] = (int32_t)j;
             deg[j] = (int32_t)(row_ptr[j + 1] - row_ptr[j]);
         }
         if (j % kNodeTile == 0 || j == n) {
             const int64_t t = (j + kNodeTile - 1) / kNodeTile;   // j == n: the end of the last tile
-            if (t <= ntile) {
-                ltile[t] = lptr[j];
-                rtile[t] = rptr[j];
-            }
+            if (t <= ntile) rtile[t] = rptr[j];
         }
     }
 }
 
-// scatter every in-edge (ascending source within its target) to its class
+template <typename W>
+__global__ void k_fill_pad(uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ lw, int64_t cnt) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+        lsrc[e] = (uint16_t)kNodeTile;     // the always-zero outflow slot
+        if (lw) lw[e] = StoreW<W>(0);
+    }
+}
+
+// every in-edge (ascending source within its target) to its class: local ->
+// sliced-ELL slot; light remote -> the tile's record block; heavy remote ->
+// a record in CSC order plus its sort key (source stripe) and heavy index
 template <typename W>
 __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *__restrict__ tsrc,
-                              const StoreW<W> *__restrict__ tw, int64_t n, const int64_t *__restrict__ lptr,
+                              const StoreW<W> *__restrict__ tw, int64_t n, const int64_t *__restrict__ ltile,
+                              const uint32_t *__restrict__ wofs, const int32_t *__restrict__ rank,
                               const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
-                              const int32_t *__restrict__ hidx, uint16_t *__restrict__ lsrc,
-                              StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ hrec) {
+                              const int32_t *__restrict__ hidx, int64_t stripe_nodes, uint16_t *__restrict__ lsrc,
+                              StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
+                              uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval, uint32_t *__restrict__ hof) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lane = lane_id();
@@ -166,10 +223,12 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
     for (int64_t t = warp; t < n; t += nw) {
         const int64_t b = tptr[t], e = tptr[t + 1];
         const int64_t tile = t / kNodeTile;
-        const bool heavy = hidx[t] >= 0;
-        int64_t lo = lptr[t];
-        int64_t ro = heavy ? hptr[t] : rptr[t];
-        RemRec<W> *dst = heavy ? hrec : rrec;
+        const int32_t hx = hidx[t];
+        // sliced-ELL slots of target t: base + 32 s, s = its s-th local in-edge
+        const int rk = rank[t];
+        const int64_t lbase = ltile[tile] + wofs[tile * (kTileWarps + 1) + rk / 32] + (rk % 32);
+        int64_t lo = 0;
+        int64_t ro = hx >= 0 ? hptr[t] : rptr[t];
         for (int64_t k0 = b; k0 < e; k0 += 32) {
             const int64_t k = k0 + lane;
             const bool ok = k < e;
@@ -178,7 +237,7 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
             const unsigned bl = __ballot_sync(0xffffffffu, loc);
             const unsigned br = __ballot_sync(0xffffffffu, ok && !loc);
             if (loc) {
-                const int64_t o = lo + __popc(bl & lt);
+                const int64_t o = lbase + 32 * (lo + __popc(bl & lt));
                 lsrc[o] = (uint16_t)(s - tile * kNodeTile);
                 if (kW) lw[o] = tw[k];
             } else if (ok) {
@@ -187,7 +246,14 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
                 r.src = s;
                 if constexpr (kW) r.w = tw[k];
                 else r.w = 1.0f;
-                dst[o] = r;
+                if (hx >= 0) {
+                    htmp[o] = r;
+                    hkey[o] = (uint32_t)(s / stripe_nodes);
+                    hval[o] = (uint32_t)o;
+                    hof[o] = (uint32_t)hx;
+                } else {
+                    rrec[o] = r;
+                }
             }
             lo += __popc(bl);
             ro += __popc(br);
@@ -195,7 +261,65 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
     }
 }
 
-// share of every source's outflow that leaves its tile (warp per source)
+// heavy edges in (stripe, target, source) order: records, stripe and target of each
+template <typename W>
+__global__ void k_heavy_gather(const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sval, int64_t mh,
+                               const RemRec<W> *__restrict__ htmp, const uint32_t *__restrict__ hof,
+                               RemRec<W> *__restrict__ hrec, uint32_t *__restrict__ hh) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = sval[p];
+        hrec[p] = htmp[q];
+        hh[p] = hof[q];
+    }
+}
+
+// run / segment / chunk flags: run = (stripe, target); chunk = 2048 edges from
+// the stripe's start; segment = run cut at chunk starts
+__global__ void k_heavy_flags(const uint32_t *__restrict__ st, const uint32_t *__restrict__ hh, int64_t mh,
+                              const int64_t *__restrict__ sbeg, int64_t *__restrict__ runf, int64_t *__restrict__ segf,
+                              int64_t *__restrict__ chkf) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = st[p];
+        const bool run = p == 0 || st[p - 1] != s || hh[p - 1] != hh[p];
+        const bool chk = (p - sbeg[s]) % kHeavyChunk == 0;
+        runf[p] = run;
+        chkf[p] = chk;
+        segf[p] = run || chk;
+    }
+}
+
+__global__ void k_heavy_index(const int64_t *__restrict__ runf, const int64_t *__restrict__ segf,
+                              const int64_t *__restrict__ chkf, const int64_t *__restrict__ runid,
+                              const int64_t *__restrict__ segid, const int64_t *__restrict__ chkid,
+                              const uint32_t *__restrict__ hh, int64_t mh, int64_t *__restrict__ seg_start,
+                              int64_t *__restrict__ chunk_start, int64_t *__restrict__ cfirst,
+                              int32_t *__restrict__ run_h, int64_t *__restrict__ run_seg,
+                              unsigned long long *__restrict__ frun) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
+        if (segf[p]) seg_start[segid[p]] = p;
+        if (chkf[p]) {
+            chunk_start[chkid[p]] = p;
+            cfirst[chkid[p]] = segid[p];
+        }
+        if (runf[p]) {
+            run_h[runid[p]] = (int32_t)hh[p];
+            run_seg[runid[p]] = segid[p];
+            atomicMin(&frun[hh[p]], (unsigned long long)runid[p]);   // the target's first (lowest-stripe) run
+        }
+    }
+}
+
+__global__ void k_mark_first_run(const unsigned long long *__restrict__ frun, int64_t nh, int32_t *__restrict__ run_h) {
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x)
+        run_h[frun[h]] |= (int32_t)0x80000000;
+}
+
+__global__ void k_fill_u64(unsigned long long *__restrict__ p, int64_t cnt, unsigned long long v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// share of every source's out-weight that leaves its tile (warp per source)
 template <typename W>
 __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const StoreW<W> *__restrict__ w, const double *__restrict__ inv, int64_t n,
@@ -213,51 +337,17 @@ __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_
     }
 }
 
-// heavy segments: segments of heavy target h = its edge range cut at chunk boundaries
-__global__ void k_seg_count(const int32_t *__restrict__ hj, const int64_t *__restrict__ hptr, int64_t nh,
-                            int64_t *__restrict__ cnt) {
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = hptr[hj[h]], e = hptr[hj[h] + 1];
-        cnt[h] = (e - 1) / kHeavyChunk - b / kHeavyChunk + 1;
-    }
-}
-
-__global__ void k_seg_write(const int32_t *__restrict__ hj, const int64_t *__restrict__ hptr, int64_t nh,
-                            const int64_t *__restrict__ hfirst, int64_t *__restrict__ seg_start,
-                            int64_t *__restrict__ cfirst) {
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = hptr[hj[h]];
-        const int64_t s0 = hfirst[h], s1 = hfirst[h + 1];
-        for (int64_t q = 0; q < s1 - s0; ++q) {
-            const int64_t p = q == 0 ? b : (b / kHeavyChunk + q) * kHeavyChunk;
-            seg_start[s0 + q] = p;
-            if (p % kHeavyChunk == 0) cfirst[p / kHeavyChunk] = s0 + q;   // every chunk starts a segment
-        }
-    }
-}
-
 __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntile, unsigned long long *__restrict__ mx) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntile; t += (int64_t)gridDim.x * blockDim.x)
         atomicMax(mx, (unsigned long long)(ltile[t + 1] - ltile[t]));
 }
 
 void free_tiles(TilePlan &t) {
-    cudaFree(t.lrel);
-    cudaFree(t.rrel);
-    cudaFree(t.hidx);
-    cudaFree(t.wr);
-    cudaFree(t.deg);
-    cudaFree(t.ltile);
-    cudaFree(t.rtile);
-    cudaFree(t.lsrc);
-    cudaFree(t.lw);
-    cudaFree(t.rrec);
-    cudaFree(t.hrec);
-    cudaFree(t.seg_start);
-    cudaFree(t.cfirst);
-    cudaFree(t.hfirst);
-    cudaFree(t.part);
-    cudaFree(t.hsum);
+    for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
+                    (void *)t.lperm, (void *)t.wofs, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
+                    (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
+                    (void *)t.hsum})
+        cudaFree(p);
     t = TilePlan();
 }
 
@@ -266,6 +356,23 @@ static int64_t read_i64(const int64_t *p, cudaStream_t st) {
     DI_CUDA(cudaMemcpyAsync(&v, p, sizeof(v), cudaMemcpyDeviceToHost, st));
     DI_CUDA(cudaStreamSynchronize(st));
     return v;
+}
+
+static int bits_for(int64_t x) {
+    int b = 1;
+    while (b < 32 && ((int64_t)1 << b) < x) ++b;
+    return b;
+}
+
+__global__ void k_u32_to_i64(const uint32_t *__restrict__ a, int64_t *__restrict__ b, int64_t cnt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+// per-stripe edge counts of the sorted stripe keys
+__global__ void k_stripe_count(const uint32_t *__restrict__ st, int64_t mh, unsigned long long *__restrict__ cnt) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x)
+        if (p == mh - 1 || st[p + 1] != st[p]) atomicAdd(&cnt[st[p]], (unsigned long long)(p + 1));
 }
 
 template <typename W>
@@ -277,63 +384,140 @@ static void build_tiles_t(di_graph *h) {
     const int grid = h->num_sms * 8;
     using SW = StoreW<W>;
     constexpr bool kW = !std::is_same<W, NoW>::value;
+    const size_t rs = sizeof(RemRec<W>);
     tp.ntile = (n + kNodeTile - 1) / kNodeTile;
-    int64_t *lc, *rc, *lrc, *hc, *hflag, *lptr, *rptr, *hptr, *hpos;
-    for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &lptr, &rptr, &hptr, &hpos})
+    tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
+    const int64_t S = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
+    // ---- classes of the in-edges
+    int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
+    for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
         DI_CUDA(cudaMallocAsync(p, (n + 1) * sizeof(int64_t), st));
     k_count_local<<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, n, lc, rc);
     k_classify<<<grid_for(h, tp.ntile), 256, 0, st>>>(rc, n, tp.ntile, lrc, hc, hflag);
     count_launch(2);
-    exclusive_scan_i64(lc, lptr, n, st);
     exclusive_scan_i64(lrc, rptr, n, st);
     exclusive_scan_i64(hc, hptr, n, st);
     exclusive_scan_i64(hflag, hpos, n, st);
-    tp.mloc = read_i64(lptr + n, st);
     tp.mlight = read_i64(rptr + n, st);
     tp.mh = read_i64(hptr + n, st);
     tp.nh = read_i64(hpos + n, st);
-    const size_t rs = sizeof(RemRec<W>);
-    DI_CUDA(cudaMalloc(&tp.lrel, n * sizeof(uint32_t)));
+    if (tp.mh >= (int64_t)0xffffffffLL) {
+        set_error("tiled plan: too many heavy remote edges for one graph handle");
+        throw Fail{DI_ERR_INVALID};
+    }
+    // ---- sliced-ELL layout of the local in-edges
+    int32_t *rank;
+    int64_t *pcnt;
+    DI_CUDA(cudaMallocAsync(&rank, (n > 0 ? n : 1) * sizeof(int32_t), st));
+    DI_CUDA(cudaMallocAsync(&pcnt, (tp.ntile + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMalloc(&tp.lperm, tp.ntile * kNodeTile * sizeof(uint16_t)));
+    DI_CUDA(cudaMalloc(&tp.wofs, tp.ntile * (kTileWarps + 1) * sizeof(uint32_t)));
+    DI_CUDA(cudaMalloc(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t)));
+    k_tile_rank<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
+        lc, n, tp.ntile, tp.lperm, rank, tp.wofs, pcnt);
+    count_launch();
+    exclusive_scan_i64(pcnt, tp.ltile, tp.ntile, st);
+    tp.mpad = read_i64(tp.ltile + tp.ntile, st);
+    tp.mloc = g.m - tp.mlight - tp.mh;
+    // +16 B: aligned TMA supersets may read up to 15 bytes past the end
+    DI_CUDA(cudaMalloc(&tp.lsrc, tp.mpad * sizeof(uint16_t) + 16));
+    if (kW) DI_CUDA(cudaMalloc(&tp.lw, tp.mpad * sizeof(SW) + 16));
+    if (tp.mpad > 0) {
+        k_fill_pad<W><<<grid_for(h, tp.mpad), 256, 0, st>>>(tp.lsrc, (SW *)tp.lw, tp.mpad);
+        count_launch();
+    }
+    // ---- per-node arrays, tile bases
     DI_CUDA(cudaMalloc(&tp.rrel, n * sizeof(uint32_t)));
     DI_CUDA(cudaMalloc(&tp.hidx, n * sizeof(int32_t)));
     DI_CUDA(cudaMalloc(&tp.wr, n * sizeof(float)));
     DI_CUDA(cudaMalloc(&tp.deg, n * sizeof(int32_t)));
-    DI_CUDA(cudaMalloc(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t)));
     DI_CUDA(cudaMalloc(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t)));
-    // +16 B: aligned TMA supersets may read up to 15 bytes past the end
-    DI_CUDA(cudaMalloc(&tp.lsrc, tp.mloc * sizeof(uint16_t) + 16));
-    if (kW) DI_CUDA(cudaMalloc(&tp.lw, tp.mloc * sizeof(SW) + 16));
+    k_tile_rel<<<grid_for(h, n + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, tp.ntile, tp.rrel, tp.hidx, tp.deg,
+                                                   tp.rtile);
+    k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.wr);
+    count_launch(2);
+    // ---- edges to their classes
     DI_CUDA(cudaMalloc(&tp.rrec, tp.mlight * rs + 16));
     DI_CUDA(cudaMalloc(&tp.hrec, tp.mh * rs + 16));
+    const int64_t mh1 = tp.mh > 0 ? tp.mh : 1;
+    RemRec<W> *htmp;
+    uint32_t *k0, *v0, *k1, *v1, *hof, *hh;
+    DI_CUDA(cudaMallocAsync(&htmp, mh1 * rs, st));
+    for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
+    k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, tp.ltile, tp.wofs, rank, rptr,
+                                           hptr, tp.hidx, tp.stripe_nodes, tp.lsrc, (SW *)tp.lw,
+                                           (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
+    count_launch();
+    // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
+    tp.s_chunk.assign(S + 1, 0);
+    tp.s_run.assign(S + 1, 0);
+    if (tp.mh > 0) {
+        auto sorted = radix_sort_u32(k0, v0, k1, v1, tp.mh, bits_for(S + 1), st);
+        uint32_t *skey = sorted.first, *sval = sorted.second;
+        k_heavy_gather<W><<<grid_for(h, tp.mh), 256, 0, st>>>(skey, sval, tp.mh, htmp, hof, (RemRec<W> *)tp.hrec, hh);
+        count_launch();
+        // stripe starts
+        unsigned long long *scnt;
+        DI_CUDA(cudaMallocAsync(&scnt, (S + 1) * sizeof(unsigned long long), st));
+        DI_CUDA(cudaMemsetAsync(scnt, 0, (S + 1) * sizeof(unsigned long long), st));
+        k_stripe_count<<<grid_for(h, tp.mh), 256, 0, st>>>(skey, tp.mh, scnt);
+        count_launch();
+        std::vector<unsigned long long> ends(S + 1);
+        DI_CUDA(cudaMemcpyAsync(ends.data(), scnt, (S + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        DI_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> sbeg(S + 1, 0);
+        for (int64_t s = 0, last = 0; s < S; ++s) {   // ends[s] = one past the stripe's last edge (0 if empty)
+            sbeg[s] = last;
+            if (ends[s]) last = (int64_t)ends[s];
+            sbeg[s + 1] = last;
+        }
+        for (int64_t s = 0; s < S; ++s)
+            tp.s_chunk[s + 1] = tp.s_chunk[s] + (sbeg[s + 1] - sbeg[s] + kHeavyChunk - 1) / kHeavyChunk;
+        tp.nchunk = tp.s_chunk[S];
+        int64_t *sbeg_d;
+        DI_CUDA(cudaMallocAsync(&sbeg_d, (S + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMemcpyAsync(sbeg_d, sbeg.data(), (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        // flags -> ids
+        int64_t *runf, *segf, *chkf, *runid, *segid, *chkid;
+        for (int64_t **p : {&runf, &segf, &chkf, &runid, &segid, &chkid})
+            DI_CUDA(cudaMallocAsync(p, (tp.mh + 1) * sizeof(int64_t), st));
+        k_heavy_flags<<<grid_for(h, tp.mh), 256, 0, st>>>(skey, hh, tp.mh, sbeg_d, runf, segf, chkf);
+        count_launch();
+        exclusive_scan_i64(runf, runid, tp.mh, st);
+        exclusive_scan_i64(segf, segid, tp.mh, st);
+        exclusive_scan_i64(chkf, chkid, tp.mh, st);
+        tp.nrun = read_i64(runid + tp.mh, st);
+        tp.nseg = read_i64(segid + tp.mh, st);
+        if (read_i64(chkid + tp.mh, st) != tp.nchunk) {
+            set_error("tiled plan: heavy chunk count mismatch");
+            throw Fail{DI_ERR_CUDA};
+        }
+        DI_CUDA(cudaMalloc(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t)));
+        DI_CUDA(cudaMalloc(&tp.chunk_start, (tp.nchunk + 1) * sizeof(int64_t)));
+        DI_CUDA(cudaMalloc(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t)));
+        DI_CUDA(cudaMalloc(&tp.run_h, tp.nrun * sizeof(int32_t)));
+        DI_CUDA(cudaMalloc(&tp.run_seg, (tp.nrun + 1) * sizeof(int64_t)));
+        DI_CUDA(cudaMalloc(&tp.part, tp.nseg * sizeof(double)));
+        unsigned long long *frun;
+        DI_CUDA(cudaMallocAsync(&frun, tp.nh * sizeof(unsigned long long), st));
+        k_fill_u64<<<grid_for(h, tp.nh), 256, 0, st>>>(frun, tp.nh, ~0ull);
+        k_heavy_index<<<grid_for(h, tp.mh), 256, 0, st>>>(runf, segf, chkf, runid, segid, chkid, hh, tp.mh,
+                                                          tp.seg_start, tp.chunk_start, tp.cfirst, tp.run_h,
+                                                          tp.run_seg, frun);
+        k_mark_first_run<<<grid_for(h, tp.nh), 256, 0, st>>>(frun, tp.nh, tp.run_h);
+        count_launch(3);
+        DI_CUDA(cudaMemcpyAsync(tp.seg_start + tp.nseg, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        DI_CUDA(cudaMemcpyAsync(tp.chunk_start + tp.nchunk, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        DI_CUDA(cudaMemcpyAsync(tp.cfirst + tp.nchunk, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        DI_CUDA(cudaMemcpyAsync(tp.run_seg + tp.nrun, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        // first run of every stripe
+        for (int64_t s = 0; s < S; ++s) tp.s_run[s] = sbeg[s] < tp.mh ? read_i64(runid + sbeg[s], st) : tp.nrun;
+        tp.s_run[S] = tp.nrun;
+        for (int64_t *p : {runf, segf, chkf, runid, segid, chkid, sbeg_d}) DI_CUDA(cudaFreeAsync(p, st));
+        DI_CUDA(cudaFreeAsync(frun, st));
+        DI_CUDA(cudaFreeAsync(scnt, st));
+    }
     DI_CUDA(cudaMalloc(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double)));
-    int32_t *hj;
-    DI_CUDA(cudaMallocAsync(&hj, (tp.nh > 0 ? tp.nh : 1) * sizeof(int32_t), st));
-    k_tile_rel<<<grid_for(h, n + 1), 256, 0, st>>>(lptr, rptr, hpos, hflag, g.row_ptr, n, tp.ntile, tp.lrel, tp.rrel,
-                                                   tp.hidx, hj, tp.deg, tp.ltile, tp.rtile);
-    k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, lptr, rptr, hptr, tp.hidx,
-                                           tp.lsrc, (SW *)tp.lw, (RemRec<W> *)tp.rrec, (RemRec<W> *)tp.hrec);
-    k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.wr);
-    count_launch(3);
-    // heavy segments
-    tp.nchunk = (tp.mh + kHeavyChunk - 1) / kHeavyChunk;
-    DI_CUDA(cudaMalloc(&tp.hfirst, (tp.nh + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMalloc(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t)));
-    int64_t *cnt;
-    DI_CUDA(cudaMallocAsync(&cnt, (tp.nh + 1) * sizeof(int64_t), st));
-    if (tp.nh > 0) {
-        k_seg_count<<<grid_for(h, tp.nh), 256, 0, st>>>(hj, hptr, tp.nh, cnt);
-        count_launch();
-    }
-    exclusive_scan_i64(cnt, tp.hfirst, tp.nh, st);
-    tp.nseg = read_i64(tp.hfirst + tp.nh, st);
-    DI_CUDA(cudaMalloc(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMalloc(&tp.part, (tp.nseg > 0 ? tp.nseg : 1) * sizeof(double)));
-    DI_CUDA(cudaMemcpyAsync(tp.seg_start + tp.nseg, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    DI_CUDA(cudaMemcpyAsync(tp.cfirst + tp.nchunk, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    if (tp.nh > 0) {
-        k_seg_write<<<grid_for(h, tp.nh), 256, 0, st>>>(hj, hptr, tp.nh, tp.hfirst, tp.seg_start, tp.cfirst);
-        count_launch();
-    }
     unsigned long long *mx;
     DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
     DI_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
@@ -343,8 +527,10 @@ static void build_tiles_t(di_graph *h) {
     }
     unsigned long long mxh = 0;
     DI_CUDA(cudaMemcpyAsync(&mxh, mx, sizeof(mxh), cudaMemcpyDeviceToHost, st));
-    for (int64_t *p : {lc, rc, lrc, hc, hflag, lptr, rptr, hptr, hpos, cnt}) DI_CUDA(cudaFreeAsync(p, st));
-    DI_CUDA(cudaFreeAsync(hj, st));
+    for (int64_t *p : {lc, rc, lrc, hc, hflag, rptr, hptr, hpos, pcnt}) DI_CUDA(cudaFreeAsync(p, st));
+    for (uint32_t *p : {k0, v0, k1, v1, hof, hh}) DI_CUDA(cudaFreeAsync(p, st));
+    DI_CUDA(cudaFreeAsync(htmp, st));
+    DI_CUDA(cudaFreeAsync(rank, st));
     DI_CUDA(cudaFreeAsync(mx, st));
     DI_CUDA(cudaStreamSynchronize(st));
     DI_CUDA(cudaGetLastError());
@@ -367,63 +553,93 @@ void build_tiles(di_graph *h) {
     }
 }
 
-// ---------------------------------------------------------------- heavy remote gather
-// hsum[h] = sum over heavy target h's remote in-edges of A(src) w, from the
-// previous sweep's outflow.  CTA per 2048-edge chunk: products staged in
-// shared memory, then one warp per segment (lane-strided + fixed butterfly).
+// ---------------------------------------------------------------- heavy remote sums
+// One launch per stripe s (and one more after the last): first the previous
+// stripe's runs are folded into hsum (run order = target order within the
+// stripe; a target's first run sets, later stripes add: fixed order), then
+// the chunks of stripe s: CTA per chunk stages A(src) w of its edges in
+// shared memory, warp per segment sums (lane-strided + fixed butterfly).
 template <typename W>
-__global__ void __launch_bounds__(kThreads) k_heavy(const RemRec<W> *__restrict__ hrec, int64_t mh, int64_t nchunk,
-                                                    const int64_t *__restrict__ seg_start,
-                                                    const int64_t *__restrict__ cfirst, const double *__restrict__ A0,
-                                                    const double *__restrict__ A1, double *__restrict__ part,
-                                                    const Ctrl *__restrict__ ctrl, int force) {
+__global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restrict__ hrec,
+                                                      const int64_t *__restrict__ chunk_start,
+                                                      const int64_t *__restrict__ seg_start,
+                                                      const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
+                                                      const int32_t *__restrict__ run_h,
+                                                      const int64_t *__restrict__ run_seg, int64_t q0, int64_t q1,
+                                                      const double *__restrict__ A0, const double *__restrict__ A1,
+                                                      double *__restrict__ part, double *__restrict__ hsum,
+                                                      const Ctrl *__restrict__ ctrl, int force) {
     __shared__ double vals[kHeavyChunk];
+    __shared__ int sbnd[kHeavyChunk + 1];
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
     if (!ctrl->gather) return;
     // the previous sweep wrote A[(sweeps - 1) & 1]
     const double *__restrict__ A = (ctrl->sweeps & 1) ? A0 : A1;
     const unsigned w = threadIdx.x >> 5, lane = lane_id();
-    for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
-        const int64_t e0 = c * kHeavyChunk;
-        const int cnt = (int)min(kHeavyChunk, mh - e0);
-#pragma unroll 4
+    // fold the previous stripe's runs (lane per run; long runs by the whole warp)
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = q0 + gw * 32; base < q1; base += nw * 32) {
+        const int64_t q = base + lane;
+        int64_t sb = 0, se = 0;
+        int32_t hv = 0;
+        if (q < q1) {
+            sb = run_seg[q];
+            se = run_seg[q + 1];
+            hv = run_h[q];
+        }
+        const int cnt = (int)(se - sb);
+        if (cnt > 0 && cnt < 32) {
+            double acc = 0.0;
+            for (int64_t s = sb; s < se; ++s) acc += part[s];
+            const int32_t hx = hv & 0x7fffffff;
+            hsum[hx] = (hv < 0) ? acc : hsum[hx] + acc;
+        }
+        unsigned big = __ballot_sync(0xffffffffu, cnt >= 32);
+        while (big) {
+            const int b = __ffs(big) - 1;
+            big &= big - 1;
+            const int64_t bb = __shfl_sync(0xffffffffu, sb, b), be = __shfl_sync(0xffffffffu, se, b);
+            const int32_t bh = __shfl_sync(0xffffffffu, hv, b);
+            double acc = 0.0;
+            for (int64_t s = bb + lane; s < be; s += 32) acc += part[s];
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                const int32_t hx = bh & 0x7fffffff;
+                hsum[hx] = (bh < 0) ? acc : hsum[hx] + acc;
+            }
+        }
+    }
+    // this stripe's chunks: products and segment bounds staged in shared memory
+    for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
+        const int64_t e0 = chunk_start[c];
+        const int cnt = (int)(chunk_start[c + 1] - e0);
+        const int64_t sg0 = cfirst[c];
+        const int ns = (int)(cfirst[c + 1] - sg0);
+        for (int q = threadIdx.x; q < ns; q += kThreads) sbnd[q] = (int)(seg_start[sg0 + q] - e0);
+        if (threadIdx.x == 0) sbnd[ns] = cnt;
+#pragma unroll 8
         for (int k = threadIdx.x; k < cnt; k += kThreads) {
             const RemRec<W> r = hrec[e0 + k];
             vals[k] = A[r.src] * rec_w(r);
         }
         __syncthreads();
-        const int64_t s1 = cfirst[c + 1];
-        for (int64_t s = cfirst[c] + w; s < s1; s += kWarps) {
-            const int b = (int)(seg_start[s] - e0), e = (int)(seg_start[s + 1] - e0);
+        for (int q = (int)w; q < ns; q += kWarps) {
+            const int b = sbnd[q], e = sbnd[q + 1];
             double acc = 0.0;
             for (int k = b + (int)lane; k < e; k += 32) acc += vals[k];
             acc = warp_sum(acc);
-            if (lane == 0) part[s] = acc;
+            if (lane == 0) part[sg0 + q] = acc;
         }
         __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_heavy_fix(const int64_t *__restrict__ hfirst, int64_t nh,
-                                                        const double *__restrict__ part, double *__restrict__ hsum,
-                                                        const Ctrl *__restrict__ ctrl, int force) {
-    if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
-    if (!ctrl->gather) return;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t h = warp; h < nh; h += nw) {
-        const int64_t s0 = hfirst[h], s1 = hfirst[h + 1];
-        double acc = 0.0;
-        for (int64_t s = s0 + lane_id(); s < s1; s += 32) acc += part[s];
-        acc = warp_sum(acc);
-        if (lane_id() == 0) hsum[h] = acc;
     }
 }
 
 // ---------------------------------------------------------------- tile kernel
 template <typename W>
 struct TileArgs {
-    const uint32_t *lrel, *rrel;
+    const uint16_t *lperm;
+    const uint32_t *wofs, *rrel;
     const int32_t *hidx, *deg;
     const float *wr;
     const double *inv;
@@ -439,26 +655,31 @@ struct TileArgs {
     int64_t edge_cap;        // bytes of shared memory for the staged local edges
 };
 
+// one target's local pushes in its sliced-ELL column: slots base, base+32, ...
+// (coalesced across the warp), sources in ascending order (Eq. (8) order)
 template <typename W>
-__device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> *ew, const double *gq, int kb, int ke) {
+__device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> *ew, const double *gq, int base,
+                                            int K) {
     constexpr bool kW = !std::is_same<W, NoW>::value;
     double acc = 0.0;
-    int k = kb;
-    for (; k + 4 <= ke; k += 4) {
-        const int s0 = es[k], s1 = es[k + 1], s2 = es[k + 2], s3 = es[k + 3];
+    int s = 0;
+    for (; s + 4 <= K; s += 4) {
+        const int k = base + 32 * s;
+        const int s0 = es[k], s1 = es[k + 32], s2 = es[k + 64], s3 = es[k + 96];
         double v0 = gq[s0], v1 = gq[s1], v2 = gq[s2], v3 = gq[s3];
         if constexpr (kW) {
             v0 *= (double)ew[k];
-            v1 *= (double)ew[k + 1];
-            v2 *= (double)ew[k + 2];
-            v3 *= (double)ew[k + 3];
+            v1 *= (double)ew[k + 32];
+            v2 *= (double)ew[k + 64];
+            v3 *= (double)ew[k + 96];
         }
         acc += v0;
         acc += v1;
         acc += v2;
         acc += v3;
     }
-    for (; k < ke; ++k) {
+    for (; s < K; ++s) {
+        const int k = base + 32 * s;
         double v = gq[es[k]];
         if constexpr (kW) v *= (double)ew[k];
         acc += v;
@@ -467,15 +688,20 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
 }
 
 template <typename W>
+constexpr int tile_fixed_smem() {
+    return (2 * (int)kNodeTile + 2) * 8 + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
+}
+
+template <typename W>
 __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool kW = !std::is_same<W, NoW>::value;
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     constexpr int kRS = (int)sizeof(RemRec<W>);
-    constexpr int kRecBytes = (int)kLightCap * kRS + 32;
-    double *gq = reinterpret_cast<double *>(smem);                       // [kNodeTile]
-    unsigned char *rbuf = smem + kNodeTile * sizeof(double);             // light records (16-B aligned)
-    unsigned char *ebuf = rbuf + kRecBytes;                              // local edges (16-B aligned)
+    double *gq = reinterpret_cast<double *>(smem);                       // [kNodeTile + 2]: outflow, zero pad slot
+    double *fs = gq + kNodeTile + 2;                                     // [kNodeTile]: round results by node
+    unsigned char *rbuf = reinterpret_cast<unsigned char *>(fs + kNodeTile);   // light records (16-B aligned)
+    unsigned char *ebuf = smem + tile_fixed_smem<W>();                   // local edges (16-B aligned)
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double s_r[kTileWarps], s_l[kTileWarps];
     __shared__ unsigned long long s_c[kTileWarps][2];
@@ -488,7 +714,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     const double *__restrict__ Aprev = (sw & 1) ? a.A0 : a.A1;
     const uint32_t barp = smem_u32(&bar);
     const int i = threadIdx.x;
+    const int lane = i & 31, wp = i >> 5;
     if (i == 0) {
+        gq[kNodeTile] = 0.0;                         // padding slots read this
+        gq[kNodeTile + 1] = 0.0;
         mbar_init(barp, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -496,11 +725,17 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     uint32_t phase = 0;
     double resid = 0.0, leak = 0.0;
     unsigned long long nodes = 0, edges = 0;
+    // tile scalars, loaded one tile ahead
+    int64_t nl0 = 0, nl1 = 0, nr0 = 0, nr1 = 0;
+    if (blockIdx.x < a.ntile) {
+        nl0 = a.ltile[blockIdx.x], nl1 = a.ltile[blockIdx.x + 1];
+        nr0 = a.rtile[blockIdx.x], nr1 = a.rtile[blockIdx.x + 1];
+    }
     for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
         const int64_t a0 = tile * kNodeTile;
         const int nn = (int)min(kNodeTile, a.n - a0);
-        const int64_t l0 = a.ltile[tile], l1 = a.ltile[tile + 1];
-        const int64_t r0 = gather ? a.rtile[tile] : 0, r1 = gather ? a.rtile[tile + 1] : 0;
+        const int64_t l0 = nl0, l1 = nl1;
+        const int64_t r0 = gather ? nr0 : 0, r1 = gather ? nr1 : 0;
         // aligned byte supersets of the tile's ranges
         const int64_t rb0 = (r0 * kRS) & ~int64_t(15), rb1 = (r1 * kRS + 15) & ~int64_t(15);
         const int64_t sb0 = (l0 * 2) & ~int64_t(15), sb1 = (l1 * 2 + 15) & ~int64_t(15);
@@ -529,15 +764,18 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
         const int64_t j = a0 + i;
         double Fi = 0.0, Hi = 0.0, ivi = 0.0, hs = 0.0;
         float wri = 0.f;
-        int dgi = 0, lb = 0, le = 0, rb = 0, re = 0;
+        int dgi = 0, rb = 0, re = 0;
+        // sliced-ELL role: this thread computes the local pushes into node pk
+        const int pk = a.lperm[a0 + i];
+        const uint32_t wo0 = a.wofs[tile * (kTileWarps + 1) + wp];
+        const int K = (int)((a.wofs[tile * (kTileWarps + 1) + wp + 1] - wo0) >> 5);
+        const int base = (int)wo0 + lane;
         if (valid) {
             Fi = a.F[j];
             Hi = a.H[j];
             ivi = a.inv[j];
             dgi = a.deg[j];
             wri = a.wr[j];
-            lb = (int)a.lrel[j];
-            le = i + 1 < nn ? (int)a.lrel[j + 1] : (int)(l1 - l0);
             if (gather) {
                 rb = (int)a.rrel[j];
                 re = i + 1 < nn ? (int)a.rrel[j + 1] : (int)(r1 - r0);
@@ -583,12 +821,21 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
             }
             gq[i] = q;
             __syncthreads();
-            if (valid) f = local_sum<W>(es, ew, gq, lb, le);   // Eq. (8) local pushes, edge order
+            if (pk < nn) fs[pk] = local_sum<W>(es, ew, gq, base, K);   // Eq. (8) local pushes into pk
             __syncthreads();
+            f = fs[i];
         }
-        // 3. state out
+        // next tile's scalars, in flight during the epilogue
+        {
+            const int64_t nt = tile + gridDim.x;
+            if (nt < a.ntile) {
+                nl0 = a.ltile[nt], nl1 = a.ltile[nt + 1];
+                nr0 = a.rtile[nt], nr1 = a.rtile[nt + 1];
+            }
+        }
+        // 3. state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
         if (valid) {
-            const double An = d * D * ivi;           // remote pushes, completed by the next sweep
+            const double An = d * D * ivi;
             a.F[j] = f;
             if (D != 0.0) a.H[j] = Hi + D;
             Anext[j] = An;
@@ -674,7 +921,8 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     State &s = h->s;
     TilePlan &tp = g.tl;
     TileArgs<W> a;
-    a.lrel = tp.lrel;
+    a.lperm = tp.lperm;
+    a.wofs = tp.wofs;
     a.rrel = tp.rrel;
     a.hidx = tp.hidx;
     a.deg = tp.deg;
@@ -699,17 +947,24 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     return a;
 }
 
+// the heavy targets' remote inflow hsum: one launch per stripe + the last fold
 template <typename W>
 static void launch_heavy_t(di_graph *h, int force) {
     TilePlan &tp = h->g.tl;
     State &s = h->s;
     if (tp.nh == 0) return;
-    const int grid = (int)std::min<int64_t>(tp.nchunk, (int64_t)h->num_sms * 8);
-    k_heavy<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.mh, tp.nchunk, tp.seg_start, tp.cfirst,
-                                                 s.A, s.A2, tp.part, s.ctrl, force);
-    k_heavy_fix<<<(unsigned)std::min<int64_t>((tp.nh + kWarps - 1) / kWarps, (int64_t)h->num_sms * 8), kThreads, 0,
-                  h->stream>>>(tp.hfirst, tp.nh, tp.part, tp.hsum, s.ctrl, force);
-    count_launch(2);
+    const int64_t S = (int64_t)tp.s_chunk.size() - 1;
+    for (int64_t st = 0; st <= S; ++st) {
+        const int64_t c0 = st < S ? tp.s_chunk[st] : 0, c1 = st < S ? tp.s_chunk[st + 1] : 0;
+        const int64_t q0 = st > 0 ? tp.s_run[st - 1] : 0, q1 = st > 0 ? tp.s_run[st] : 0;
+        const int64_t work = std::max<int64_t>(c1 - c0, (q1 - q0 + 255) / 256);
+        if (work == 0) continue;
+        const int grid = (int)std::min<int64_t>(work, (int64_t)h->num_sms * 8);
+        k_heavy_s<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
+                                                       tp.cfirst, c0, c1, tp.run_h, tp.run_seg, q0, q1, s.A, s.A2,
+                                                       tp.part, tp.hsum, s.ctrl, force);
+        count_launch();
+    }
 }
 
 template <typename W>
@@ -727,7 +982,7 @@ static void launch_tile_t(di_graph *h, int rounds) {
     cudaFuncAttributes fa;
     DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    const int64_t fixed = kNodeTile * (int64_t)sizeof(double) + (int64_t)kLightCap * sizeof(RemRec<W>) + 32;
+    const int64_t fixed = tile_fixed_smem<W>();
     const int64_t budget = (int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes;
     const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
     int64_t cap = (budget - fixed) & ~int64_t(15);
