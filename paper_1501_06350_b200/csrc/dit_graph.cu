@@ -82,7 +82,7 @@ static void launch_scales(di_graph *h, const unsigned char *only) {
 
 void build_scales(di_graph *h) {
     DevGraph &g = h->g;
-    if (!g.inv) DI_CUDA(cudaMalloc(&g.inv, (g.n > 0 ? g.n : 1) * sizeof(double)));
+    if (!g.inv) DI_CUDA(cudaMalloc(&g.inv, (g.n > 0 ? g.n : 1) * sizeof(double) + 16));   // +16: TMA tile rows
     launch_scales(h, nullptr);
 }
 

@@ -95,12 +95,17 @@ struct TilePlan {
     int32_t *deg = nullptr;        // out-degree (diffused-edge accounting)
     // per tile [ntile+1]
     int64_t *ltile = nullptr, *rtile = nullptr;
-    // local in-edges in a sliced-ELL layout per tile: the tile's targets are
-    // ranked by local in-degree (lperm: rank -> node, descending degree); warp w
-    // of the tile kernel takes ranks [32w, 32w+32) and slot s of lane l sits at
-    // ltile[t] + wofs[t*17+w] + 32 s + l (padding: source kNodeTile, weight 0)
-    uint16_t *lperm = nullptr;     // [ntile*kNodeTile]
-    uint32_t *wofs = nullptr;      // [ntile*17] slot offset of each warp, relative to ltile[t]
+    // local in-edges in a balanced sliced-ELL layout per tile: each target's
+    // local in-edge list is cut into pieces of <= cap edges (cap chosen so the
+    // tile has <= 2 x kNodeTile pieces); pieces are ranked by length (longest
+    // first) and cut into 32 virtual warps of 32; real warp w runs virtual
+    // warps w and 31-w (longest with shortest).  Slot s of the piece of rank r
+    // sits at ltile[t] + vofs[t*33 + r/32] + 32 s + r%32 (padding: source
+    // kNodeTile, weight 0).  A target's pieces, in edge order, are the ranks
+    // plist[t*1024 + vfirst[t*513 + i] ...  vfirst[t*513 + i + 1]).
+    uint32_t *vofs = nullptr;      // [ntile*33]
+    uint16_t *vfirst = nullptr;    // [ntile*513]
+    uint16_t *plist = nullptr;     // [ntile*1024]
     uint16_t *lsrc = nullptr;      // [mpad] source - tile base (+16 B for aligned TMA supersets)
     void *lw = nullptr;            // [mpad] raw weight (graph storage kind) or null
     int64_t mloc = 0, mpad = 0;    // local in-edges, padded slots

@@ -287,8 +287,8 @@ void ensure_state(di_graph *h) {
     const int64_t n = h->g.n;
     if (s.F) return;
     const int64_t nn = n > 0 ? n : 1;
-    DI_CUDA(cudaMalloc(&s.F, (h->g.nt > 0 ? h->g.nt : 1) * sizeof(double)));
-    DI_CUDA(cudaMalloc(&s.H, nn * sizeof(double)));
+    DI_CUDA(cudaMalloc(&s.F, (h->g.nt > 0 ? h->g.nt : 1) * sizeof(double) + 16));   // +16: TMA tile rows
+    DI_CUDA(cudaMalloc(&s.H, nn * sizeof(double) + 16));
     s.ent_cap = n + h->g.m / kSplit + 1;
     DI_CUDA(cudaMalloc(&s.ent, s.ent_cap * sizeof(uint4)));
     DI_CUDA(cudaMalloc(&s.ctrl, sizeof(Ctrl)));

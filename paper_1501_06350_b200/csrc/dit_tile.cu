@@ -39,12 +39,18 @@
 #include "dit_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // thread i owns node i of the tile
 constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kVRows = 2 * (int)kNodeTile;       // local-edge pieces per tile (at most)
+constexpr int kVWarps = kVRows / 32;             // virtual warps: real warp w runs w and kVWarps-1-w
+constexpr int kVofsStride = 36;                  // u32 per tile (kVWarps + 1, padded to 16 B)
+constexpr int kVfStride = 520;                   // u16 per tile (kNodeTile + 1, padded to 16 B)
+static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per warp");
 
 template <typename W>
 using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
@@ -140,36 +146,61 @@ __global__ void k_classify(const int64_t *__restrict__ rc, int64_t n, int64_t nt
     }
 }
 
-// rank the tile's targets by local in-degree (descending, ties by id) and
-// lay out the sliced-ELL warp offsets; CTA per tile
-__global__ void __launch_bounds__(kTileThreads) k_tile_rank(const int64_t *__restrict__ lc, int64_t n, int64_t ntile,
-                                                             uint16_t *__restrict__ lperm, int32_t *__restrict__ rank,
-                                                             uint32_t *__restrict__ wofs, int64_t *__restrict__ pcnt) {
-    __shared__ int64_t deg_s[kNodeTile];
-    __shared__ uint16_t perm_s[kNodeTile];
+// balanced sliced-ELL layout of a tile's local in-edges: CTA per tile
+__global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__restrict__ lc, int64_t n,
+                                                               int64_t ntile, uint32_t *__restrict__ vofs,
+                                                               uint16_t *__restrict__ vfirst,
+                                                               uint16_t *__restrict__ plist, int32_t *__restrict__ vcap,
+                                                               int64_t *__restrict__ pcnt) {
+    __shared__ int64_t d_s[kNodeTile];
+    __shared__ int32_t len_s[kVRows], lenr_s[kVRows];
+    __shared__ uint16_t vf_s[kNodeTile + 1], rank_s[kVRows];
+    __shared__ int s_V;
     const int k = threadIdx.x;
     for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
         const int64_t a0 = t * kNodeTile;
         const int nn = (int)min(kNodeTile, n - a0);
-        const int64_t dk = k < nn ? lc[a0 + k] : 0;
-        deg_s[k] = dk;
+        d_s[k] = k < nn ? lc[a0 + k] : 0;
         __syncthreads();
-        int r = 0;
-        for (int j = 0; j < (int)kNodeTile; ++j) {
-            const int64_t dj = deg_s[j];
-            r += (dj > dk) || (dj == dk && j < k);
+        if (k == 0) {
+            // cap: at most kVRows pieces (E / cap + nonzero rows <= kVRows)
+            int64_t E = 0, nz = 0;
+            for (int i = 0; i < (int)kNodeTile; ++i) {
+                E += d_s[i];
+                nz += d_s[i] > 0;
+            }
+            const int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
+            int V = 0;
+            for (int i = 0; i < (int)kNodeTile; ++i) {
+                vf_s[i] = (uint16_t)V;
+                for (int64_t b = 0; b < d_s[i]; b += cap) len_s[V++] = (int32_t)min(cap, d_s[i] - b);
+            }
+            vf_s[kNodeTile] = (uint16_t)V;
+            s_V = V;
+            vcap[t] = (int32_t)cap;
         }
-        perm_s[r] = (uint16_t)k;
-        if (k < nn) rank[a0 + k] = r;
         __syncthreads();
-        lperm[a0 + k] = perm_s[k];
+        const int V = s_V;
+        for (int p = k; p < V; p += kTileThreads) {   // rank: longest first, ties by piece order
+            const int lp = len_s[p];
+            int r = 0;
+            for (int q = 0; q < V; ++q) {
+                const int lq = len_s[q];
+                r += (lq > lp) || (lq == lp && q < p);
+            }
+            rank_s[p] = (uint16_t)r;
+            lenr_s[r] = lp;
+        }
+        __syncthreads();
+        for (int p = k; p < kVRows; p += kTileThreads) plist[t * kVRows + p] = p < V ? rank_s[p] : 0;
+        for (int i = k; i < kVfStride; i += kTileThreads) vfirst[t * kVfStride + i] = vf_s[min(i, (int)kNodeTile)];
         if (k == 0) {
             uint32_t off = 0;
-            for (int w = 0; w < kTileWarps; ++w) {
-                wofs[t * (kTileWarps + 1) + w] = off;
-                off += 32u * (uint32_t)deg_s[perm_s[32 * w]];   // the warp's largest degree
+            for (int vw = 0; vw < kVWarps; ++vw) {
+                vofs[t * kVofsStride + vw] = off;
+                off += 32u * (uint32_t)(32 * vw < V ? lenr_s[32 * vw] : 0);   // the virtual warp's longest piece
             }
-            wofs[t * (kTileWarps + 1) + kTileWarps] = off;
+            for (int vw = kVWarps; vw < kVofsStride; ++vw) vofs[t * kVofsStride + vw] = off;
             pcnt[t] = off;
         }
         __syncthreads();
@@ -210,7 +241,8 @@ __global__ void k_fill_pad(uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ 
 template <typename W>
 __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *__restrict__ tsrc,
                               const StoreW<W> *__restrict__ tw, int64_t n, const int64_t *__restrict__ ltile,
-                              const uint32_t *__restrict__ wofs, const int32_t *__restrict__ rank,
+                              const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
+                              const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
                               const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
                               const int32_t *__restrict__ hidx, int64_t stripe_nodes, uint16_t *__restrict__ lsrc,
                               StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
@@ -224,9 +256,9 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
         const int64_t b = tptr[t], e = tptr[t + 1];
         const int64_t tile = t / kNodeTile;
         const int32_t hx = hidx[t];
-        // sliced-ELL slots of target t: base + 32 s, s = its s-th local in-edge
-        const int rk = rank[t];
-        const int64_t lbase = ltile[tile] + wofs[tile * (kTileWarps + 1) + rk / 32] + (rk % 32);
+        // balanced sliced-ELL: local in-edge s of t is slot s % cap of its piece s / cap
+        const int64_t cap = vcap[tile];
+        const int pf = vfirst[tile * kVfStride + (t - tile * kNodeTile)];
         int64_t lo = 0;
         int64_t ro = hx >= 0 ? hptr[t] : rptr[t];
         for (int64_t k0 = b; k0 < e; k0 += 32) {
@@ -237,7 +269,9 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
             const unsigned bl = __ballot_sync(0xffffffffu, loc);
             const unsigned br = __ballot_sync(0xffffffffu, ok && !loc);
             if (loc) {
-                const int64_t o = lbase + 32 * (lo + __popc(bl & lt));
+                const int64_t q = lo + __popc(bl & lt);
+                const int r = plist[tile * kVRows + pf + (int)(q / cap)];
+                const int64_t o = ltile[tile] + vofs[tile * kVofsStride + r / 32] + 32 * (q % cap) + (r % 32);
                 lsrc[o] = (uint16_t)(s - tile * kNodeTile);
                 if (kW) lw[o] = tw[k];
             } else if (ok) {
@@ -344,7 +378,7 @@ __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntil
 
 void free_tiles(TilePlan &t) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
-                    (void *)t.lperm, (void *)t.wofs, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
+                    (void *)t.vofs, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
                     (void *)t.hsum})
         cudaFree(p);
@@ -406,15 +440,16 @@ static void build_tiles_t(di_graph *h) {
         throw Fail{DI_ERR_INVALID};
     }
     // ---- sliced-ELL layout of the local in-edges
-    int32_t *rank;
+    int32_t *vcap;
     int64_t *pcnt;
-    DI_CUDA(cudaMallocAsync(&rank, (n > 0 ? n : 1) * sizeof(int32_t), st));
+    DI_CUDA(cudaMallocAsync(&vcap, (tp.ntile + 1) * sizeof(int32_t), st));
     DI_CUDA(cudaMallocAsync(&pcnt, (tp.ntile + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMalloc(&tp.lperm, tp.ntile * kNodeTile * sizeof(uint16_t)));
-    DI_CUDA(cudaMalloc(&tp.wofs, tp.ntile * (kTileWarps + 1) * sizeof(uint32_t)));
+    DI_CUDA(cudaMalloc(&tp.vofs, tp.ntile * kVofsStride * sizeof(uint32_t)));
+    DI_CUDA(cudaMalloc(&tp.vfirst, tp.ntile * kVfStride * sizeof(uint16_t)));
+    DI_CUDA(cudaMalloc(&tp.plist, tp.ntile * kVRows * sizeof(uint16_t)));
     DI_CUDA(cudaMalloc(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t)));
-    k_tile_rank<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
-        lc, n, tp.ntile, tp.lperm, rank, tp.wofs, pcnt);
+    k_tile_layout<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
+        lc, n, tp.ntile, tp.vofs, tp.vfirst, tp.plist, vcap, pcnt);
     count_launch();
     exclusive_scan_i64(pcnt, tp.ltile, tp.ntile, st);
     tp.mpad = read_i64(tp.ltile + tp.ntile, st);
@@ -427,10 +462,10 @@ static void build_tiles_t(di_graph *h) {
         count_launch();
     }
     // ---- per-node arrays, tile bases
-    DI_CUDA(cudaMalloc(&tp.rrel, n * sizeof(uint32_t)));
-    DI_CUDA(cudaMalloc(&tp.hidx, n * sizeof(int32_t)));
-    DI_CUDA(cudaMalloc(&tp.wr, n * sizeof(float)));
-    DI_CUDA(cudaMalloc(&tp.deg, n * sizeof(int32_t)));
+    DI_CUDA(cudaMalloc(&tp.rrel, n * sizeof(uint32_t) + 16));
+    DI_CUDA(cudaMalloc(&tp.hidx, n * sizeof(int32_t) + 16));
+    DI_CUDA(cudaMalloc(&tp.wr, n * sizeof(float) + 16));
+    DI_CUDA(cudaMalloc(&tp.deg, n * sizeof(int32_t) + 16));
     DI_CUDA(cudaMalloc(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t)));
     k_tile_rel<<<grid_for(h, n + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, tp.ntile, tp.rrel, tp.hidx, tp.deg,
                                                    tp.rtile);
@@ -444,7 +479,8 @@ static void build_tiles_t(di_graph *h) {
     uint32_t *k0, *v0, *k1, *v1, *hof, *hh;
     DI_CUDA(cudaMallocAsync(&htmp, mh1 * rs, st));
     for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
-    k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, tp.ltile, tp.wofs, rank, rptr,
+    k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, tp.ltile, tp.vofs, tp.vfirst,
+                                           tp.plist, vcap, rptr,
                                            hptr, tp.hidx, tp.stripe_nodes, tp.lsrc, (SW *)tp.lw,
                                            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
     count_launch();
@@ -530,7 +566,7 @@ static void build_tiles_t(di_graph *h) {
     for (int64_t *p : {lc, rc, lrc, hc, hflag, rptr, hptr, hpos, pcnt}) DI_CUDA(cudaFreeAsync(p, st));
     for (uint32_t *p : {k0, v0, k1, v1, hof, hh}) DI_CUDA(cudaFreeAsync(p, st));
     DI_CUDA(cudaFreeAsync(htmp, st));
-    DI_CUDA(cudaFreeAsync(rank, st));
+    DI_CUDA(cudaFreeAsync(vcap, st));
     DI_CUDA(cudaFreeAsync(mx, st));
     DI_CUDA(cudaStreamSynchronize(st));
     DI_CUDA(cudaGetLastError());
@@ -624,12 +660,29 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
             vals[k] = A[r.src] * rec_w(r);
         }
         __syncthreads();
-        for (int q = (int)w; q < ns; q += kWarps) {
-            const int b = sbnd[q], e = sbnd[q + 1];
-            double acc = 0.0;
-            for (int k = b + (int)lane; k < e; k += 32) acc += vals[k];
-            acc = warp_sum(acc);
-            if (lane == 0) part[sg0 + q] = acc;
+        // short segments: one thread each; long ones (>= 64 edges): the whole warp
+        for (int q0 = (int)(w * 32); q0 < ns; q0 += kThreads) {
+            const int q = q0 + (int)lane;
+            int b = 0, e = 0;
+            if (q < ns) {
+                b = sbnd[q];
+                e = sbnd[q + 1];
+            }
+            if (e - b < 64 && e > b) {
+                double acc = 0.0;
+                for (int k = b; k < e; ++k) acc += vals[k];
+                part[sg0 + q] = acc;
+            }
+            unsigned big = __ballot_sync(0xffffffffu, e - b >= 64);
+            while (big) {
+                const int l = __ffs(big) - 1;
+                big &= big - 1;
+                const int bb = __shfl_sync(0xffffffffu, b, l), be = __shfl_sync(0xffffffffu, e, l);
+                double acc = 0.0;
+                for (int k = bb + (int)lane; k < be; k += 32) acc += vals[k];
+                acc = warp_sum(acc);
+                if (lane == 0) part[sg0 + q0 + l] = acc;
+            }
         }
         __syncthreads();
     }
@@ -638,8 +691,9 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
 // ---------------------------------------------------------------- tile kernel
 template <typename W>
 struct TileArgs {
-    const uint16_t *lperm;
-    const uint32_t *wofs, *rrel;
+    const uint32_t *vofs;
+    const uint16_t *vfirst, *plist;
+    const uint32_t *rrel;
     const int32_t *hidx, *deg;
     const float *wr;
     const double *inv;
@@ -687,11 +741,85 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     return acc;
 }
 
+constexpr int kMetaBytes = kVofsStride * 4 + kVfStride * 2 + kVRows * 2;   // per-tile layout, TMA-staged
+constexpr int kRecOff = ((int)kNodeTile + 2) * 8 + kVRows * 8 + kMetaBytes;  // light records after gq, psum, meta
+static_assert(kRecOff % 16 == 0 && kMetaBytes % 16 == 0, "16-byte aligned shared buffers");
+
 template <typename W>
 constexpr int tile_fixed_smem() {
-    return (2 * (int)kNodeTile + 2) * 8 + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
+    return kRecOff + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
 }
 
+// One tile's TMA bundle (a buffer of the double-buffered pipeline): the
+// per-node state, the tile's layout, its light records and (when they fit)
+// its local edges.
+constexpr int kNodeBytes = (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
+template <typename W>
+constexpr int tile_buf_fixed() {
+    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
+}
+constexpr int kSharedHead = ((int)kNodeTile + 2) * 8 + kVRows * 8;         // gq, psum
+static_assert(kNodeBytes % 16 == 0 && kSharedHead % 16 == 0, "16-byte aligned shared buffers");
+
+struct TileScalars {
+    int64_t l0, l1, r0, r1;
+};
+
+// thread 0: issue tile `tile`'s bundle into buffer `buf` (bytes counted on `bar`)
+template <typename W>
+__device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *Fsrc, int64_t tile,
+                                           const TileScalars &ts, bool gather, unsigned char *buf,
+                                           uint32_t bar) {
+    constexpr bool kW = !std::is_same<W, NoW>::value;
+    constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
+    constexpr int kRS = (int)sizeof(RemRec<W>);
+    const int64_t a0 = tile * kNodeTile;
+    const int nn = (int)min(kNodeTile, a.n - a0);
+    const uint32_t n8 = (uint32_t)((nn * 8 + 15) & ~15), n4 = (uint32_t)((nn * 4 + 15) & ~15);
+    const int64_t r0 = gather ? ts.r0 : 0, r1 = gather ? ts.r1 : 0;
+    const int64_t rb0 = (r0 * kRS) & ~int64_t(15), rb1 = (r1 * kRS + 15) & ~int64_t(15);
+    const int64_t sb0 = (ts.l0 * 2) & ~int64_t(15), sb1 = (ts.l1 * 2 + 15) & ~int64_t(15);
+    const int64_t wb0 = (ts.l0 * kWB) & ~int64_t(15), wb1 = (ts.l1 * kWB + 15) & ~int64_t(15);
+    const int64_t ebytes = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0);
+    const bool staged = ebytes <= a.edge_cap;
+    uint32_t bytes = 3 * n8 + 4 * n4 + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
+    if (staged) bytes += (uint32_t)ebytes;
+    // order this CTA's earlier generic-proxy accesses of the buffer before the async writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(bar, bytes);
+    unsigned char *p = buf;
+    const uint32_t sb = smem_u32(buf);
+    tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
+    tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
+    tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
+    const uint32_t q = 3 * kNodeTile * 8;
+    tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
+    tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
+    tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
+    tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
+    const uint32_t m = kNodeBytes;
+    tma_load(sb + m, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
+    tma_load(sb + m + kVofsStride * 4, a.vfirst + tile * kVfStride, kVfStride * 2, bar);
+    tma_load(sb + m + kVofsStride * 4 + kVfStride * 2, a.plist + tile * kVRows, kVRows * 2, bar);
+    const uint32_t rofs = kNodeBytes + kMetaBytes;
+    if (rb1 > rb0)
+        tma_load(sb + rofs, reinterpret_cast<const unsigned char *>(a.rrec) + rb0, (uint32_t)(rb1 - rb0), bar);
+    const uint32_t eofs = tile_buf_fixed<W>();
+    if (!staged) {                                   // rounds read them from global: bring them to L2 now
+        if (sb1 > sb0) tma_prefetch_l2(reinterpret_cast<const unsigned char *>(a.lsrc) + sb0, (uint32_t)(sb1 - sb0));
+        if (kW && wb1 > wb0) tma_prefetch_l2(reinterpret_cast<const unsigned char *>(a.lw) + wb0, (uint32_t)(wb1 - wb0));
+    }
+    if (staged) {
+        if (sb1 > sb0) tma_load(sb + eofs, reinterpret_cast<const unsigned char *>(a.lsrc) + sb0, (uint32_t)(sb1 - sb0), bar);
+        if (kW && wb1 > wb0)
+            tma_load(sb + eofs + (uint32_t)(sb1 - sb0), reinterpret_cast<const unsigned char *>(a.lw) + wb0,
+                     (uint32_t)(wb1 - wb0), bar);
+    }
+    (void)p;
+}
+
+// Persistent kernel, one 512-thread CTA per SM, tiles round-robin; the next
+// tile's bundle streams in (TMA) while the current tile gathers and diffuses.
 template <typename W>
 __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -699,10 +827,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     constexpr int kRS = (int)sizeof(RemRec<W>);
     double *gq = reinterpret_cast<double *>(smem);                       // [kNodeTile + 2]: outflow, zero pad slot
-    double *fs = gq + kNodeTile + 2;                                     // [kNodeTile]: round results by node
-    unsigned char *rbuf = reinterpret_cast<unsigned char *>(fs + kNodeTile);   // light records (16-B aligned)
-    unsigned char *ebuf = smem + tile_fixed_smem<W>();                   // local edges (16-B aligned)
-    __shared__ __align__(8) unsigned long long bar;
+    double *psum = gq + kNodeTile + 2;                                   // [kVRows]: piece sums by rank
+    const int bufsz = (int)(tile_buf_fixed<W>() + a.edge_cap);
+    __shared__ __align__(8) unsigned long long bars[2];
     __shared__ double s_r[kTileWarps], s_l[kTileWarps];
     __shared__ unsigned long long s_c[kTileWarps][2];
     __shared__ bool s_last;
@@ -712,93 +839,84 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     const unsigned long long sw = ctrl->sweeps;
     double *__restrict__ Anext = (sw & 1) ? a.A1 : a.A0;
     const double *__restrict__ Aprev = (sw & 1) ? a.A0 : a.A1;
-    const uint32_t barp = smem_u32(&bar);
     const int i = threadIdx.x;
     const int lane = i & 31, wp = i >> 5;
+    const int64_t G = gridDim.x;
+    auto scal = [&](int64_t t) {
+        TileScalars ts{0, 0, 0, 0};
+        if (t < a.ntile) ts = TileScalars{a.ltile[t], a.ltile[t + 1], a.rtile[t], a.rtile[t + 1]};
+        return ts;
+    };
+    TileScalars cur = scal(blockIdx.x), nxt = scal(blockIdx.x + G);
     if (i == 0) {
         gq[kNodeTile] = 0.0;                         // padding slots read this
         gq[kNodeTile + 1] = 0.0;
-        mbar_init(barp, 1);
+        mbar_init(smem_u32(&bars[0]), 1);
+        mbar_init(smem_u32(&bars[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < a.ntile)
+            issue_tile<W>(a, a.F, blockIdx.x, cur, gather, smem + kSharedHead, smem_u32(&bars[0]));
     }
     __syncthreads();
-    uint32_t phase = 0;
     double resid = 0.0, leak = 0.0;
     unsigned long long nodes = 0, edges = 0;
-    // tile scalars, loaded one tile ahead
-    int64_t nl0 = 0, nl1 = 0, nr0 = 0, nr1 = 0;
-    if (blockIdx.x < a.ntile) {
-        nl0 = a.ltile[blockIdx.x], nl1 = a.ltile[blockIdx.x + 1];
-        nr0 = a.rtile[blockIdx.x], nr1 = a.rtile[blockIdx.x + 1];
-    }
-    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += G, ++k) {
+        const int b = k & 1;
+        unsigned char *buf = smem + kSharedHead + b * bufsz;
+        // next tile's bundle into the other buffer (freed by the previous iteration)
+        const TileScalars after = scal(tile + 2 * G);
+        if (i == 0 && tile + G < a.ntile)
+            issue_tile<W>(a, a.F, tile + G, nxt, gather, smem + kSharedHead + (b ^ 1) * bufsz,
+                          smem_u32(&bars[b ^ 1]));
         const int64_t a0 = tile * kNodeTile;
         const int nn = (int)min(kNodeTile, a.n - a0);
-        const int64_t l0 = nl0, l1 = nl1;
-        const int64_t r0 = gather ? nr0 : 0, r1 = gather ? nr1 : 0;
-        // aligned byte supersets of the tile's ranges
-        const int64_t rb0 = (r0 * kRS) & ~int64_t(15), rb1 = (r1 * kRS + 15) & ~int64_t(15);
+        const int64_t l0 = cur.l0, l1 = cur.l1;
+        const int64_t r0 = gather ? cur.r0 : 0, r1 = gather ? cur.r1 : 0;
+        const int64_t rb0 = (r0 * kRS) & ~int64_t(15);
         const int64_t sb0 = (l0 * 2) & ~int64_t(15), sb1 = (l1 * 2 + 15) & ~int64_t(15);
         const int64_t wb0 = (l0 * kWB) & ~int64_t(15), wb1 = (l1 * kWB + 15) & ~int64_t(15);
         const bool staged = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0) <= a.edge_cap;
-        if (i == 0) {
-            // order this CTA's earlier generic-proxy accesses of the buffers before the async writes
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            uint32_t bytes = (uint32_t)(rb1 - rb0);
-            if (staged) bytes += (uint32_t)((sb1 - sb0) + (kW ? (wb1 - wb0) : 0));
-            mbar_arrive_tx(barp, bytes);
-            if (rb1 > rb0)
-                tma_load(smem_u32(rbuf), reinterpret_cast<const unsigned char *>(a.rrec) + rb0, (uint32_t)(rb1 - rb0),
-                         barp);
-            if (staged) {
-                if (sb1 > sb0)
-                    tma_load(smem_u32(ebuf), reinterpret_cast<const unsigned char *>(a.lsrc) + sb0,
-                             (uint32_t)(sb1 - sb0), barp);
-                if (kW && wb1 > wb0)
-                    tma_load(smem_u32(ebuf + (sb1 - sb0)), reinterpret_cast<const unsigned char *>(a.lw) + wb0,
-                             (uint32_t)(wb1 - wb0), barp);
-            }
-        }
-        // per-node state into registers while the bulk copies fly
+        const double *Fs = reinterpret_cast<const double *>(buf);
+        const double *Hs = Fs + kNodeTile;
+        const double *Is = Hs + kNodeTile;
+        const int32_t *Ds = reinterpret_cast<const int32_t *>(Is + kNodeTile);
+        const float *Ws = reinterpret_cast<const float *>(Ds + kNodeTile);
+        const uint32_t *Rs = reinterpret_cast<const uint32_t *>(Ws + kNodeTile);
+        const int32_t *Xs = reinterpret_cast<const int32_t *>(Rs + kNodeTile);
+        const uint32_t *vofs_s = reinterpret_cast<const uint32_t *>(buf + kNodeBytes);
+        const uint16_t *vf_s = reinterpret_cast<const uint16_t *>(vofs_s + kVofsStride);
+        const uint16_t *pl_s = vf_s + kVfStride;
+        unsigned char *rbuf = buf + kNodeBytes + kMetaBytes;
+        unsigned char *ebuf = buf + tile_buf_fixed<W>();
+        mbar_wait(smem_u32(&bars[b]), (uint32_t)((k >> 1) & 1));
         const bool valid = i < nn;
         const int64_t j = a0 + i;
-        double Fi = 0.0, Hi = 0.0, ivi = 0.0, hs = 0.0;
-        float wri = 0.f;
-        int dgi = 0, rb = 0, re = 0;
-        // sliced-ELL role: this thread computes the local pushes into node pk
-        const int pk = a.lperm[a0 + i];
-        const uint32_t wo0 = a.wofs[tile * (kTileWarps + 1) + wp];
-        const int K = (int)((a.wofs[tile * (kTileWarps + 1) + wp + 1] - wo0) >> 5);
-        const int base = (int)wo0 + lane;
-        if (valid) {
-            Fi = a.F[j];
-            Hi = a.H[j];
-            ivi = a.inv[j];
-            dgi = a.deg[j];
-            wri = a.wr[j];
-            if (gather) {
-                rb = (int)a.rrel[j];
-                re = i + 1 < nn ? (int)a.rrel[j + 1] : (int)(r1 - r0);
-                const int32_t hx = a.hidx[j];
-                if (hx >= 0) hs = a.hsum[hx];
-            }
+        // 1. remote pushes of the previous sweep: heavy sums, light records -> products in place
+        double hs = 0.0;
+        if (valid && gather) {
+            const int32_t hx = Xs[i];
+            if (hx >= 0) hs = a.hsum[hx];
         }
-        mbar_wait(barp, phase);
-        phase ^= 1u;
-        // 1. remote pushes of the previous sweep: light records -> products in place
         const int R = (int)(r1 - r0);
         RemRec<W> *recs = reinterpret_cast<RemRec<W> *>(rbuf + (r0 * kRS - rb0));
 #pragma unroll 4
-        for (int k = i; k < R; k += kTileThreads) {
-            const RemRec<W> r = recs[k];
-            *reinterpret_cast<double *>(&recs[k]) = Aprev[r.src] * rec_w(r);
+        for (int q = i; q < R; q += kTileThreads) {
+            const RemRec<W> r = recs[q];
+            *reinterpret_cast<double *>(&recs[q]) = Aprev[r.src] * rec_w(r);
         }
         __syncthreads();
-        double f = Fi;
+        double f = 0.0, ivi = 0.0;
+        int dgi = 0;
         if (valid) {
+            ivi = Is[i];
+            dgi = Ds[i];
             double s = 0.0;
-            for (int k = rb; k < re; ++k) s += *reinterpret_cast<const double *>(&recs[k]);
-            f = Fi + s + hs;
+            if (gather) {
+                const int rb = (int)Rs[i], re = i + 1 < nn ? (int)Rs[i + 1] : R;
+                for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
+            }
+            f = Fs[i] + s + hs;
         }
         // 2. local diffusion rounds in shared memory
         const uint16_t *es;
@@ -821,28 +939,34 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
             }
             gq[i] = q;
             __syncthreads();
-            if (pk < nn) fs[pk] = local_sum<W>(es, ew, gq, base, K);   // Eq. (8) local pushes into pk
+            // Eq. (8) local pushes: this warp's two virtual warps of pieces (longest with shortest)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int vw = h2 ? kVWarps - 1 - wp : wp;
+                const uint32_t o0 = vofs_s[vw];
+                const int K = (int)((vofs_s[vw + 1] - o0) >> 5);
+                if (K) psum[vw * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
+            }
             __syncthreads();
-            f = fs[i];
-        }
-        // next tile's scalars, in flight during the epilogue
-        {
-            const int64_t nt = tile + gridDim.x;
-            if (nt < a.ntile) {
-                nl0 = a.ltile[nt], nl1 = a.ltile[nt + 1];
-                nr0 = a.rtile[nt], nr1 = a.rtile[nt + 1];
+            if (valid) {                              // the node's pieces, in edge order
+                const int p0 = vf_s[i], p1 = vf_s[i + 1];
+                double acc = 0.0;
+                for (int p = p0; p < p1; ++p) acc += psum[pl_s[p]];
+                f = acc;
             }
         }
         // 3. state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
         if (valid) {
             const double An = d * D * ivi;
             a.F[j] = f;
-            if (D != 0.0) a.H[j] = Hi + D;
+            if (D != 0.0) a.H[j] = Hs[i] + D;
             Anext[j] = An;
-            resid += fabs(f) + fabs(An) * (double)wri;
+            resid += fabs(f) + fabs(An) * (double)Ws[i];
             if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
         }
-        __syncthreads();                             // buffers free for the next tile's copies
+        cur = nxt;
+        nxt = after;
+        __syncthreads();                             // buffer b free for the bundle after next
     }
     // CTA partials (fixed order) and the last-block end of the sweep
     resid = warp_sum(resid);
@@ -860,11 +984,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     if (threadIdx.x == 0) {
         double rr = 0.0, ll = 0.0;
         unsigned long long x = 0, y = 0;
-        for (int k = 0; k < kTileWarps; ++k) {
-            rr += s_r[k];
-            ll += s_l[k];
-            x += s_c[k][0];
-            y += s_c[k][1];
+        for (int q = 0; q < kTileWarps; ++q) {
+            rr += s_r[q];
+            ll += s_l[q];
+            x += s_c[q][0];
+            y += s_c[q][1];
         }
         a.part[blockIdx.x] = rr;
         a.part[gridDim.x + blockIdx.x] = ll;
@@ -881,9 +1005,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     __threadfence();
     const volatile double *vp = a.part;
     double r = 0.0, lk = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-        r += vp[b];
-        lk += vp[gridDim.x + b];
+    for (unsigned bb = 0; bb < gridDim.x; ++bb) {
+        r += vp[bb];
+        lk += vp[gridDim.x + bb];
     }
     end_sweep(ctrl, lk);
     ctrl->gather = 1;                                // this sweep's remote pushes are pending in A
@@ -921,8 +1045,9 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     State &s = h->s;
     TilePlan &tp = g.tl;
     TileArgs<W> a;
-    a.lperm = tp.lperm;
-    a.wofs = tp.wofs;
+    a.vofs = tp.vofs;
+    a.vfirst = tp.vfirst;
+    a.plist = tp.plist;
     a.rrel = tp.rrel;
     a.hidx = tp.hidx;
     a.deg = tp.deg;
@@ -947,6 +1072,17 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     return a;
 }
 
+// resident CTAs of k_heavy_s per SM: its grids are exactly one wave
+template <typename W>
+static int heavy_ctas_per_sm() {
+    static int v = 0;
+    if (!v) {
+        DI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_heavy_s<W>, kThreads, 0));
+        if (v < 1) v = 1;
+    }
+    return v;
+}
+
 // the heavy targets' remote inflow hsum: one launch per stripe + the last fold
 template <typename W>
 static void launch_heavy_t(di_graph *h, int force) {
@@ -959,7 +1095,7 @@ static void launch_heavy_t(di_graph *h, int force) {
         const int64_t q0 = st > 0 ? tp.s_run[st - 1] : 0, q1 = st > 0 ? tp.s_run[st] : 0;
         const int64_t work = std::max<int64_t>(c1 - c0, (q1 - q0 + 255) / 256);
         if (work == 0) continue;
-        const int grid = (int)std::min<int64_t>(work, (int64_t)h->num_sms * 8);
+        const int grid = (int)std::min<int64_t>(work, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
         k_heavy_s<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
                                                        tp.cfirst, c0, c1, tp.run_h, tp.run_seg, q0, q1, s.A, s.A2,
                                                        tp.part, tp.hsum, s.ctrl, force);
@@ -976,18 +1112,19 @@ static void launch_tile_t(di_graph *h, int rounds) {
     launch_heavy_t<W>(h, 0);
     mark_event(h, k, 1);
     mark_event(h, k, 2);
-    // two CTAs per SM: each takes half of the SM's shared memory
+    // two CTAs per SM, each with the shared head (gq, psum) and two bundle buffers
     int per_sm = 0;
     DI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
     cudaFuncAttributes fa;
     DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    const int64_t fixed = tile_fixed_smem<W>();
-    const int64_t budget = (int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes;
+    const int64_t fixed = tile_buf_fixed<W>();
+    const int64_t budget = ((int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
     const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
-    int64_t cap = (budget - fixed) & ~int64_t(15);
+    int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
     cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
-    const size_t smem = (size_t)(fixed + cap);
+    if (getenv("DIT_NO_EDGE_STAGING")) cap = 0;
+    const size_t smem = (size_t)(kSharedHead + 2 * (fixed + cap));
     DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TileArgs<W> a = tile_args<W>(h, rounds);
     a.edge_cap = cap;
