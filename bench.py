@@ -39,8 +39,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2)
-    p.add_argument("--variant", default="auto", choices=["auto", "push", "pull", "tiled"])
-    p.add_argument("--rounds", type=int, default=4, help="local rounds per sweep (variant tiled)")
+    p.add_argument("--variant", default="tiled", choices=["auto", "push", "pull", "tiled"])
+    p.add_argument("--rounds", type=int, default=3, help="local rounds per sweep (variant tiled)")
     p.add_argument("--theta", type=float, default=1.0)
     p.add_argument("--tol", type=float, default=None)
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -116,18 +116,36 @@ def workload_name(spec, cfg):
 
 
 # ------------------------------------------------------------------ CPU oracle
-def oracle_sweeps(spec, g, sweeps):
+TILE_NODES = 512   # include/dit.h DI_TILE_NODES (the oracle takes the tile as a parameter)
+
+
+def oracle_run(args, spec, cols, n, sweeps):
     """The CPU oracle (oracle/, test infrastructure) timed as it stands: `sweeps`
-    frontier sweeps from the cold start F_0 = (1-d)Z, single-threaded C."""
+    sweeps of the same schedule as the GPU arm (tiled: orc_tiled_sweep_run with
+    the same tile and rounds; else the theta frontier sweep) from the cold start
+    F_0 = (1-d)Z, single-threaded C.  Returns (diffused edges, seconds)."""
     from oracle import di as odi
-    from oracle import graph as ograph
-    cp, ri, pv = ograph.column_entries(g.n, g.row_ptr, g.col, g.w)
-    st_F = np.full(g.n, (1 - spec.d) / g.n)
-    st_H = np.zeros(g.n)
+    cp, ri, pv = cols
+    F = np.full(n, (1 - spec.d) / n)
+    H = np.zeros(n)
     t0 = time.perf_counter()
-    r = odi.sweep_run(g.n, cp, ri, pv, spec.d, st_F, st_H, theta=1.0, tol=0.0, max_sweeps=sweeps)
-    dt = time.perf_counter() - t0
-    return r.edges, dt, (cp, ri, pv)
+    if args.variant == "tiled":
+        r = odi.tiled_sweep_run(n, cp, ri, pv, spec.d, F, H, tile=TILE_NODES, rounds=args.rounds, tol=0.0,
+                                max_sweeps=sweeps)
+    else:
+        r = odi.sweep_run(n, cp, ri, pv, spec.d, F, H, theta=args.theta, tol=0.0, max_sweeps=sweeps)
+    return r.edges, time.perf_counter() - t0
+
+
+def oracle_cols(g):
+    from oracle import graph as ograph
+    return ograph.column_entries(g.n, g.row_ptr, g.col, g.w)
+
+
+def oracle_desc(args, sweeps):
+    sched = (f"tiled sweep (tile {TILE_NODES}, {args.rounds} rounds)" if args.variant == "tiled"
+             else f"theta={args.theta} frontier sweep")
+    return f"first {sweeps} {sched} sweep(s) of the cold solve on the full graph, single-threaded C oracle"
 
 
 def run_reference(args):
@@ -136,28 +154,23 @@ def run_reference(args):
         return 0
     spec = spec_for(args)
     g = synth.generate(spec)
-    from oracle import di as odi
-    from oracle import graph as ograph
-    cp, ri, pv = ograph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    cols = oracle_cols(g)
     sweeps = 1 if g.m > 50_000_000 else 5
     times, edges = [], []
     for it in range(args.warmup + args.steps):
-        F = np.full(g.n, (1 - spec.d) / g.n)
-        H = np.zeros(g.n)
-        t0 = time.perf_counter()
-        r = odi.sweep_run(g.n, cp, ri, pv, spec.d, F, H, theta=1.0, tol=0.0, max_sweeps=sweeps)
-        dt = time.perf_counter() - t0
+        e, dt = oracle_run(args, spec, cols, g.n, sweeps)
         if it >= args.warmup:
             times.append(dt)
-            edges.append(r.edges)
+            edges.append(e)
     tot = sum(times)
     value = sum(edges) / tot
-    sample = (f"first {sweeps} frontier sweep(s) from the cold start per step, full graph "
-              f"n={g.n} m={g.m}; single-threaded C oracle")
+    sample = oracle_desc(args, sweeps) + f" per step; n={g.n} m={g.m}"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_name(spec, args.config), "n": g.n, "m": g.m},
+            "data": "synthetic", "config": {"workload": workload_name(spec, args.config), "n": g.n, "m": g.m,
+                                            "variant": args.variant, "local_rounds": args.rounds,
+                                            "theta": args.theta},
             "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -274,10 +287,9 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu:
         sw = 1 if g.m > 50_000_000 else 5
-        ce, cdt, _ = oracle_sweeps(spec, g, sw)
+        ce, cdt = oracle_run(args, spec, oracle_cols(g), g.n, sw)
         cpu = {"value": ce / cdt, "unit": "edges/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {sw} frontier sweep(s) of the cold solve on the full graph "
-                         f"({ce} diffused edges, {cdt:.1f} s, single-threaded C oracle)"}
+               "sample": oracle_desc(args, sw) + f" ({ce} diffused edges, {cdt:.1f} s)"}
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "time_to_tol_s": total_ms / args.steps / 1e3,

@@ -84,7 +84,7 @@ typedef struct {
     int32_t dangling;    /* DI_DANGLING_*, default DI_DANGLING_DROP */
     int64_t max_sweeps;  /* stop after this many sweeps even if |F|_1 > tol; <= 0: 10^7 */
     double  pull_frac;   /* AUTO: use pull when frontier out-edges > pull_frac * m; default 0.25 */
-    int32_t local_rounds;/* TILED: diffusion rounds per tile per sweep (>= 1), default 4 */
+    int32_t local_rounds;/* TILED: diffusion rounds per tile per sweep (>= 1), default 3 */
     int32_t reserved;
 } di_solve_opts;
 

@@ -171,7 +171,7 @@ def di_graph_info(h):
 
 
 def _opts(theta=1.0, variant=DI_VARIANT_AUTO, dangling=DI_DANGLING_DROP, max_sweeps=0, pull_frac=0.25,
-          local_rounds=4):
+          local_rounds=3):
     o = di_solve_opts_default()
     o.theta, o.variant, o.dangling, o.max_sweeps, o.pull_frac = theta, variant, dangling, max_sweeps, pull_frac
     o.local_rounds = local_rounds

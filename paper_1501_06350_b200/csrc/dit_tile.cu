@@ -1112,20 +1112,28 @@ static void launch_tile_t(di_graph *h, int rounds) {
     launch_heavy_t<W>(h, 0);
     mark_event(h, k, 1);
     mark_event(h, k, 2);
-    // two CTAs per SM, each with the shared head (gq, psum) and two bundle buffers
-    int per_sm = 0;
-    DI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
-    cudaFuncAttributes fa;
-    DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    const int64_t fixed = tile_buf_fixed<W>();
-    const int64_t budget = ((int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
-    const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
-    int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
-    cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
-    if (getenv("DIT_NO_EDGE_STAGING")) cap = 0;
-    const size_t smem = (size_t)(kSharedHead + 2 * (fixed + cap));
-    DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!tp.tile_smem) {
+        // two CTAs per SM, each with the shared head (gq, psum) and two bundle
+        // buffers; computed (and the attribute set) once per plan, off the sweep path
+        int per_sm = 0;
+        DI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
+        cudaFuncAttributes fa;
+        DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
+        constexpr bool kW = !std::is_same<W, NoW>::value;
+        const int64_t fixed = tile_buf_fixed<W>();
+        const int64_t budget = ((int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
+        const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
+        int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
+        cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
+        // local edges are read from L1/L2 in the rounds (prefetched to L2 with the
+        // bundle): measured faster than staging the few tiles that fit
+        if (!getenv("DIT_EDGE_STAGING")) cap = 0;
+        tp.edge_cap = cap;
+        tp.tile_smem = (size_t)(kSharedHead + 2 * (fixed + cap));
+        DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
+    }
+    const int64_t cap = tp.edge_cap;
+    const size_t smem = tp.tile_smem;
     TileArgs<W> a = tile_args<W>(h, rounds);
     a.edge_cap = cap;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 2));

@@ -243,10 +243,38 @@ def test_config1_full_size(eng):
     spec = synth.CONFIGS[1]
     g = synth.generate(spec)
     r = oracle_solve(g, tol=1e-12)
-    for variant in ("push", "auto"):
-        G, H, res = gpu_solve(eng, g, tol=1e-12, variant=variant)
+    for variant in ("push", "auto", "tiled"):
+        G, H, res = gpu_solve(eng, g, tol=1e-12, variant=variant, local_rounds=3)
+        assert res["converged"]
         assert np.abs(H - r.H).sum() <= L1_BAR
         assert_topk(H, r.H, 1000, 2 * (res["bound"] + r.residual / (1 - D)))
+
+
+def test_config4_full_size_update(eng):
+    # BASELINE configs[4]: the config-1 graph, 1% rewired, warm restart (Theorem 4)
+    spec = synth.CONFIGS[4]
+    g = synth.generate(spec)
+    delta = synth.rewire(spec, g, fraction=0.01, seed=4)
+    rp2, c2, w2, _ = graph.apply_delta(g.n, g.row_ptr, g.col, g.w, delta["add_src"], delta["add_dst"],
+                                       delta["add_w"], delta["rem_src"], delta["rem_dst"])
+    cold = di.di_solve(g.n, rp2, c2, w2, D, tol=1e-12)
+    for variant in ("auto", "tiled"):
+        G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+        G.solve(d=D, tol=1e-9, variant=variant)
+        G.update_edges(**delta)
+        H, r = G.resume(tol=1e-12, variant=variant)
+        assert r["converged"]
+        assert np.abs(H.cpu().numpy() - cold.H).sum() <= L1_BAR
+        assert_topk(H.cpu().numpy(), cold.H, 1000, 2 * (r["bound"] + cold.residual / (1 - D)))
+
+
+_CFG2 = []
+
+
+def _config2_graph():
+    if not _CFG2:
+        _CFG2.append(synth.generate(synth.CONFIGS[2]))
+    return _CFG2[0]
 
 
 def _sampled_identity(g, H, F, d, rng, k=2000):
@@ -268,11 +296,13 @@ def _sampled_identity(g, H, F, d, rng, k=2000):
     return np.abs(resid).max()
 
 
-def test_config2_full_size_sampled(eng):
+@pytest.mark.parametrize("variant", ["auto", "tiled"])
+def test_config2_full_size_sampled(eng, variant):
+    # the bench's workload and launch configuration (tiled, 3 local rounds)
     spec = synth.CONFIGS[2]
-    g = synth.generate(spec)
+    g = _config2_graph()
     G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
-    H, res = G.solve(d=D, tol=spec.tol)
+    H, res = G.solve(d=D, tol=spec.tol, variant=variant, local_rounds=3)
     assert res["converged"] and res["residual_l1"] <= spec.tol
     F, H2, d, leak = G.state()
     H2 = H2.cpu().numpy()
