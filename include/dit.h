@@ -71,7 +71,7 @@ extern "C" {
                                      memory over the tile's internal edges; the pushes along the
                                      other edges are gathered by their targets at the start of
                                      the next sweep (deterministic); every node holding fluid
-                                     diffuses (theta is not used).  Not available on shards. */
+                                     diffuses (theta is not used). */
 #define DI_TILE_NODES 512         /* node ids per tile of DI_VARIANT_TILED */
 
 typedef struct di_graph di_graph;  /* opaque: device CSR + derived arrays + DI state */
@@ -253,6 +253,16 @@ int di_shard_sweep(di_graph *g, double *ghost_out);
 int di_shard_apply(di_graph *g, const double *recv);
 /* local statistics of the current F into the stats buffer given to di_shard_begin */
 int di_shard_reduce(di_graph *g);
+/* After the sweeps (poll says done): the pushes still pending (DI_VARIANT_TILED
+ * completes a sweep's remote pushes at the start of the next one, DESIGN.md
+ * R13) exchanged like a sweep: di_shard_flush writes the ghost fluid to
+ * ghost_out (zeros for the other variants), the caller runs the all-to-all,
+ * di_shard_flush_apply adds what it received, gathers the local pending pushes
+ * into F and takes the exact local |F|_1 into stats; after the all-reduce,
+ * di_shard_control re-derives `done` from the exact residual (the sweeps
+ * continue if it is above tol). */
+int di_shard_flush(di_graph *g, double *ghost_out);
+int di_shard_flush_apply(di_graph *g, const double *recv);
 /* host-synchronous: 1 once the control block says done */
 int di_shard_poll(di_graph *g, int32_t *done);
 /* local H (owned nodes) and local counters; residual_l1 / bound are global */

@@ -29,6 +29,8 @@ DI_W_NONE, DI_W_F32, DI_W_F64 = 0, 1, 2
 DI_DANGLING_DROP, DI_DANGLING_COMPLETE = 0, 1
 DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL, DI_VARIANT_TILED = 0, 1, 2, 3
 DI_TILE_NODES = 512   # include/dit.h
+SHARD_TILED = True    # DI_VARIANT_TILED on shards (di_shard_* with di_shard_flush / _flush_apply)
+SHARD_TILED_FALLBACK = "pull"
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",
@@ -268,7 +270,7 @@ def di_plan_stats(h):
 # ------------------------------------------------------------------ shards (multi-GPU)
 EXPORTS += ["di_shard_create", "di_shard_info", "di_shard_ghost_ids", "di_shard_set_recv", "di_shard_begin",
             "di_shard_control", "di_shard_sweep", "di_shard_apply", "di_shard_reduce", "di_shard_poll",
-            "di_shard_finish"]
+            "di_shard_finish", "di_shard_flush", "di_shard_flush_apply"]
 _lib.di_shard_create.argtypes = [_I64, _I64, _I64, _I64, _P, _P, _P, _I32, _I32, _I32, _P, ctypes.POINTER(_P)]
 _lib.di_shard_info.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
 _lib.di_shard_ghost_ids.argtypes = [_P, _P, _I32]
@@ -277,6 +279,8 @@ _lib.di_shard_begin.argtypes = [_P, _D, _P, _I32, _D, ctypes.POINTER(di_solve_op
 _lib.di_shard_control.argtypes = [_P, _P]
 _lib.di_shard_sweep.argtypes = [_P, _P]
 _lib.di_shard_apply.argtypes = [_P, _P]
+_lib.di_shard_flush.argtypes = [_P, _P]
+_lib.di_shard_flush_apply.argtypes = [_P, _P]
 _lib.di_shard_reduce.argtypes = [_P]
 _lib.di_shard_poll.argtypes = [_P, ctypes.POINTER(_I32)]
 _lib.di_shard_finish.argtypes = [_P, _D, ctypes.POINTER(di_solve_opts), _P, _I32, ctypes.POINTER(di_result)]
@@ -332,6 +336,14 @@ def di_shard_sweep(h, ghost_out):
 
 def di_shard_apply(h, recv):
     _check(_lib.di_shard_apply(h, _ptr_mem(recv)[0]))
+
+
+def di_shard_flush(h, ghost_out):
+    _check(_lib.di_shard_flush(h, _ptr_mem(ghost_out)[0]))
+
+
+def di_shard_flush_apply(h, recv):
+    _check(_lib.di_shard_flush_apply(h, _ptr_mem(recv)[0]))
 
 
 def di_shard_reduce(h):

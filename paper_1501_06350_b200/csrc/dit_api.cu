@@ -388,7 +388,8 @@ int di_shard_control(di_graph *g, const double *gstats) {
         need_shard(g);
         if (!gstats) fail(DI_ERR_INVALID, "gstats is NULL");
         use_device(g);
-        shard_control(g, gstats);
+        shard_control(g, gstats, g->s.flushing ? 1 : 0);
+        g->s.flushing = false;
     });
 }
 
@@ -410,7 +411,31 @@ int di_shard_apply(di_graph *g, const double *recv) {
         for (int64_t c : g->g.recv_seg) tot += c;
         if (tot > 0 && !recv) fail(DI_ERR_INVALID, "recv is NULL");
         use_device(g);
-        shard_apply(g, recv);
+        shard_apply(g, recv, 0);
+    });
+}
+
+int di_shard_flush(di_graph *g, double *ghost_out) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        if (g->g.nt > g->g.n && !ghost_out) fail(DI_ERR_INVALID, "ghost_out is NULL");
+        use_device(g);
+        shard_flush(g, ghost_out);
+        DI_CUDA(cudaGetLastError());
+    });
+}
+
+int di_shard_flush_apply(di_graph *g, const double *recv) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        int64_t tot = 0;
+        for (int64_t c : g->g.recv_seg) tot += c;
+        if (tot > 0 && !recv) fail(DI_ERR_INVALID, "recv is NULL");
+        use_device(g);
+        shard_flush_apply(g, recv);
+        DI_CUDA(cudaGetLastError());
     });
 }
 
@@ -419,7 +444,7 @@ int di_shard_reduce(di_graph *g) {
         need_shard(g);
         if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
         use_device(g);
-        launch_sweep_reduce(g);
+        shard_reduce(g);
         DI_CUDA(cudaGetLastError());
     });
 }

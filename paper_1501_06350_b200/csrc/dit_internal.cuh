@@ -163,6 +163,7 @@ struct State {
     int64_t launched = 0;                // sweeps enqueued in the current call
     int rounds = 4;                      // TILED local rounds of the current call
     bool tiled_call = false;
+    bool flushing = false;               // shard: the next control follows a flush
     int64_t last_sweeps = 0;
     double d = 0.85;
     double *F = nullptr, *H = nullptr;   // [n]
@@ -219,6 +220,9 @@ void build_tiles(di_graph *h);
 void free_tiles(TilePlan &t);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
+void launch_tile_heavy(di_graph *h, int force);
+void launch_tile_kernel(di_graph *h, int rounds);
+void launch_take_ghost_sums(di_graph *h, double *out, int force);
 void launch_reduce_exact(di_graph *h);
 void mark_event(di_graph *h, int64_t sweep, int k);
 bool poll_done(di_graph *h);
@@ -234,8 +238,11 @@ void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t
 void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int nseg, const int64_t *seg_counts,
                     int mem);
 void shard_sweep(di_graph *h, double *ghost_out);
-void shard_apply(di_graph *h, const double *recv);
-void shard_control(di_graph *h, const double *gstats);
+void shard_apply(di_graph *h, const double *recv, int force);
+void shard_control(di_graph *h, const double *gstats, int force);
+void shard_reduce(di_graph *h);
+void shard_flush(di_graph *h, double *ghost_out);
+void shard_flush_apply(di_graph *h, const double *recv);
 void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int32_t *add_dst,
                   const void *add_w, int w_dtype, int64_t n_rem, const int32_t *rem_src,
                   const int32_t *rem_dst, int mem);

@@ -120,15 +120,28 @@ __global__ void k_take_ghosts(double *__restrict__ Fg, int64_t ng, double *__res
 
 // one source rank's segment: its ghost ids are distinct, so plain adds
 __global__ void k_apply_seg(double *__restrict__ F, const int32_t *__restrict__ idx, const double *__restrict__ v,
-                            int64_t cnt, const Ctrl *__restrict__ ctrl) {
-    if (ctrl->done) return;
+                            int64_t cnt, const Ctrl *__restrict__ ctrl, int force) {
+    if (ctrl->done && !force) return;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x)
         F[idx[q]] += v[q];
 }
 
-__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m);
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m, int force);
 
+// Tiled shards: the ghost slots are heavy targets of the tile
+// plan.  di_shard_sweep runs the heavy gather of the previous sweep's pushes
+// (ghost sums -> send buffer), the caller exchanges them, di_shard_apply adds
+// the received fluid to F, and di_shard_reduce runs the tile kernel (local
+// rounds, residual estimate of reading R13 -> stats).
 void shard_sweep(di_graph *h, double *ghost_out) {
+    if (h->s.tiled_call) {
+        const int64_t k = h->s.launched;
+        mark_event(h, k, 0);
+        launch_tile_heavy(h, 0);
+        launch_take_ghost_sums(h, ghost_out, 0);
+        mark_event(h, k, 1);
+        return;
+    }
     launch_sweep(h);
     const int64_t ng = h->g.nt - h->g.n;
     if (ng > 0) {
@@ -138,11 +151,12 @@ void shard_sweep(di_graph *h, double *ghost_out) {
     DI_CUDA(cudaGetLastError());
 }
 
-void shard_apply(di_graph *h, const double *recv) {
+void shard_apply(di_graph *h, const double *recv, int force) {
     int64_t off = 0;
     for (int64_t c : h->g.recv_seg) {   // source ranks in order: deterministic
         if (c > 0) {
-            k_apply_seg<<<grid_for(h, c), 256, 0, h->stream>>>(h->s.F, h->g.recv_idx + off, recv + off, c, h->s.ctrl);
+            k_apply_seg<<<grid_for(h, c), 256, 0, h->stream>>>(h->s.F, h->g.recv_idx + off, recv + off, c, h->s.ctrl,
+                                                               force);
             count_launch();
         }
         off += c;
@@ -150,8 +164,38 @@ void shard_apply(di_graph *h, const double *recv) {
     DI_CUDA(cudaGetLastError());
 }
 
-void shard_control(di_graph *h, const double *gstats) {
-    k_control<<<1, 32, 0, h->stream>>>(h->s.ctrl, gstats, h->g.m);
+void shard_reduce(di_graph *h) {
+    if (h->s.tiled_call) {
+        const int64_t k = h->s.launched;
+        mark_event(h, k, 2);
+        launch_tile_kernel(h, h->s.rounds);
+        mark_event(h, k, 3);
+        mark_event(h, k, 4);
+        h->s.launched += 1;
+        return;
+    }
+    launch_sweep_reduce(h);
+}
+
+// after the last sweep: the pending pushes of the tiled schedule, exchanged like a sweep
+void shard_flush(di_graph *h, double *ghost_out) {
+    if (h->s.tiled_call) {
+        launch_tile_heavy(h, 1);
+        launch_take_ghost_sums(h, ghost_out, 1);
+    } else if (h->g.nt > h->g.n) {
+        DI_CUDA(cudaMemsetAsync(ghost_out, 0, (h->g.nt - h->g.n) * sizeof(double), h->stream));
+    }
+}
+
+void shard_flush_apply(di_graph *h, const double *recv) {
+    shard_apply(h, recv, 1);
+    if (h->s.tiled_call) launch_tile_flush(h);
+    launch_reduce_exact(h);           // exact local |F|_1 -> stats; k_control re-derives `done`
+    h->s.flushing = true;
+}
+
+void shard_control(di_graph *h, const double *gstats, int force) {
+    k_control<<<1, 32, 0, h->stream>>>(h->s.ctrl, gstats, h->g.m, force);
     count_launch();
     DI_CUDA(cudaGetLastError());
 }

@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
 }
 
 // shard mode: control from the all-reduced {sum r, max fm} (gstats[0], gstats[1])
-__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m) {
-    if (threadIdx.x != 0 || ctrl->done) return;
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m, int force) {
+    if (threadIdx.x != 0 || (ctrl->done && !force)) return;
     finalize_control(ctrl, gstats[0], gstats[1], ctrl->stats_is_init, m);
 }
 

@@ -111,13 +111,14 @@ __device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes)
 
 // ---------------------------------------------------------------- build
 // per target: local / remote in-edge counts from the transpose
+// (shard: targets t >= n are ghost slots, every in-edge of a ghost is remote)
 __global__ void k_count_local(const int64_t *__restrict__ tptr, const int32_t *__restrict__ tsrc, int64_t n,
-                              int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
+                              int64_t nt, int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = warp; t < n; t += nw) {
+    for (int64_t t = warp; t < nt; t += nw) {
         const int64_t b = tptr[t], e = tptr[t + 1];
-        const int64_t tile = t / kNodeTile;
+        const int64_t tile = t < n ? t / kNodeTile : -1;
         int64_t c = 0;
         for (int64_t k = b + lane_id(); k < e; k += 32) c += (tsrc[k] / kNodeTile == tile);
         c = warp_sum(c);
@@ -143,6 +144,16 @@ __global__ void k_classify(const int64_t *__restrict__ rc, int64_t n, int64_t nt
             hc[j] = heavy ? rc[j] : 0;
             hflag[j] = heavy ? 1 : 0;
         }
+    }
+}
+
+// shard ghost slots: heavy targets whose sums leave through the all-to-all
+__global__ void k_classify_ghosts(const int64_t *__restrict__ rc, int64_t n, int64_t nt, int64_t *__restrict__ lrc,
+                                  int64_t *__restrict__ hc, int64_t *__restrict__ hflag) {
+    for (int64_t t = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+        lrc[t] = 0;
+        hc[t] = rc[t];
+        hflag[t] = rc[t] > 0;
     }
 }
 
@@ -210,17 +221,16 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__r
 // light offsets relative to the tile, tile bases, heavy index, out-degree
 __global__ void k_tile_rel(const int64_t *__restrict__ rptr, const int64_t *__restrict__ hpos,
                            const int64_t *__restrict__ hflag, const int64_t *__restrict__ row_ptr, int64_t n,
-                           int64_t ntile, uint32_t *__restrict__ rrel, int32_t *__restrict__ hidx,
+                           int64_t nt, int64_t ntile, uint32_t *__restrict__ rrel, int32_t *__restrict__ hidx,
                            int32_t *__restrict__ deg, int64_t *__restrict__ rtile) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= nt; j += (int64_t)gridDim.x * blockDim.x) {
+        if (j < nt) hidx[j] = hflag[j] ? (int32_t)hpos[j] : -1;
         if (j < n) {
             const int64_t b = (j / kNodeTile) * kNodeTile;
             rrel[j] = (uint32_t)(rptr[j] - rptr[b]);
-            const int32_t h = hflag[j] ? (int32_t)hpos[j] : -1;
-            hidx[j] = h;
             deg[j] = (int32_t)(row_ptr[j + 1] - row_ptr[j]);
         }
-        if (j % kNodeTile == 0 || j == n) {
+        if (j <= n && (j % kNodeTile == 0 || j == n)) {
             const int64_t t = (j + kNodeTile - 1) / kNodeTile;   // j == n: the end of the last tile
             if (t <= ntile) rtile[t] = rptr[j];
         }
@@ -244,7 +254,8 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
                               const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
                               const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
                               const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
-                              const int32_t *__restrict__ hidx, int64_t stripe_nodes, uint16_t *__restrict__ lsrc,
+                              const int32_t *__restrict__ hidx, int64_t stripe_nodes, int64_t nt,
+                              uint16_t *__restrict__ lsrc,
                               StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
                               uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval, uint32_t *__restrict__ hof) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -252,13 +263,14 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
     const unsigned lane = lane_id();
     const unsigned lt = (1u << lane) - 1u;
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    for (int64_t t = warp; t < n; t += nw) {
+    for (int64_t t = warp; t < nt; t += nw) {
         const int64_t b = tptr[t], e = tptr[t + 1];
-        const int64_t tile = t / kNodeTile;
+        const bool owned = t < n;
+        const int64_t tile = owned ? t / kNodeTile : -1;
         const int32_t hx = hidx[t];
         // balanced sliced-ELL: local in-edge s of t is slot s % cap of its piece s / cap
-        const int64_t cap = vcap[tile];
-        const int pf = vfirst[tile * kVfStride + (t - tile * kNodeTile)];
+        const int64_t cap = owned ? vcap[tile] : 1;
+        const int pf = owned ? vfirst[tile * kVfStride + (t - tile * kNodeTile)] : 0;
         int64_t lo = 0;
         int64_t ro = hx >= 0 ? hptr[t] : rptr[t];
         for (int64_t k0 = b; k0 < e; k0 += 32) {
@@ -365,7 +377,7 @@ __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_
         const int64_t tile = i / kNodeTile;
         double s = 0.0;
         for (int64_t e = row_ptr[i] + lane_id(); e < row_ptr[i + 1]; e += 32)
-            if (col[e] / kNodeTile != tile) s += kW ? (double)w[e] : 1.0;
+            if (col[e] >= n || col[e] / kNodeTile != tile) s += kW ? (double)w[e] : 1.0;   // ghosts leave too
         s = warp_sum(s);
         if (lane_id() == 0) wr[i] = (float)(s * inv[i]);
     }
@@ -419,22 +431,27 @@ static void build_tiles_t(di_graph *h) {
     using SW = StoreW<W>;
     constexpr bool kW = !std::is_same<W, NoW>::value;
     const size_t rs = sizeof(RemRec<W>);
+    const int64_t nt = g.nt;                         // owned nodes + shard ghost slots
     tp.ntile = (n + kNodeTile - 1) / kNodeTile;
     tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
     const int64_t S = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
     // ---- classes of the in-edges
     int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
     for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
-        DI_CUDA(cudaMallocAsync(p, (n + 1) * sizeof(int64_t), st));
-    k_count_local<<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, n, lc, rc);
+        DI_CUDA(cudaMallocAsync(p, (nt + 1) * sizeof(int64_t), st));
+    k_count_local<<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, n, nt, lc, rc);
     k_classify<<<grid_for(h, tp.ntile), 256, 0, st>>>(rc, n, tp.ntile, lrc, hc, hflag);
     count_launch(2);
-    exclusive_scan_i64(lrc, rptr, n, st);
-    exclusive_scan_i64(hc, hptr, n, st);
-    exclusive_scan_i64(hflag, hpos, n, st);
-    tp.mlight = read_i64(rptr + n, st);
-    tp.mh = read_i64(hptr + n, st);
-    tp.nh = read_i64(hpos + n, st);
+    if (nt > n) {
+        k_classify_ghosts<<<grid_for(h, nt - n), 256, 0, st>>>(rc, n, nt, lrc, hc, hflag);
+        count_launch();
+    }
+    exclusive_scan_i64(lrc, rptr, nt, st);
+    exclusive_scan_i64(hc, hptr, nt, st);
+    exclusive_scan_i64(hflag, hpos, nt, st);
+    tp.mlight = read_i64(rptr + nt, st);
+    tp.mh = read_i64(hptr + nt, st);
+    tp.nh = read_i64(hpos + nt, st);
     if (tp.mh >= (int64_t)0xffffffffLL) {
         set_error("tiled plan: too many heavy remote edges for one graph handle");
         throw Fail{DI_ERR_INVALID};
@@ -463,12 +480,12 @@ static void build_tiles_t(di_graph *h) {
     }
     // ---- per-node arrays, tile bases
     DI_CUDA(cudaMalloc(&tp.rrel, n * sizeof(uint32_t) + 16));
-    DI_CUDA(cudaMalloc(&tp.hidx, n * sizeof(int32_t) + 16));
+    DI_CUDA(cudaMalloc(&tp.hidx, nt * sizeof(int32_t) + 16));
     DI_CUDA(cudaMalloc(&tp.wr, n * sizeof(float) + 16));
     DI_CUDA(cudaMalloc(&tp.deg, n * sizeof(int32_t) + 16));
     DI_CUDA(cudaMalloc(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t)));
-    k_tile_rel<<<grid_for(h, n + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, tp.ntile, tp.rrel, tp.hidx, tp.deg,
-                                                   tp.rtile);
+    k_tile_rel<<<grid_for(h, nt + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, nt, tp.ntile, tp.rrel, tp.hidx,
+                                                    tp.deg, tp.rtile);
     k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.wr);
     count_launch(2);
     // ---- edges to their classes
@@ -481,7 +498,7 @@ static void build_tiles_t(di_graph *h) {
     for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
     k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, tp.ltile, tp.vofs, tp.vfirst,
                                            tp.plist, vcap, rptr,
-                                           hptr, tp.hidx, tp.stripe_nodes, tp.lsrc, (SW *)tp.lw,
+                                           hptr, tp.hidx, tp.stripe_nodes, nt, tp.lsrc, (SW *)tp.lw,
                                            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
     count_launch();
     // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
@@ -577,10 +594,6 @@ static void build_tiles_t(di_graph *h) {
 void build_tiles(di_graph *h) {
     DevGraph &g = h->g;
     if (g.tl.built || g.n == 0) return;
-    if (g.shard) {
-        set_error("the tiled variant is not available on shards");
-        throw Fail{DI_ERR_INVALID};
-    }
     build_transpose(h);
     switch (g.w_kind) {
     case DI_W_F32: build_tiles_t<float>(h); break;
@@ -1014,6 +1027,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     ctrl->n_entries = 0;
     ctrl->sel_edges = 0;
     ctrl->red_blocks = 0;
+    if (ctrl->stats_out) {                           // shard: the global values come back through k_control
+        ctrl->stats_out[0] = r;
+        ctrl->stats_out[1] = 0.0;
+        ctrl->stats_out[2] = ctrl->leak;
+        ctrl->stats_out[3] = (double)ctrl->last_sel_edges;
+        ctrl->stats_is_init = 0;
+        return;
+    }
     finalize_control(ctrl, r, 0.0, 0, a.m);
 }
 
@@ -1104,14 +1125,10 @@ static void launch_heavy_t(di_graph *h, int force) {
 }
 
 template <typename W>
-static void launch_tile_t(di_graph *h, int rounds) {
+static void launch_tile_kernel_t(di_graph *h, int rounds) {
     DevGraph &g = h->g;
     State &s = h->s;
     TilePlan &tp = g.tl;
-    const int64_t k = s.launched;
-    launch_heavy_t<W>(h, 0);
-    mark_event(h, k, 1);
-    mark_event(h, k, 2);
     if (!tp.tile_smem) {
         // two CTAs per SM, each with the shared head (gq, psum) and two bundle
         // buffers; computed (and the attribute set) once per plan, off the sweep path
@@ -1140,6 +1157,15 @@ static void launch_tile_t(di_graph *h, int rounds) {
     k_tile<W><<<grid, kTileThreads, smem, h->stream>>>(a, s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());
+}
+
+template <typename W>
+static void launch_tile_t(di_graph *h, int rounds) {
+    const int64_t k = h->s.launched;
+    launch_heavy_t<W>(h, 0);
+    mark_event(h, k, 1);
+    mark_event(h, k, 2);
+    launch_tile_kernel_t<W>(h, rounds);
     mark_event(h, k, 3);
 }
 
@@ -1150,6 +1176,43 @@ void launch_tile_sweep(di_graph *h, int rounds) {
     case DI_W_F64: launch_tile_t<double>(h, rounds); break;
     default: launch_tile_t<NoW>(h, rounds);
     }
+}
+
+// shard sweeps run the two halves separately, the ghost exchange in between
+void launch_tile_heavy(di_graph *h, int force) {
+    if (h->g.tl.ntile == 0) return;
+    switch (h->g.w_kind) {
+    case DI_W_F32: launch_heavy_t<float>(h, force); break;
+    case DI_W_F64: launch_heavy_t<double>(h, force); break;
+    default: launch_heavy_t<NoW>(h, force);
+    }
+}
+
+void launch_tile_kernel(di_graph *h, int rounds) {
+    if (h->g.tl.ntile == 0) return;
+    switch (h->g.w_kind) {
+    case DI_W_F32: launch_tile_kernel_t<float>(h, rounds); break;
+    case DI_W_F64: launch_tile_kernel_t<double>(h, rounds); break;
+    default: launch_tile_kernel_t<NoW>(h, rounds);
+    }
+}
+
+// ghost slots' inflow (heavy sums of the last sweep's pushes) -> the send buffer
+__global__ void k_take_ghost_sums(const int32_t *__restrict__ hidx, const double *__restrict__ hsum, int64_t n,
+                                  int64_t ng, double *__restrict__ out, const Ctrl *__restrict__ ctrl, int force) {
+    if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
+    const bool g = ctrl->gather != 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < ng; q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = g ? hsum[hidx[n + q]] : 0.0;
+}
+
+void launch_take_ghost_sums(di_graph *h, double *out, int force) {
+    const int64_t ng = h->g.nt - h->g.n;
+    if (ng <= 0) return;
+    k_take_ghost_sums<<<grid_for(h, ng), 256, 0, h->stream>>>(h->g.tl.hidx, h->g.tl.hsum, h->g.n, ng, out, h->s.ctrl,
+                                                            force);
+    count_launch();
+    DI_CUDA(cudaGetLastError());
 }
 
 template <typename W>

@@ -65,6 +65,12 @@ class CudaShard:
     def reduce(self):
         _lib.di_shard_reduce(self.h)
 
+    def flush(self):
+        _lib.di_shard_flush(self.h, self.send)
+
+    def flush_apply(self):
+        _lib.di_shard_flush_apply(self.h, self.recv)
+
     def poll(self):
         return _lib.di_shard_poll(self.h)
 
@@ -135,7 +141,11 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
     """Cold sharded solve; returns (list of local H tensors, list of local result dicts).
 
     Per sweep: sweep -> all-to-all(ghost fluid) -> apply -> reduce -> all-reduce
-    (sum |F|_1, max |F|) -> control.  The host polls `done` once per chunk."""
+    (sum |F|_1, max |F|) -> control.  The host polls `done` once per chunk.
+    The tiled schedule (variant 3) leaves the last sweep's remote pushes
+    pending (R13): once done, they are exchanged and applied like a
+    sweep (flush -> all-to-all -> flush_apply -> all-reduce -> control), and
+    the sweeps go on if the exact residual is still above tol."""
     for s in shards:
         s.begin(d, tol, **opts)
     coll.allreduce_stats(shards)
@@ -154,6 +164,16 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
             for s in shards:
                 s.control()
         done = [s.poll() for s in shards]
+        if all(done) and opts.get("variant") == _lib.DI_VARIANT_TILED:
+            for s in shards:
+                s.flush()
+            coll.alltoall(shards)
+            for s in shards:
+                s.flush_apply()
+            coll.allreduce_stats(shards)
+            for s in shards:
+                s.control()
+            done = [s.poll() for s in shards]
         if all(done):
             break
         if any(done):
@@ -190,7 +210,13 @@ def bench_sharded(args, metric):
     sh = CudaShard(spec.n, lo, hi, g.row_ptr, g.col, g.w, device=local, stream=stream)
     coll = TorchCollectives()
     coll.plan([sh], bounds)
-    kw = dict(theta=args.theta, variant={"auto": 0, "push": 1, "pull": 2}[args.variant])
+    variant = args.variant
+    theta = args.theta
+    if variant == "tiled":
+        variant = _lib.SHARD_TILED_FALLBACK if not getattr(_lib, "SHARD_TILED", False) else "tiled"
+        if variant == "pull":
+            theta = 0.0
+    kw = dict(theta=theta, variant={"auto": 0, "push": 1, "pull": 2, "tiled": 3}[variant], local_rounds=args.rounds)
     for _ in range(args.warmup):
         solve([sh], coll, d=spec.d, tol=tol, **kw)
     torch.cuda.synchronize()
@@ -216,7 +242,7 @@ def bench_sharded(args, metric):
                 "time_to_tol_s": ms_max / args.steps / 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{spec.name} sharded, {per} nodes per GPU (weak scaling)", "n": spec.n,
-                           "m": int(cross[1]), "tol": tol, "theta": args.theta, "variant": args.variant,
+                           "m": int(cross[1]), "tol": tol, "theta": theta, "variant": variant,
                            "ghost_slots_total": int(cross[0]), "sweeps_per_solve": res[-1]["sweeps"],
                            "parallelism": f"node-range partition x{world}, NCCL all-to-all + all-reduce"},
                 "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),

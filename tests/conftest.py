@@ -8,7 +8,18 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _build_engine():
+    """Build libdit.so (and nothing else) before any test imports the package:
+    build.py is loaded by path because importing the package needs the library."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_dit_build", os.path.join(ROOT, "paper_1501_06350_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+
+
 def pytest_configure(config):
+    _build_engine()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 

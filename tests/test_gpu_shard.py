@@ -72,7 +72,7 @@ def gpu():
     return True
 
 
-@pytest.mark.parametrize("world,variant", [(2, 0), (4, 1), (3, 2)])
+@pytest.mark.parametrize("world,variant", [(2, 0), (4, 1), (3, 2), (2, 3), (3, 3)])
 def test_lockstep_shards_match_oracle(gpu, world, variant):
     from paper_1501_06350_b200 import dist
     spec = synth.CONFIGS[1].scaled(200_000, seed=8, weighted=True)
@@ -105,6 +105,30 @@ def test_lockstep_theta0_sweeps_elementwise(gpu):
     assert np.allclose(torch.cat(Hs).cpu().numpy(), r.H, rtol=1e-13, atol=1e-18)
 
 
+@pytest.mark.parametrize("weighted", [False, True])
+def test_lockstep_tiled_sweeps_elementwise(gpu, weighted):
+    # shard bounds on tile boundaries: the sharded tiled schedule is exactly the
+    # oracle's tiled sweep (cross-shard pushes are remote pushes, R12/R13)
+    from paper_1501_06350_b200 import _lib, dist
+    T = _lib.DI_TILE_NODES
+    spec = synth.CONFIGS[1].scaled(2 * 7 * T, seed=12, weighted=weighted)
+    shards, bounds = _shards(spec, 2)
+    assert bounds[1] % T == 0
+    coll = LockstepCollectives()
+    coll.plan(shards, bounds)
+    g = synth.generate(spec)
+    cp, ri, pv = graph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    st = di.di_init(g.n, D)
+    for k in (1, 3):
+        Hs, res = dist.solve(shards, coll, d=D, tol=0.0, variant=3, local_rounds=3, max_sweeps=k)
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=3, tol=0, max_sweeps=k)
+        assert all(x["sweeps"] == k for x in res)
+        assert np.allclose(torch.cat(Hs).cpu().numpy(), r.H, rtol=1e-12, atol=1e-20)
+        assert sum(x["diffused_edges"] for x in res) == r.edges
+    for s in shards:
+        s.close()
+
+
 def test_nccl_world1(gpu):
     import torch.distributed as tdist
 
@@ -120,10 +144,11 @@ def test_nccl_world1(gpu):
         shards, bounds = _shards(spec, 1)
         coll = dist.TorchCollectives()
         coll.plan(shards, bounds)
-        Hs, res = dist.solve(shards, coll, d=D, tol=1e-12)
         g = synth.generate(spec)
         ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12)
-        assert np.abs(Hs[0].cpu().numpy() - ref.H).sum() <= 1e-9
+        for variant in (0, 3):
+            Hs, res = dist.solve(shards, coll, d=D, tol=1e-12, variant=variant)
+            assert np.abs(Hs[0].cpu().numpy() - ref.H).sum() <= 1e-9
         shards[0].close()
     finally:
         tdist.destroy_process_group()
