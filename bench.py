@@ -195,6 +195,29 @@ def load_traffic(workload, kernel):
         return None
 
 
+KERNEL_NAMES = {"tiled": {"pull": "k_heavy_s", "tile": "k_tile"}}
+
+
+def roofline_from(prof_tot, workload, variant):
+    """Roofline of the dominant kernel class (largest summed CUDA-event time):
+    algorithmic bytes / event time, against the measured peak."""
+    peak, peak_kind = load_peaks()
+    kinds = ["select", "push", "pull", "reduce", "tile"]
+    dom = max(kinds, key=lambda k: prof_tot.get(f"{k}_ms", 0.0))
+    dom_ms = prof_tot[f"{dom}_ms"]
+    dom_launch = max(1, prof_tot[f"{dom}_launches"])
+    achieved = prof_tot[f"{dom}_bytes"] / (dom_ms / 1e3) / 1e9
+    tot_ms = max(1e-9, sum(prof_tot.get(f"{q}_ms", 0.0) for q in kinds))
+    names = KERNEL_NAMES.get(variant, {})
+    share = {names.get(k, f"k_{k}"): prof_tot.get(f"{k}_ms", 0.0) / tot_ms for k in kinds}
+    name = names.get(dom, f"k_{dom}")
+    return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_kind,
+            "traffic": load_traffic(workload, name), "algorithmic_bytes_per_launch": prof_tot[f"{dom}_bytes"] / dom_launch,
+            "avg_launch_ms": dom_ms / dom_launch, "share_of_step": share,
+            "sweep_bytes_per_s_all_kernels": sum(prof_tot.get(f"{k}_bytes", 0) for k in kinds) / (tot_ms / 1e3) / 1e9}
+
+
 def run_ours(args):
     import torch
     import paper_1501_06350_b200 as eng
@@ -204,7 +227,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     if world > 1 or args.gpus > 1:
         from paper_1501_06350_b200 import dist
-        return dist.bench_sharded(args, METRIC)
+        return dist.bench_sharded(args, METRIC, {"clock": ClockSampler, "roofline": roofline_from,
+                                                 "pinned": pinned_alloc})
     torch.cuda.set_device(0)
     spec = spec_for(args)
     tol = args.tol if args.tol is not None else spec.tol
@@ -247,22 +271,7 @@ def run_ours(args):
     value = edges_tot / (total_ms / 1e3)
     res = results[-1]
     assert res["converged"], res
-    # roofline of the dominant kernel (largest summed device time)
-    peak, peak_kind = load_peaks()
-    kinds = ["select", "push", "pull", "reduce", "tile"]
-    dom = max(kinds, key=lambda k: prof_tot.get(f"{k}_ms", 0.0))
-    dom_ms = prof_tot[f"{dom}_ms"]
-    dom_launch = max(1, prof_tot[f"{dom}_launches"])
-    achieved = prof_tot[f"{dom}_bytes"] / (dom_ms / 1e3) / 1e9
-    share = {k: prof_tot.get(f"{k}_ms", 0.0) / max(1e-9, sum(prof_tot.get(f"{q}_ms", 0.0) for q in kinds))
-             for k in kinds}
-    traffic = load_traffic(spec.name, dom)
-    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": peak_kind,
-                "traffic": traffic, "algorithmic_bytes_per_launch": prof_tot[f"{dom}_bytes"] / dom_launch,
-                "avg_launch_ms": dom_ms / dom_launch, "share_of_step": share,
-                "sweep_bytes_per_s_all_kernels": sum(prof_tot.get(f"{k}_bytes", 0) for k in kinds) /
-                (sum(prof_tot.get(f"{k}_ms", 0.0) for k in kinds) / 1e3) / 1e9}
+    roofline = roofline_from(prof_tot, spec.name, args.variant)
     # e2e through the C ABI with host buffers
     e2e = None
     if args.e2e_steps > 0:

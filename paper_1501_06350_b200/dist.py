@@ -184,9 +184,11 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
 
 
 # ------------------------------------------------------------------ bench (torchrun)
-def bench_sharded(args, metric):
+def bench_sharded(args, metric, tools):
     """bench.py --gpus N under torchrun: weak scaling, each rank owns the rows of
-    a configs[2]-shaped slice (50M nodes, ~1B edges per GPU)."""
+    a configs[2]-shaped slice (50M nodes, ~1B edges per GPU).  `tools` carries
+    bench.py's clock sampler, roofline arithmetic and pinned allocator
+    (measurement plumbing only)."""
     import json
     import os
     import time
@@ -221,21 +223,60 @@ def bench_sharded(args, metric):
         solve([sh], coll, d=spec.d, tol=tol, **kw)
     torch.cuda.synchronize()
     dist.barrier()
+    _lib.di_profile_enable(sh.h, True)
+    prof_tot = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.di_kernel_launches()
-    e0.record(stream)
-    res = []
-    for _ in range(args.steps):
-        _, r = solve([sh], coll, d=spec.d, tol=tol, **kw)
-        res.append(r[0])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
+    with tools["clock"](local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        res = []
+        for _ in range(args.steps):
+            _, r = solve([sh], coll, d=spec.d, tol=tol, **kw)
+            res.append(r[0])
+            for k, v in _lib.di_profile_get(sh.h).items():
+                prof_tot[k] = prof_tot.get(k, 0) + v
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    _lib.di_profile_enable(sh.h, False)
     ms = e0.elapsed_time(e1)
     launches = _lib.di_kernel_launches() - l0
     ms_max = coll.allreduce_max([ms], stream.device)[0]
     edges = coll.allreduce_sum([float(sum(r["diffused_edges"] for r in res))], stream.device)[0]
     cross = coll.allreduce_sum([float(sh.n_ghost), float(g.m)], stream.device)
+    # e2e: every rank builds its shard from pinned host buffers, solves and reads H back
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = tools["pinned"]
+        rp = pin((len(g.row_ptr),), np.int64)
+        rp[:] = g.row_ptr
+        cl = pin((len(g.col),), np.int32)
+        cl[:] = g.col
+        wv = None
+        if g.w is not None:
+            wv = pin((len(g.w),), np.float32)
+            wv[:] = g.w
+        Hh = pin((hi - lo,), np.float64)
+        e_ms, e_edges = 0.0, 0.0
+        for _ in range(args.e2e_steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a.record(stream)
+            s2 = CudaShard(spec.n, lo, hi, rp, cl, wv, device=local, stream=stream)
+            coll.plan([s2], bounds)
+            Hd, r2 = solve([s2], coll, d=spec.d, tol=tol, **kw)
+            Hh[:] = Hd[0].cpu().numpy()
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms += coll.allreduce_max([a.elapsed_time(b)], stream.device)[0]
+            e_edges += coll.allreduce_sum([float(r2[0]["diffused_edges"])], stream.device)[0]
+            s2.close()
+        h2d = coll.allreduce_sum([float(rp.nbytes + cl.nbytes + (wv.nbytes if wv is not None else 0))],
+                                 stream.device)[0]
+        e2e = {"value": e_edges / (e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(spec.n * 8), "ms_per_step": e_ms / args.e2e_steps}
     if rank == 0:
         line = {"metric": metric, "value": edges / (ms_max / 1e3), "unit": "edges/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -243,10 +284,12 @@ def bench_sharded(args, metric):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{spec.name} sharded, {per} nodes per GPU (weak scaling)", "n": spec.n,
                            "m": int(cross[1]), "tol": tol, "theta": theta, "variant": variant,
-                           "ghost_slots_total": int(cross[0]), "sweeps_per_solve": res[-1]["sweeps"],
+                           "local_rounds": args.rounds, "ghost_slots_total": int(cross[0]),
+                           "sweeps_per_solve": res[-1]["sweeps"],
+                           "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",
                            "parallelism": f"node-range partition x{world}, NCCL all-to-all + all-reduce"},
-                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
-                "clocks": None}
+                "roofline": tools["roofline"](prof_tot, spec.name, variant), "cpu_baseline": None, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     sh.close()
     dist.destroy_process_group()
