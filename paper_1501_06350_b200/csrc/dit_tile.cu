@@ -702,6 +702,9 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
 }
 
 // ---------------------------------------------------------------- tile kernel
+// DIT_TILE_TIMING (debug): per-CTA phase cycle counters of k_tile
+static unsigned long long *g_tile_dbg = nullptr;
+
 template <typename W>
 struct TileArgs {
     const uint32_t *vofs;
@@ -717,6 +720,7 @@ struct TileArgs {
     const double *hsum;
     double *F, *H, *A0, *A1;
     double *part;            // per-CTA partials: resid [grid], leak [grid]
+    unsigned long long *dbg; // optional per-CTA phase cycle counters [grid][5] (DIT_TILE_TIMING)
     int64_t n, ntile, m;
     int rounds;
     int64_t edge_cap;        // bytes of shared memory for the staged local edges
@@ -902,7 +906,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
         const uint16_t *pl_s = vf_s + kVfStride;
         unsigned char *rbuf = buf + kNodeBytes + kMetaBytes;
         unsigned char *ebuf = buf + tile_buf_fixed<W>();
+        long long c0 = a.dbg ? clock64() : 0;
         mbar_wait(smem_u32(&bars[b]), (uint32_t)((k >> 1) & 1));
+        long long c1 = a.dbg ? clock64() : 0;
         const bool valid = i < nn;
         const int64_t j = a0 + i;
         // 1. remote pushes of the previous sweep: heavy sums, light records -> products in place
@@ -931,6 +937,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
             }
             f = Fs[i] + s + hs;
         }
+        long long c2 = a.dbg ? clock64() : 0;
         // 2. local diffusion rounds in shared memory
         const uint16_t *es;
         const StoreW<W> *ew = nullptr;
@@ -968,6 +975,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
                 f = acc;
             }
         }
+        long long c3 = a.dbg ? clock64() : 0;
         // 3. state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
         if (valid) {
             const double An = d * D * ivi;
@@ -980,6 +988,15 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
         cur = nxt;
         nxt = after;
         __syncthreads();                             // buffer b free for the bundle after next
+        if (a.dbg && i == 0) {
+            const long long c4 = clock64();
+            unsigned long long *qd = a.dbg + blockIdx.x * 5;
+            qd[0] += c1 - c0;                        // waiting for the bundle
+            qd[1] += c2 - c1;                        // remote inflow (gathers)
+            qd[2] += c3 - c2;                        // local rounds
+            qd[3] += c4 - c3;                        // state out
+            qd[4] += 1;
+        }
     }
     // CTA partials (fixed order) and the last-block end of the sweep
     resid = warp_sum(resid);
@@ -1090,6 +1107,7 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     a.m = g.m;
     a.rounds = rounds;
     a.edge_cap = 0;
+    a.dbg = nullptr;
     return a;
 }
 
@@ -1153,6 +1171,13 @@ static void launch_tile_kernel_t(di_graph *h, int rounds) {
     const size_t smem = tp.tile_smem;
     TileArgs<W> a = tile_args<W>(h, rounds);
     a.edge_cap = cap;
+    if (getenv("DIT_TILE_TIMING")) {
+        if (!g_tile_dbg) {
+            DI_CUDA(cudaMalloc(&g_tile_dbg, 4096 * 5 * sizeof(unsigned long long)));
+            DI_CUDA(cudaMemset(g_tile_dbg, 0, 4096 * 5 * sizeof(unsigned long long)));
+        }
+        a.dbg = g_tile_dbg;
+    }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 2));
     k_tile<W><<<grid, kTileThreads, smem, h->stream>>>(a, s.ctrl);
     count_launch();
@@ -1233,3 +1258,16 @@ void launch_tile_flush(di_graph *h) {
 }
 
 }  // namespace dit
+
+// Debug (not part of include/dit.h): k_tile phase cycles {wait, inflow, rounds,
+// state out} summed over CTAs, and the number of (CTA, tile) iterations.
+extern "C" int di_debug_tile_timing(double *out5) {
+    if (!dit::g_tile_dbg || !out5) return 1;
+    std::vector<unsigned long long> v(4096 * 5);
+    if (cudaMemcpy(v.data(), dit::g_tile_dbg, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost))
+        return 2;
+    for (int q = 0; q < 5; ++q) out5[q] = 0;
+    for (int bb = 0; bb < 4096; ++bb)
+        for (int q = 0; q < 5; ++q) out5[q] += (double)v[bb * 5 + q];
+    return 0;
+}
