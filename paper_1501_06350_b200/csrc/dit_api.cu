@@ -45,6 +45,16 @@ static void fail(int code, const char *msg) {
 
 static void use_device(const di_graph *g) { DI_CUDA(cudaSetDevice(g->device)); }
 
+// The builders' temporaries come from the device's default stream-ordered pool;
+// keep freed blocks cached there (release threshold = max) so that a second
+// build on the device does not remap gigabytes of memory.
+static void keep_pool_memory(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
 static di_solve_opts resolve(const di_solve_opts *o) {
     di_solve_opts r;
     di_solve_opts_default(&r);
@@ -97,6 +107,7 @@ int di_graph_create(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t 
         if (mem == DI_MEM_HOST && row_ptr[n] != m) fail(DI_ERR_INVALID, "row_ptr[n] != m");
         if (m >= (1LL << 40)) fail(DI_ERR_INVALID, "m must be < 2^40");
         DI_CUDA(cudaSetDevice(device));
+        keep_pool_memory(device);
         di_graph *g = new di_graph();
         g->device = device;
         try {
@@ -292,6 +303,8 @@ int di_shard_create(int64_t n_global, int64_t lo, int64_t hi, int64_t m, const i
         if (mem == DI_MEM_HOST && row_ptr[hi - lo] != m) fail(DI_ERR_INVALID, "row_ptr[hi-lo] != m");
         if (m >= (1LL << 40)) fail(DI_ERR_INVALID, "m must be < 2^40");
         DI_CUDA(cudaSetDevice(device));
+        keep_pool_memory(device);
+        keep_pool_memory(device);
         di_graph *g = new di_graph();
         g->device = device;
         try {

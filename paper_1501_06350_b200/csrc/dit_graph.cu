@@ -82,7 +82,7 @@ static void launch_scales(di_graph *h, const unsigned char *only) {
 
 void build_scales(di_graph *h) {
     DevGraph &g = h->g;
-    if (!g.inv) DI_CUDA(cudaMalloc(&g.inv, (g.n > 0 ? g.n : 1) * sizeof(double) + 16));   // +16: TMA tile rows
+    if (!g.inv) DI_CUDA(cudaMallocAsync(&g.inv, (g.n > 0 ? g.n : 1) * sizeof(double) + 16, h->stream));   // +16: TMA tile rows
     launch_scales(h, nullptr);
 }
 
@@ -103,23 +103,25 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     DevGraph &g = h->g;
     cudaStream_t st = h->stream;
     g.n = n;
+    phase_mark(st, "create: start");
     g.m = m;
     g.nt = n;
     g.n_global = n;
     const cudaMemcpyKind kind = mem == DI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    DI_CUDA(cudaMalloc(&g.row_ptr, (n + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMalloc(&g.col, (m > 0 ? m : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMallocAsync(&g.row_ptr, (n + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&g.col, (m > 0 ? m : 1) * sizeof(int32_t), st));
     DI_CUDA(cudaMemcpyAsync(g.row_ptr, row_ptr, (n + 1) * sizeof(int64_t), kind, st));
     if (m > 0) DI_CUDA(cudaMemcpyAsync(g.col, col, m * sizeof(int32_t), kind, st));
     void *wtmp = nullptr;
     if (w_dtype != DI_W_NONE && m > 0) {
         const size_t es = w_dtype == DI_W_F32 ? 4 : 8;
-        DI_CUDA(cudaMalloc(&wtmp, m * es));
+        DI_CUDA(cudaMallocAsync(&wtmp, m * es, st));
         DI_CUDA(cudaMemcpyAsync(wtmp, weights, m * es, kind, st));
     }
     int *flags = nullptr;
     DI_CUDA(cudaMallocAsync(&flags, 2 * sizeof(int), st));
     DI_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+    phase_mark(st, "create: upload");
     k_check_rows<<<grid_for(h, n + 1), 256, 0, st>>>(g.row_ptr, n, m, flags);
     count_launch();
     if (m > 0) {
@@ -150,7 +152,7 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
             g.w = wtmp;
             g.w_kind = DI_W_F64;
         } else {   // every weight is exactly a float: store 4 bytes per edge
-            DI_CUDA(cudaMalloc(&g.w, m * sizeof(float)));
+            DI_CUDA(cudaMallocAsync(&g.w, m * sizeof(float), st));
             k_f64_to_f32<<<grid_for(h, m), 256, 0, st>>>((const double *)wtmp, (float *)g.w, m);
             count_launch();
             DI_CUDA(cudaStreamSynchronize(st));
@@ -158,7 +160,8 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
             g.w_kind = DI_W_F32;
         }
     }
-    build_scales(h);
+
+    phase_mark(st, "create: check + scales");    build_scales(h);
 }
 
 static void free_transpose(DevGraph &g) {
@@ -407,7 +410,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // f32 weight storage must stay exact: promote to f64 if an added weight is not a float
         if (g.w_kind == DI_W_F32 && aw && fl[2]) {
             double *w64 = nullptr;
-            DI_CUDA(cudaMalloc(&w64, (g.m > 0 ? g.m : 1) * sizeof(double)));
+            DI_CUDA(cudaMallocAsync(&w64, (g.m > 0 ? g.m : 1) * sizeof(double), st));
             if (g.m > 0) {
                 k_f32_to_f64<<<grid_for(h, g.m), 256, 0, st>>>((const float *)g.w, w64, g.m);
                 count_launch();
@@ -425,7 +428,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         track(deg);
         DI_CUDA(cudaMallocAsync(&cursor, (n > 0 ? n : 1) * sizeof(int64_t), st));
         track(cursor);
-        DI_CUDA(cudaMalloc(&nrp, (n + 1) * sizeof(int64_t)));
+        DI_CUDA(cudaMallocAsync(&nrp, (n + 1) * sizeof(int64_t), st));
         if (n > 0) {
             k_new_deg<<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, del, chg, addcnt, n, deg);
             count_launch();
@@ -436,9 +439,9 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         DI_CUDA(cudaStreamSynchronize(st));
         int32_t *ncol = nullptr;
         void *nwt = nullptr;
-        DI_CUDA(cudaMalloc(&ncol, (m2 > 0 ? m2 : 1) * sizeof(int32_t)));
+        DI_CUDA(cudaMallocAsync(&ncol, (m2 > 0 ? m2 : 1) * sizeof(int32_t), st));
         const size_t es = g.w_kind == DI_W_F64 ? 8 : (g.w_kind == DI_W_F32 ? 4 : 0);
-        if (es) DI_CUDA(cudaMalloc(&nwt, (m2 > 0 ? m2 : 1) * es));
+        if (es) DI_CUDA(cudaMallocAsync(&nwt, (m2 > 0 ? m2 : 1) * es, st));
         if (n > 0) {
             if (g.w_kind == DI_W_F64)
                 k_copy_kept<double><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, del, chg,
@@ -478,7 +481,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             if (need > s.ent_cap) {
                 cudaFree(s.ent);
                 s.ent = nullptr;
-                DI_CUDA(cudaMalloc(&s.ent, need * sizeof(uint4)));
+                DI_CUDA(cudaMallocAsync(&s.ent, need * sizeof(uint4), st));
                 s.ent_cap = need;
             }
             // l as a function of the state (R5): sum of H over the

@@ -250,6 +250,9 @@ void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStre
 std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1,
                                                  int64_t count, int bits, cudaStream_t st);
 
+// ---- DIT_BUILD_TIMING (debug): host-side phase timer, stream-synchronised ----
+void phase_mark(cudaStream_t st, const char *name);
+
 // ---- device helpers ----
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

@@ -226,11 +226,11 @@ void build_plan_pieces(di_graph *h, PullPlan &pd) {
     DI_CUDA(cudaMemcpyAsync(&np, po + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     DI_CUDA(cudaStreamSynchronize(st));
     pd.npieces = np;
-    DI_CUDA(cudaMalloc(&pd.pieces, (np > 0 ? np : 1) * sizeof(uint4)));
-    DI_CUDA(cudaMalloc(&pd.pbuf, (np > 0 ? np : 1) * sizeof(double)));
-    DI_CUDA(cudaMalloc(&pd.fix, (nt > 0 ? nt : 1) * sizeof(int4)));
+    DI_CUDA(cudaMallocAsync(&pd.pieces, (np > 0 ? np : 1) * sizeof(uint4), st));
+    DI_CUDA(cudaMallocAsync(&pd.pbuf, (np > 0 ? np : 1) * sizeof(double), st));
+    DI_CUDA(cudaMallocAsync(&pd.fix, (nt > 0 ? nt : 1) * sizeof(int4), st));
     pd.ntiles = (m + kPullTile - 1) / kPullTile;
-    DI_CUDA(cudaMalloc(&pd.tile_start, (pd.ntiles + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMallocAsync(&pd.tile_start, (pd.ntiles + 1) * sizeof(int64_t), st));
     DI_CUDA(cudaMemcpyAsync(pd.tile_start + pd.ntiles, &pd.npieces, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     unsigned long long *nf;
     DI_CUDA(cudaMallocAsync(&nf, sizeof(unsigned long long), st));
@@ -270,10 +270,10 @@ void build_transpose(di_graph *h) {
     T.m = m;
     const bool wide = m >= (int64_t)0xffffffffLL;
     const size_t vsz = wide ? 8 : 4;
-    DI_CUDA(cudaMalloc(&T.ptr, (nt + 1) * sizeof(int64_t)));
-    DI_CUDA(cudaMalloc(&T.src, (m > 0 ? m : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMallocAsync(&T.ptr, (nt + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&T.src, (m > 0 ? m : 1) * sizeof(int32_t), st));
     const size_t wsz = g.w_kind == DI_W_F32 ? 4 : (g.w_kind == DI_W_F64 ? 8 : 0);
-    if (wsz) DI_CUDA(cudaMalloc(&T.w, (m > 0 ? m : 1) * wsz));
+    if (wsz) DI_CUDA(cudaMallocAsync(&T.w, (m > 0 ? m : 1) * wsz, st));
     int64_t *cnt = nullptr;
     DI_CUDA(cudaMallocAsync(&cnt, (nt + 1) * sizeof(int64_t), st));
     DI_CUDA(cudaMemsetAsync(cnt, 0, (nt + 1) * sizeof(int64_t), st));
@@ -302,6 +302,7 @@ void build_transpose(di_graph *h) {
         DI_CUDA(cudaFreeAsync(hc, st));
         DI_CUDA(cudaFreeAsync(ho, st));
         // in-degrees -> ptr
+        phase_mark(st, "transpose: radix sort");
         k_run_bounds<<<grid, kThreads, 0, st>>>(k0, m, cnt);
         count_launch();
         DI_CUDA(cudaMallocAsync(&esrc, m * 4, st));
@@ -325,9 +326,11 @@ void build_transpose(di_graph *h) {
         DI_CUDA(cudaFreeAsync(v0, st));
         DI_CUDA(cudaFreeAsync(v1, st));
     }
-    exclusive_scan_i64(cnt, T.ptr, nt, st);
+
+    phase_mark(st, "transpose: gather");    exclusive_scan_i64(cnt, T.ptr, nt, st);
     DI_CUDA(cudaFreeAsync(cnt, st));
     build_plan_pieces(h, T);
+    phase_mark(st, "transpose: pull pieces");
 }
 
 // ---------------------------------------------------------------- pull sweep

@@ -3,6 +3,10 @@
 // tile sums -> one-block scan of the tile sums -> tile-local scan + offset.
 #include "dit_internal.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace dit {
 
 constexpr int kScanItems = 8;
@@ -97,6 +101,17 @@ void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStre
     DI_CUDA(cudaMemcpyAsync(out + count, ts + ntiles, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     DI_CUDA(cudaFreeAsync(ts, st));
     DI_CUDA(cudaGetLastError());
+}
+
+// DIT_BUILD_TIMING=1: print the time since the previous mark (stream synchronised)
+void phase_mark(cudaStream_t st, const char *name) {
+    static const bool on = getenv("DIT_BUILD_TIMING") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[dit] %-28s %9.2f ms\n", name, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
 }
 
 }  // namespace dit

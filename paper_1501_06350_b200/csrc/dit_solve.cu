@@ -287,18 +287,18 @@ void ensure_state(di_graph *h) {
     const int64_t n = h->g.n;
     if (s.F) return;
     const int64_t nn = n > 0 ? n : 1;
-    DI_CUDA(cudaMalloc(&s.F, (h->g.nt > 0 ? h->g.nt : 1) * sizeof(double) + 16));   // +16: TMA tile rows
-    DI_CUDA(cudaMalloc(&s.H, nn * sizeof(double) + 16));
+    DI_CUDA(cudaMallocAsync(&s.F, (h->g.nt > 0 ? h->g.nt : 1) * sizeof(double) + 16, h->stream));   // +16: TMA tile rows
+    DI_CUDA(cudaMallocAsync(&s.H, nn * sizeof(double) + 16, h->stream));
     s.ent_cap = n + h->g.m / kSplit + 1;
-    DI_CUDA(cudaMalloc(&s.ent, s.ent_cap * sizeof(uint4)));
+    DI_CUDA(cudaMallocAsync(&s.ent, s.ent_cap * sizeof(uint4), h->stream));
     DI_CUDA(cudaMalloc(&s.ctrl, sizeof(Ctrl)));
     DI_CUDA(cudaMallocHost(&s.ctrl_host, sizeof(Ctrl)));
     std::memset(s.ctrl_host, 0, sizeof(Ctrl));
     // fixed grid for every grid-stride kernel: 8 resident 256-thread blocks per SM
     const int64_t want = (n + kThreads - 1) / kThreads;
     s.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->num_sms * 8));
-    DI_CUDA(cudaMalloc(&s.part, (size_t)s.grid * 3 * sizeof(double)));
-    DI_CUDA(cudaMalloc(&s.hist, kHistCap * sizeof(SweepRec)));
+    DI_CUDA(cudaMallocAsync(&s.part, (size_t)s.grid * 3 * sizeof(double), h->stream));
+    DI_CUDA(cudaMallocAsync(&s.hist, kHistCap * sizeof(SweepRec), h->stream));
     DI_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(Ctrl), h->stream));
 }
 
@@ -440,9 +440,9 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
         build_transpose(h);
         if (o.variant == DI_VARIANT_TILED) {
             build_tiles(h);
-            if (!s.A2) DI_CUDA(cudaMalloc(&s.A2, g.n * sizeof(double)));
+            if (!s.A2) DI_CUDA(cudaMallocAsync(&s.A2, g.n * sizeof(double), h->stream));
         }
-        if (!s.A) DI_CUDA(cudaMalloc(&s.A, g.n * sizeof(double)));
+        if (!s.A) DI_CUDA(cudaMallocAsync(&s.A, g.n * sizeof(double), h->stream));
     }
     s.rounds = o.local_rounds > 0 ? o.local_rounds : 4;
     DI_CUDA(cudaMemcpyAsync(s.ctrl_host, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));

@@ -263,46 +263,143 @@ __global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *_
     const unsigned lane = lane_id();
     const unsigned lt = (1u << lane) - 1u;
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    for (int64_t t = warp; t < nt; t += nw) {
+    // a warp takes 32 targets: their metadata in one coalesced round of loads,
+    // then their in-edges one target at a time (32 edges per step)
+    for (int64_t base = warp * 32; base < nt; base += nw * 32) {
+        const int64_t tl = base + lane;
+        int64_t mb = 0, me = 0, mro = 0, mlb = 0, mcap = 1;
+        int32_t mhx = -1;
+        int mpf = 0;
+        if (tl < nt) {
+            mb = tptr[tl];
+            me = tptr[tl + 1];
+            mhx = hidx[tl];
+            mro = mhx >= 0 ? hptr[tl] : rptr[tl];
+            if (tl < n) {
+                const int64_t tile = tl / kNodeTile;
+                mcap = vcap[tile];
+                mpf = vfirst[tile * kVfStride + (tl - tile * kNodeTile)];
+                mlb = ltile[tile];
+            }
+        }
+        const int cntT = (int)min((int64_t)32, nt - base);
+        for (int q = 0; q < cntT; ++q) {
+            const int64_t t = base + q;
+            const int64_t b = __shfl_sync(0xffffffffu, mb, q), e = __shfl_sync(0xffffffffu, me, q);
+            const int32_t hx = __shfl_sync(0xffffffffu, mhx, q);
+            const int64_t cap = __shfl_sync(0xffffffffu, mcap, q);
+            const int pf = __shfl_sync(0xffffffffu, mpf, q);
+            const int64_t lbase = __shfl_sync(0xffffffffu, mlb, q);
+            const bool owned = t < n;
+            const int64_t tile = owned ? t / kNodeTile : -1;
+            int64_t lo = 0;
+            int64_t ro = __shfl_sync(0xffffffffu, mro, q);
+            for (int64_t k0 = b; k0 < e; k0 += 32) {
+                const int64_t k = k0 + lane;
+                const bool ok = k < e;
+                const int32_t s = ok ? tsrc[k] : 0;
+                const bool loc = ok && (s / kNodeTile == tile);
+                const unsigned bl = __ballot_sync(0xffffffffu, loc);
+                const unsigned br = __ballot_sync(0xffffffffu, ok && !loc);
+                if (loc) {
+                    // balanced sliced-ELL: local in-edge s of t is slot s % cap of its piece s / cap
+                    const int64_t qq = lo + __popc(bl & lt);
+                    const int r = plist[tile * kVRows + pf + (int)(qq / cap)];
+                    const int64_t o = lbase + vofs[tile * kVofsStride + r / 32] + 32 * (qq % cap) + (r % 32);
+                    lsrc[o] = (uint16_t)(s - tile * kNodeTile);
+                    if (kW) lw[o] = tw[k];
+                } else if (ok) {
+                    const int64_t o = ro + __popc(br & lt);
+                    RemRec<W> r{};
+                    r.src = s;
+                    if constexpr (kW) r.w = tw[k];
+                    else r.w = 1.0f;
+                    if (hx >= 0) {
+                        htmp[o] = r;
+                        hkey[o] = (uint32_t)(s / stripe_nodes);
+                        hval[o] = (uint32_t)o;
+                        hof[o] = (uint32_t)hx;
+                    } else {
+                        rrec[o] = r;
+                    }
+                }
+                lo += __popc(bl);
+                ro += __popc(br);
+            }
+        }
+    }
+}
+
+// ---- edge-parallel plan build (hub targets with millions of in-edges must not
+// serialise on one warp): target of every CSC position, local flags, their
+// exclusive scan L, so that a local in-edge's rank within its target is
+// L[k] - L[tptr[t]] and a remote one's (k - tptr[t]) minus that.
+__global__ void k_fill_tkey(const int64_t *__restrict__ tptr, int64_t nt, uint32_t *__restrict__ tkey) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < nt; t += nw)
+        for (int64_t k = tptr[t] + lane_id(); k < tptr[t + 1]; k += 32) tkey[k] = (uint32_t)t;
+}
+
+__global__ void k_local_flags(const uint32_t *__restrict__ tkey, const int32_t *__restrict__ tsrc, int64_t m,
+                              int64_t n, int64_t *__restrict__ flag) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = tkey[k];
+        flag[k] = (t < n && tsrc[k] / kNodeTile == t / kNodeTile) ? 1 : 0;
+    }
+}
+
+__global__ void k_counts_from_scan(const int64_t *__restrict__ tptr, const int64_t *__restrict__ L, int64_t nt,
+                                   int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = tptr[t], e = tptr[t + 1];
+        lc[t] = L[e] - L[b];
+        rc[t] = (e - b) - lc[t];
+    }
+}
+
+// every in-edge to its class, one thread per CSC position (see k_split_edges)
+template <typename W>
+__global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *__restrict__ tkey,
+                             const int32_t *__restrict__ tsrc, const StoreW<W> *__restrict__ tw,
+                             const int64_t *__restrict__ L, int64_t m, int64_t n, const int64_t *__restrict__ ltile,
+                             const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
+                             const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
+                             const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
+                             const int32_t *__restrict__ hidx, int64_t stripe_nodes, uint16_t *__restrict__ lsrc,
+                             StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
+                             uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval, uint32_t *__restrict__ hof) {
+    constexpr bool kW = !std::is_same<W, NoW>::value;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = tkey[k];
+        const int32_t s = tsrc[k];
+        const int64_t b = tptr[t];
+        const int64_t lrank = L[k] - L[b];
         const bool owned = t < n;
         const int64_t tile = owned ? t / kNodeTile : -1;
-        const int32_t hx = hidx[t];
-        // balanced sliced-ELL: local in-edge s of t is slot s % cap of its piece s / cap
-        const int64_t cap = owned ? vcap[tile] : 1;
-        const int pf = owned ? vfirst[tile * kVfStride + (t - tile * kNodeTile)] : 0;
-        int64_t lo = 0;
-        int64_t ro = hx >= 0 ? hptr[t] : rptr[t];
-        for (int64_t k0 = b; k0 < e; k0 += 32) {
-            const int64_t k = k0 + lane;
-            const bool ok = k < e;
-            const int32_t s = ok ? tsrc[k] : 0;
-            const bool loc = ok && (s / kNodeTile == tile);
-            const unsigned bl = __ballot_sync(0xffffffffu, loc);
-            const unsigned br = __ballot_sync(0xffffffffu, ok && !loc);
-            if (loc) {
-                const int64_t q = lo + __popc(bl & lt);
-                const int r = plist[tile * kVRows + pf + (int)(q / cap)];
-                const int64_t o = ltile[tile] + vofs[tile * kVofsStride + r / 32] + 32 * (q % cap) + (r % 32);
-                lsrc[o] = (uint16_t)(s - tile * kNodeTile);
-                if (kW) lw[o] = tw[k];
-            } else if (ok) {
-                const int64_t o = ro + __popc(br & lt);
-                RemRec<W> r{};
-                r.src = s;
-                if constexpr (kW) r.w = tw[k];
-                else r.w = 1.0f;
-                if (hx >= 0) {
-                    htmp[o] = r;
-                    hkey[o] = (uint32_t)(s / stripe_nodes);
-                    hval[o] = (uint32_t)o;
-                    hof[o] = (uint32_t)hx;
-                } else {
-                    rrec[o] = r;
-                }
+        if (owned && s / kNodeTile == tile) {
+            // balanced sliced-ELL: local in-edge q of t is slot q % cap of its piece q / cap
+            const int64_t cap = vcap[tile];
+            const int pf = vfirst[tile * kVfStride + (t - tile * kNodeTile)];
+            const int r = plist[tile * kVRows + pf + (int)(lrank / cap)];
+            const int64_t o = ltile[tile] + vofs[tile * kVofsStride + r / 32] + 32 * (lrank % cap) + (r % 32);
+            lsrc[o] = (uint16_t)(s - tile * kNodeTile);
+            if constexpr (kW) lw[o] = tw[k];
+        } else {
+            const int32_t hx = hidx[t];
+            const int64_t o = (hx >= 0 ? hptr[t] : rptr[t]) + (k - b) - lrank;
+            RemRec<W> r{};
+            r.src = s;
+            if constexpr (kW) r.w = tw[k];
+            else r.w = 1.0f;
+            if (hx >= 0) {
+                htmp[o] = r;
+                hkey[o] = (uint32_t)(s / stripe_nodes);
+                hval[o] = (uint32_t)o;
+                hof[o] = (uint32_t)hx;
+            } else {
+                rrec[o] = r;
             }
-            lo += __popc(bl);
-            ro += __popc(br);
         }
     }
 }
@@ -432,6 +529,7 @@ static void build_tiles_t(di_graph *h) {
     constexpr bool kW = !std::is_same<W, NoW>::value;
     const size_t rs = sizeof(RemRec<W>);
     const int64_t nt = g.nt;                         // owned nodes + shard ghost slots
+    phase_mark(st, "tiles: start");
     tp.ntile = (n + kNodeTile - 1) / kNodeTile;
     tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
     const int64_t S = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
@@ -439,7 +537,18 @@ static void build_tiles_t(di_graph *h) {
     int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
     for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
         DI_CUDA(cudaMallocAsync(p, (nt + 1) * sizeof(int64_t), st));
-    k_count_local<<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, n, nt, lc, rc);
+    const int64_t m = g.m;
+    uint32_t *tkey = nullptr;
+    int64_t *lflag = nullptr, *L = nullptr;
+    DI_CUDA(cudaMallocAsync(&tkey, (m > 0 ? m : 1) * sizeof(uint32_t), st));
+    DI_CUDA(cudaMallocAsync(&lflag, (m + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&L, (m + 1) * sizeof(int64_t), st));
+    k_fill_tkey<<<grid, 256, 0, st>>>(g.t.ptr, nt, tkey);
+    if (m > 0) k_local_flags<<<grid_for(h, m), 256, 0, st>>>(tkey, g.t.src, m, n, lflag);
+    count_launch(2);
+    exclusive_scan_i64(lflag, L, m, st);
+    DI_CUDA(cudaFreeAsync(lflag, st));
+    k_counts_from_scan<<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, L, nt, lc, rc);
     k_classify<<<grid_for(h, tp.ntile), 256, 0, st>>>(rc, n, tp.ntile, lrc, hc, hflag);
     count_launch(2);
     if (nt > n) {
@@ -456,15 +565,16 @@ static void build_tiles_t(di_graph *h) {
         set_error("tiled plan: too many heavy remote edges for one graph handle");
         throw Fail{DI_ERR_INVALID};
     }
+    phase_mark(st, "tiles: classify");
     // ---- sliced-ELL layout of the local in-edges
     int32_t *vcap;
     int64_t *pcnt;
     DI_CUDA(cudaMallocAsync(&vcap, (tp.ntile + 1) * sizeof(int32_t), st));
     DI_CUDA(cudaMallocAsync(&pcnt, (tp.ntile + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMalloc(&tp.vofs, tp.ntile * kVofsStride * sizeof(uint32_t)));
-    DI_CUDA(cudaMalloc(&tp.vfirst, tp.ntile * kVfStride * sizeof(uint16_t)));
-    DI_CUDA(cudaMalloc(&tp.plist, tp.ntile * kVRows * sizeof(uint16_t)));
-    DI_CUDA(cudaMalloc(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMallocAsync(&tp.vofs, tp.ntile * kVofsStride * sizeof(uint32_t), st));
+    DI_CUDA(cudaMallocAsync(&tp.vfirst, tp.ntile * kVfStride * sizeof(uint16_t), st));
+    DI_CUDA(cudaMallocAsync(&tp.plist, tp.ntile * kVRows * sizeof(uint16_t), st));
+    DI_CUDA(cudaMallocAsync(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t), st));
     k_tile_layout<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
         lc, n, tp.ntile, tp.vofs, tp.vfirst, tp.plist, vcap, pcnt);
     count_launch();
@@ -472,35 +582,41 @@ static void build_tiles_t(di_graph *h) {
     tp.mpad = read_i64(tp.ltile + tp.ntile, st);
     tp.mloc = g.m - tp.mlight - tp.mh;
     // +16 B: aligned TMA supersets may read up to 15 bytes past the end
-    DI_CUDA(cudaMalloc(&tp.lsrc, tp.mpad * sizeof(uint16_t) + 16));
-    if (kW) DI_CUDA(cudaMalloc(&tp.lw, tp.mpad * sizeof(SW) + 16));
+    DI_CUDA(cudaMallocAsync(&tp.lsrc, tp.mpad * sizeof(uint16_t) + 16, st));
+    if (kW) DI_CUDA(cudaMallocAsync(&tp.lw, tp.mpad * sizeof(SW) + 16, st));
     if (tp.mpad > 0) {
         k_fill_pad<W><<<grid_for(h, tp.mpad), 256, 0, st>>>(tp.lsrc, (SW *)tp.lw, tp.mpad);
         count_launch();
     }
+    phase_mark(st, "tiles: ELL layout");
     // ---- per-node arrays, tile bases
-    DI_CUDA(cudaMalloc(&tp.rrel, n * sizeof(uint32_t) + 16));
-    DI_CUDA(cudaMalloc(&tp.hidx, nt * sizeof(int32_t) + 16));
-    DI_CUDA(cudaMalloc(&tp.wr, n * sizeof(float) + 16));
-    DI_CUDA(cudaMalloc(&tp.deg, n * sizeof(int32_t) + 16));
-    DI_CUDA(cudaMalloc(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t)));
+    DI_CUDA(cudaMallocAsync(&tp.rrel, n * sizeof(uint32_t) + 16, st));
+    DI_CUDA(cudaMallocAsync(&tp.hidx, nt * sizeof(int32_t) + 16, st));
+    DI_CUDA(cudaMallocAsync(&tp.wr, n * sizeof(float) + 16, st));
+    DI_CUDA(cudaMallocAsync(&tp.deg, n * sizeof(int32_t) + 16, st));
+    DI_CUDA(cudaMallocAsync(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t), st));
     k_tile_rel<<<grid_for(h, nt + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, nt, tp.ntile, tp.rrel, tp.hidx,
                                                     tp.deg, tp.rtile);
     k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.wr);
     count_launch(2);
+    phase_mark(st, "tiles: node arrays");
     // ---- edges to their classes
-    DI_CUDA(cudaMalloc(&tp.rrec, tp.mlight * rs + 16));
-    DI_CUDA(cudaMalloc(&tp.hrec, tp.mh * rs + 16));
+    DI_CUDA(cudaMallocAsync(&tp.rrec, tp.mlight * rs + 16, st));
+    DI_CUDA(cudaMallocAsync(&tp.hrec, tp.mh * rs + 16, st));
     const int64_t mh1 = tp.mh > 0 ? tp.mh : 1;
     RemRec<W> *htmp;
     uint32_t *k0, *v0, *k1, *v1, *hof, *hh;
     DI_CUDA(cudaMallocAsync(&htmp, mh1 * rs, st));
     for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
-    k_split_edges<W><<<grid, 256, 0, st>>>(g.t.ptr, g.t.src, (const SW *)g.t.w, n, tp.ltile, tp.vofs, tp.vfirst,
-                                           tp.plist, vcap, rptr,
-                                           hptr, tp.hidx, tp.stripe_nodes, nt, tp.lsrc, (SW *)tp.lw,
-                                           (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
+    if (m > 0)
+        k_split_flat<W><<<grid_for(h, m), 256, 0, st>>>(g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, L, m, n, tp.ltile,
+                                                        tp.vofs, tp.vfirst, tp.plist, vcap, rptr, hptr, tp.hidx,
+                                                        tp.stripe_nodes, tp.lsrc, (SW *)tp.lw, (RemRec<W> *)tp.rrec,
+                                                        htmp, k0, v0, hof);
+    DI_CUDA(cudaFreeAsync(tkey, st));
+    DI_CUDA(cudaFreeAsync(L, st));
     count_launch();
+    phase_mark(st, "tiles: split edges");
     // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
     tp.s_chunk.assign(S + 1, 0);
     tp.s_run.assign(S + 1, 0);
@@ -509,6 +625,7 @@ static void build_tiles_t(di_graph *h) {
         uint32_t *skey = sorted.first, *sval = sorted.second;
         k_heavy_gather<W><<<grid_for(h, tp.mh), 256, 0, st>>>(skey, sval, tp.mh, htmp, hof, (RemRec<W> *)tp.hrec, hh);
         count_launch();
+        phase_mark(st, "heavy: stripe sort");
         // stripe starts
         unsigned long long *scnt;
         DI_CUDA(cudaMallocAsync(&scnt, (S + 1) * sizeof(unsigned long long), st));
@@ -539,18 +656,19 @@ static void build_tiles_t(di_graph *h) {
         exclusive_scan_i64(runf, runid, tp.mh, st);
         exclusive_scan_i64(segf, segid, tp.mh, st);
         exclusive_scan_i64(chkf, chkid, tp.mh, st);
+        phase_mark(st, "heavy: flags + scans");
         tp.nrun = read_i64(runid + tp.mh, st);
         tp.nseg = read_i64(segid + tp.mh, st);
         if (read_i64(chkid + tp.mh, st) != tp.nchunk) {
             set_error("tiled plan: heavy chunk count mismatch");
             throw Fail{DI_ERR_CUDA};
         }
-        DI_CUDA(cudaMalloc(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t)));
-        DI_CUDA(cudaMalloc(&tp.chunk_start, (tp.nchunk + 1) * sizeof(int64_t)));
-        DI_CUDA(cudaMalloc(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t)));
-        DI_CUDA(cudaMalloc(&tp.run_h, tp.nrun * sizeof(int32_t)));
-        DI_CUDA(cudaMalloc(&tp.run_seg, (tp.nrun + 1) * sizeof(int64_t)));
-        DI_CUDA(cudaMalloc(&tp.part, tp.nseg * sizeof(double)));
+        DI_CUDA(cudaMallocAsync(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.chunk_start, (tp.nchunk + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.run_h, tp.nrun * sizeof(int32_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.run_seg, (tp.nrun + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.part, tp.nseg * sizeof(double), st));
         unsigned long long *frun;
         DI_CUDA(cudaMallocAsync(&frun, tp.nh * sizeof(unsigned long long), st));
         k_fill_u64<<<grid_for(h, tp.nh), 256, 0, st>>>(frun, tp.nh, ~0ull);
@@ -563,6 +681,7 @@ static void build_tiles_t(di_graph *h) {
         DI_CUDA(cudaMemcpyAsync(tp.chunk_start + tp.nchunk, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         DI_CUDA(cudaMemcpyAsync(tp.cfirst + tp.nchunk, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         DI_CUDA(cudaMemcpyAsync(tp.run_seg + tp.nrun, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        phase_mark(st, "heavy: index");
         // first run of every stripe
         for (int64_t s = 0; s < S; ++s) tp.s_run[s] = sbeg[s] < tp.mh ? read_i64(runid + sbeg[s], st) : tp.nrun;
         tp.s_run[S] = tp.nrun;
@@ -570,7 +689,8 @@ static void build_tiles_t(di_graph *h) {
         DI_CUDA(cudaFreeAsync(frun, st));
         DI_CUDA(cudaFreeAsync(scnt, st));
     }
-    DI_CUDA(cudaMalloc(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double)));
+    phase_mark(st, "tiles: heavy sort + index");
+    DI_CUDA(cudaMallocAsync(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double), st));
     unsigned long long *mx;
     DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
     DI_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
@@ -589,6 +709,7 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaGetLastError());
     tp.max_tile_edges = (int64_t)mxh;
     tp.built = true;
+    phase_mark(st, "tiles: free + done");
 }
 
 void build_tiles(di_graph *h) {
