@@ -82,7 +82,10 @@ struct PullPlan {
 // records would overflow kLightCap) are gathered by k_heavy over fixed chunks
 // of the heavy edge array (segments = target ∩ chunk), deterministic.
 constexpr int64_t kLightCap = 2048;     // light remote records per tile (shared memory)
-constexpr int64_t kHeavyTh = 16;        // remote in-degree above which a target is heavy
+#ifndef DIT_HEAVY_TH
+#define DIT_HEAVY_TH 16
+#endif
+constexpr int64_t kHeavyTh = DIT_HEAVY_TH;       // remote in-degree above which a target is heavy
 constexpr int64_t kHeavyChunk = 2048;   // heavy edges per k_heavy chunk
 
 struct TilePlan {
