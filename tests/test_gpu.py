@@ -124,32 +124,43 @@ def test_weight_storage_and_parity(eng):
 
 
 # ----------------------------------------------------------------- edge cases
-def test_edge_cases_small_graphs(eng):
+@pytest.mark.parametrize("variant", ["auto", "tiled"])
+def test_edge_cases_small_graphs(eng, variant):
+    kw = dict(variant=variant)
     # single dangling node: x = (1-d) Z; completed: 1
     G = eng.DIGraph(1, np.array([0, 0]), np.zeros(0, np.int32))
-    H, res = G.solve(d=D, tol=0.0)
+    H, res = G.solve(d=D, tol=0.0, **kw)
     assert H.item() == pytest.approx(0.15, abs=1e-16) and res["leak"] == pytest.approx(0.15)
-    H, res = G.solve(d=D, tol=0.0, dangling="complete")
+    H, res = G.solve(d=D, tol=0.0, dangling="complete", **kw)
     assert H.item() == pytest.approx(1.0, abs=1e-14)
     # golden 3-chain and 2-cycle
     ch = load("chain3.txt")
     rp, c, _ = csr_from_edges(3, ch["edges"])
-    H, res = eng.DIGraph(3, rp, c).solve(d=ch["d"], tol=0.0)
+    H, res = eng.DIGraph(3, rp, c).solve(d=ch["d"], tol=0.0, **kw)
     assert np.allclose(H.cpu().numpy(), ch["x"], atol=1e-16)
     cy = load("cycle2.txt")
     rp, c, _ = csr_from_edges(2, cy["edges"])
-    H, res = eng.DIGraph(2, rp, c).solve(d=cy["d"], Z=np.array([0.5, 0.5]), tol=1e-15)
+    H, res = eng.DIGraph(2, rp, c).solve(d=cy["d"], Z=np.array([0.5, 0.5]), tol=1e-15, **kw)
     assert np.allclose(H.cpu().numpy(), cy["x"], atol=1e-14)
     # self-loop only: x = (1-d)/(1-d) Z = 1 on one node
-    H, res = eng.DIGraph(1, np.array([0, 1]), np.array([0], np.int32)).solve(d=D, tol=1e-15)
+    H, res = eng.DIGraph(1, np.array([0, 1]), np.array([0], np.int32)).solve(d=D, tol=1e-15, **kw)
     assert H.item() == pytest.approx(1.0, abs=1e-13)
-    # empty graph n = 0
+    # empty graph n = 0, and nodes without any edge
     G0 = eng.DIGraph(0, np.array([0]), np.zeros(0, np.int32))
-    H, res = G0.solve(d=D, tol=1e-12)
+    H, res = G0.solve(d=D, tol=1e-12, **kw)
     assert H.numel() == 0 and res["sweeps"] == 0
+    Ge = eng.DIGraph(700, np.zeros(701, np.int64), np.zeros(0, np.int32))
+    H, res = Ge.solve(d=D, tol=0.0, **kw)
+    assert np.allclose(H.cpu().numpy(), 0.15 / 700, rtol=1e-15) and res["converged"]
+    # a ring longer than a tile: all pushes remote at the tile seams, exact x = 1/n
+    n = 1100
+    rp = np.arange(n + 1, dtype=np.int64)
+    c = ((np.arange(n) + 1) % n).astype(np.int32)
+    H, res = eng.DIGraph(n, rp, c).solve(d=D, tol=1e-14, **kw)
+    assert np.abs(H.cpu().numpy() - 1.0 / n).sum() <= 1e-12
 
 
-@pytest.mark.parametrize("variant", ["push", "pull"])
+@pytest.mark.parametrize("variant", ["push", "pull", "tiled"])
 def test_heavy_rows_hubs_and_ragged_sizes(eng, variant):
     # out-degrees far above the 512-edge split, a hub with in-degree far above
     # the 256-edge pull piece, n not a multiple of 32 / 256
