@@ -46,6 +46,14 @@ namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // thread i owns node i of the tile
 constexpr int kTileWarps = kTileThreads / 32;
+// k_tile launch shape: 1024 threads (32 warps, one per virtual warp of pieces)
+// and one CTA per SM, or 512 threads (two virtual warps each) and two per SM
+#ifndef DIT_TILE_BLOCK
+#define DIT_TILE_BLOCK 512
+#endif
+constexpr int kTileBlock = DIT_TILE_BLOCK;
+constexpr int kTileBlocksPerSM = kTileBlock == 1024 ? 1 : 2;
+constexpr int kTileBlockWarps = kTileBlock / 32;
 constexpr int kVRows = 2 * (int)kNodeTile;       // local-edge pieces per tile (at most)
 constexpr int kVWarps = kVRows / 32;             // virtual warps: real warp w runs w and kVWarps-1-w
 constexpr int kVofsStride = 36;                  // u32 per tile (kVWarps + 1, padded to 16 B)
@@ -857,7 +865,12 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     int s = 0;
     for (; s + 4 <= K; s += 4) {
         const int k = base + 32 * s;
+#ifdef DIT_EXPERIMENT_NOCONFLICT
+        const int s0 = (es[k] & 0) + (threadIdx.x & 31), s1 = (es[k + 32] & 0) + (threadIdx.x & 31),
+                  s2 = (es[k + 64] & 0) + (threadIdx.x & 31), s3 = (es[k + 96] & 0) + (threadIdx.x & 31);
+#else
         const int s0 = es[k], s1 = es[k + 32], s2 = es[k + 64], s3 = es[k + 96];
+#endif
         double v0 = gq[s0], v1 = gq[s1], v2 = gq[s2], v3 = gq[s3];
         if constexpr (kW) {
             v0 *= (double)ew[k];
@@ -959,7 +972,7 @@ __device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *F
 // Persistent kernel, one 512-thread CTA per SM, tiles round-robin; the next
 // tile's bundle streams in (TMA) while the current tile gathers and diffuses.
 template <typename W>
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
+__global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool kW = !std::is_same<W, NoW>::value;
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
@@ -968,8 +981,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     double *psum = gq + kNodeTile + 2;                                   // [kVRows]: piece sums by rank
     const int bufsz = (int)(tile_buf_fixed<W>() + a.edge_cap);
     __shared__ __align__(8) unsigned long long bars[2];
-    __shared__ double s_r[kTileWarps], s_l[kTileWarps];
-    __shared__ unsigned long long s_c[kTileWarps][2];
+    __shared__ double s_r[kTileBlockWarps], s_l[kTileBlockWarps];
+    __shared__ unsigned long long s_c[kTileBlockWarps][2];
     __shared__ bool s_last;
     if (ctrl->done || ctrl->use_pull != kUseTiled) return;
     const double d = ctrl->d;
@@ -1041,7 +1054,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
         const int R = (int)(r1 - r0);
         RemRec<W> *recs = reinterpret_cast<RemRec<W> *>(rbuf + (r0 * kRS - rb0));
 #pragma unroll 4
-        for (int q = i; q < R; q += kTileThreads) {
+        for (int q = i; q < R; q += kTileBlock) {
             const RemRec<W> r = recs[q];
             *reinterpret_cast<double *>(&recs[q]) = Aprev[r.src] * rec_w(r);
         }
@@ -1078,15 +1091,22 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
                 edges += (unsigned long long)dgi;
                 q = d * f * ivi;                     // d F(i) / sum_k w_{i,k}
             }
-            gq[i] = q;
+            if (i < kTileThreads) gq[i] = q;
             __syncthreads();
-            // Eq. (8) local pushes: this warp's two virtual warps of pieces (longest with shortest)
+            if constexpr (kTileBlockWarps == kVWarps) {
+                // Eq. (8) local pushes: warp w runs virtual warp w of pieces
+                const uint32_t o0 = vofs_s[wp];
+                const int K = (int)((vofs_s[wp + 1] - o0) >> 5);
+                if (K) psum[wp * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
+            } else {
+                // Eq. (8) local pushes: this warp's two virtual warps of pieces (longest with shortest)
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                const int vw = h2 ? kVWarps - 1 - wp : wp;
-                const uint32_t o0 = vofs_s[vw];
-                const int K = (int)((vofs_s[vw + 1] - o0) >> 5);
-                if (K) psum[vw * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int vw = h2 ? kVWarps - 1 - wp : wp;
+                    const uint32_t o0 = vofs_s[vw];
+                    const int K = (int)((vofs_s[vw + 1] - o0) >> 5);
+                    if (K) psum[vw * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
+                }
             }
             __syncthreads();
             if (valid) {                              // the node's pieces, in edge order
@@ -1135,7 +1155,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileArgs<W> a, Ctrl *_
     if (threadIdx.x == 0) {
         double rr = 0.0, ll = 0.0;
         unsigned long long x = 0, y = 0;
-        for (int q = 0; q < kTileWarps; ++q) {
+        for (int q = 0; q < kTileBlockWarps; ++q) {
             rr += s_r[q];
             ll += s_l[q];
             x += s_c[q][0];
@@ -1269,21 +1289,24 @@ static void launch_tile_kernel_t(di_graph *h, int rounds) {
     State &s = h->s;
     TilePlan &tp = g.tl;
     if (!tp.tile_smem) {
-        // two CTAs per SM, each with the shared head (gq, psum) and two bundle
-        // buffers; computed (and the attribute set) once per plan, off the sweep path
+        // kTileBlocksPerSM CTAs per SM, each with the shared head (gq, psum) and two
+        // bundle buffers; computed (and the attribute set) once per plan, off the sweep path
         int per_sm = 0;
         DI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
         cudaFuncAttributes fa;
         DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
         constexpr bool kW = !std::is_same<W, NoW>::value;
         const int64_t fixed = tile_buf_fixed<W>();
-        const int64_t budget = ((int64_t)per_sm / 2 - 1024 - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
+        int optin = 0;
+        DI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        const int64_t per_cta = std::min<int64_t>(optin, (int64_t)per_sm / kTileBlocksPerSM - 1024);
+        const int64_t budget = (per_cta - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
         const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
         int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
         cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
-        // local edges are read from L1/L2 in the rounds (prefetched to L2 with the
-        // bundle): measured faster than staging the few tiles that fit
-        if (!getenv("DIT_EDGE_STAGING")) cap = 0;
+        // with two CTAs per SM the edge buffers do not fit: the rounds read the
+        // edges from L1/L2 (prefetched to L2 with the bundle)
+        if (kTileBlocksPerSM > 1 || getenv("DIT_NO_EDGE_STAGING")) cap = 0;
         tp.edge_cap = cap;
         tp.tile_smem = (size_t)(kSharedHead + 2 * (fixed + cap));
         DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
@@ -1299,8 +1322,8 @@ static void launch_tile_kernel_t(di_graph *h, int rounds) {
         }
         a.dbg = g_tile_dbg;
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 2));
-    k_tile<W><<<grid, kTileThreads, smem, h->stream>>>(a, s.ctrl);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * kTileBlocksPerSM));
+    k_tile<W><<<grid, kTileBlock, smem, h->stream>>>(a, s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());
 }

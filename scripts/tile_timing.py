@@ -9,7 +9,7 @@ rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 spec = synth.CONFIGS[2]
 g = synth.generate(spec)
 G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
-H, r = G.solve(d=spec.d, tol=spec.tol, variant="tiled", local_rounds=rounds)
+H, r = G.solve(d=spec.d, tol=spec.tol, variant="tiled", local_rounds=rounds, max_sweeps=int(os.environ.get("MAX_SWEEPS", "0")))
 out = (ctypes.c_double * 5)()
 _lib._lib.di_debug_tile_timing(out)
 v = list(out)
