@@ -211,62 +211,69 @@ int64_t orc_power_iteration(int64_t n, const int64_t *col_ptr, const int32_t *ro
 }
 
 /* ------------------------------------------------------------------------
- * Tile-local sweeps (reading R12), a D-Iteration schedule
+ * Tile-local sweeps (readings R12, R15), a D-Iteration schedule
  * ("freedom in the choice of a scheduler", §3.4), step by step:
  *   1. r = |F|_1; stop if r <= tol.
- *   2. for each tile [a, a+tile) in ascending order, starting from the tile's
- *      fluid f = F[a..): `rounds` times: every tile node i with f(i) != 0 is
- *      diffused (Eq. (8), (10)): D(i) += f(i), and d f(i) P_{t,i} is pushed
- *      to its out-neighbours t INSIDE the tile (the new f); F[a..) = f.
- *   3. then, for every node i, the pushes of all its diffusions to targets
- *      OUTSIDE its tile: F(t) += d D(i) P_{t,i} (Eq. (8) is linear in the
- *      diffused amount, so the deferred pushes add up to the same fluid).
- *   4. H += D; l += D(i) for dangling i (§3.3).
- * rounds = 1 is the theta = 0 sweep of orc_sweep_run.
+ *   2. for each wave c = 0 .. waves-1 (tile index mod waves = c):
+ *      a. for each tile [a, a+tile) of the wave, in ascending order, starting
+ *         from the tile's fluid f = F[a..): `rounds` times: every tile node i
+ *         with f(i) != 0 is diffused (Eqs. (8), (10)): D(i) += f(i), and
+ *         d f(i) P_{t,i} is pushed to its out-neighbours t INSIDE the tile (the
+ *         new f); F[a..) = f.
+ *      b. then, for every node i of the wave, the pushes of all its diffusions
+ *         to targets OUTSIDE its tile: F(t) += d D(i) P_{t,i} (Eq. (8) is
+ *         linear in the diffused amount) -- a tile of a later wave takes them
+ *         in during this sweep, any other tile in the next one.
+ *      c. H += D; l += D(i) for dangling i (§3.3).
+ * waves = 1, rounds = 1 is the theta = 0 sweep of orc_sweep_run.
  * ---------------------------------------------------------------------- */
 int64_t orc_tiled_sweep_run(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, const double *pval,
-                            double d, int64_t tile, int rounds, double tol, int64_t max_sweeps, double *F,
-                            double *H, double *leak, int64_t *edges, int64_t *nodes, double *residual_out)
+                            double d, int64_t tile, int rounds, int waves, double tol, int64_t max_sweeps,
+                            double *F, double *H, double *leak, int64_t *edges, int64_t *nodes,
+                            double *residual_out)
 {
     int64_t sweeps = 0;
     double *D = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double *f = (double *)malloc(sizeof(double) * (size_t)(tile > 0 ? tile : 1));
     double *fn = (double *)malloc(sizeof(double) * (size_t)(tile > 0 ? tile : 1));
     double r = 0.0;
+    if (waves < 1) waves = 1;
     for (;;) {
         r = 0.0;
         for (int64_t i = 0; i < n; ++i) r += fabs(F[i]);
         if (r <= tol || sweeps >= max_sweeps) break;
-        for (int64_t i = 0; i < n; ++i) D[i] = 0.0;
-        for (int64_t a = 0; a < n; a += tile) {
-            int64_t z = a + tile < n ? a + tile : n;
-            for (int64_t i = a; i < z; ++i) f[i - a] = F[i];
-            for (int k = 0; k < rounds; ++k) {
-                for (int64_t i = a; i < z; ++i) fn[i - a] = 0.0;
-                for (int64_t i = a; i < z; ++i) {
-                    double fi = f[i - a];
-                    if (fi == 0.0) continue;
-                    D[i] += fi;
-                    *nodes += 1;
-                    *edges += col_ptr[i + 1] - col_ptr[i];
-                    for (int64_t e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
-                        int64_t t = row_idx[e];
-                        if (t >= a && t < z) fn[t - a] += d * fi * pval[e];
+        for (int c = 0; c < waves; ++c) {
+            for (int64_t i = 0; i < n; ++i) D[i] = 0.0;
+            for (int64_t a = (int64_t)c * tile; a < n; a += (int64_t)waves * tile) {
+                int64_t z = a + tile < n ? a + tile : n;
+                for (int64_t i = a; i < z; ++i) f[i - a] = F[i];
+                for (int k = 0; k < rounds; ++k) {
+                    for (int64_t i = a; i < z; ++i) fn[i - a] = 0.0;
+                    for (int64_t i = a; i < z; ++i) {
+                        double fi = f[i - a];
+                        if (fi == 0.0) continue;
+                        D[i] += fi;
+                        *nodes += 1;
+                        *edges += col_ptr[i + 1] - col_ptr[i];
+                        for (int64_t e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
+                            int64_t t = row_idx[e];
+                            if (t >= a && t < z) fn[t - a] += d * fi * pval[e];
+                        }
                     }
+                    for (int64_t i = a; i < z; ++i) f[i - a] = fn[i - a];
                 }
-                for (int64_t i = a; i < z; ++i) f[i - a] = fn[i - a];
+                for (int64_t i = a; i < z; ++i) F[i] = f[i - a];
             }
-            for (int64_t i = a; i < z; ++i) F[i] = f[i - a];
-        }
-        for (int64_t i = 0; i < n; ++i) {
-            if (D[i] == 0.0) continue;
-            int64_t a = (i / tile) * tile, z = a + tile;
-            if (col_ptr[i] == col_ptr[i + 1]) *leak += D[i];
-            for (int64_t e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
-                int64_t t = row_idx[e];
-                if (t < a || t >= z) F[t] += d * D[i] * pval[e];
+            for (int64_t i = 0; i < n; ++i) {
+                if (D[i] == 0.0) continue;
+                int64_t a = (i / tile) * tile, z = a + tile;
+                if (col_ptr[i] == col_ptr[i + 1]) *leak += D[i];
+                for (int64_t e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
+                    int64_t t = row_idx[e];
+                    if (t < a || t >= z) F[t] += d * D[i] * pval[e];
+                }
+                H[i] += D[i];
             }
-            H[i] += D[i];
         }
         ++sweeps;
     }

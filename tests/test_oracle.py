@@ -365,21 +365,43 @@ def test_tiled_one_round_equals_theta0_sweep():
         assert a.edges == b.edges and a.nodes == b.nodes
 
 
-@pytest.mark.parametrize("tile,rounds", [(16, 2), (64, 5), (1024, 3)])
-def test_tiled_conservation_and_convergence(tile, rounds):
+def test_tiled_waves_absorb_in_the_same_sweep():
+    # R15: tile 0 -> tile 1 push (edge 0 -> 4, tile = 4): with two waves tile 1
+    # takes it in during the sweep that produced it, with one wave a sweep later
+    n, d = 8, 0.85
+    rp, c, _ = csr_from_edges(n, [(0, 4)])
+    cp, ri, pv = graph.column_entries(n, rp, c)
+    f0 = (1 - d) / n
+    st = di.di_init(n, d)
+    r2 = di.tiled_sweep_run(n, cp, ri, pv, d, st.F, st.H, tile=4, rounds=1, tol=0, max_sweeps=1, waves=2)
+    assert r2.H[0] == f0 and r2.H[4] == pytest.approx(f0 * (1 + d), rel=1e-15) and np.all(r2.F == 0)
+    assert r2.leak == pytest.approx(n * f0 + d * f0 - f0, rel=1e-15)      # all but node 0 dangling
+    r1 = di.tiled_sweep_run(n, cp, ri, pv, d, st.F, st.H, tile=4, rounds=1, tol=0, max_sweeps=1, waves=1)
+    assert r1.H[4] == f0 and r1.F[4] == pytest.approx(d * f0, rel=1e-15)
+    # one wave per tile from node 4's side: the push goes back to the earlier wave
+    rp, c, _ = csr_from_edges(n, [(4, 0)])
+    cp, ri, pv = graph.column_entries(n, rp, c)
+    r = di.tiled_sweep_run(n, cp, ri, pv, d, st.F, st.H, tile=4, rounds=1, tol=0, max_sweeps=1, waves=2)
+    assert r.H[0] == f0 and r.F[0] == pytest.approx(d * f0, rel=1e-15)
+
+
+@pytest.mark.parametrize("tile,rounds,waves", [(16, 2, 1), (64, 5, 1), (1024, 3, 1), (16, 2, 2), (32, 3, 3),
+                                               (16, 1, 5)])
+def test_tiled_conservation_and_convergence(tile, rounds, waves):
     g = small_graph(200, 13)
     cp, ri, pv = cols_of(g)
     P = graph.dense_P(g.n, cp, ri, pv)
     st = di.di_init(g.n, D)
     F, H, lk = st.F, st.H, 0.0
     for _ in range(6):
-        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, F, H, tile=tile, rounds=rounds, tol=0, max_sweeps=1, leak=lk)
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, F, H, tile=tile, rounds=rounds, tol=0, max_sweeps=1, leak=lk,
+                               waves=waves)
         F, H, lk = r.F, r.H, r.leak
         assert np.abs(H + F - st.F0 - D * (P @ H)).max() <= 1e-15           # Eq. (12)
         assert lk == pytest.approx(H[graph.dangling_mask(g.n, g.row_ptr)].sum(), abs=1e-15)
     x = dense.dense_solve(P, D, synth.uniform_Z(g.n))
-    r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=rounds, tol=1e-13)
+    r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=rounds, tol=1e-13, waves=waves)
     assert np.abs(r.H - x).sum() <= 1e-12
     # more local rounds never need more sweeps than one round
-    r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13)
+    r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13, waves=waves)
     assert r.steps <= r1.steps
