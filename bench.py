@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--variant", default="tiled", choices=["auto", "push", "pull", "tiled"])
-    p.add_argument("--rounds", type=int, default=3, help="local rounds per sweep (variant tiled)")
+    p.add_argument("--rounds", type=int, default=4, help="local rounds per sweep (variant tiled)")
     p.add_argument("--theta", type=float, default=1.0)
     p.add_argument("--tol", type=float, default=None)
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -117,6 +117,7 @@ def workload_name(spec, cfg):
 
 # ------------------------------------------------------------------ CPU oracle
 TILE_NODES = 512   # include/dit.h DI_TILE_NODES (the oracle takes the tile as a parameter)
+TILE_WAVES = 2     # include/dit.h DI_TILE_WAVES
 
 
 def oracle_run(args, spec, cols, n, sweeps):
@@ -131,7 +132,7 @@ def oracle_run(args, spec, cols, n, sweeps):
     t0 = time.perf_counter()
     if args.variant == "tiled":
         r = odi.tiled_sweep_run(n, cp, ri, pv, spec.d, F, H, tile=TILE_NODES, rounds=args.rounds, tol=0.0,
-                                max_sweeps=sweeps)
+                                max_sweeps=sweeps, waves=TILE_WAVES)
     else:
         r = odi.sweep_run(n, cp, ri, pv, spec.d, F, H, theta=args.theta, tol=0.0, max_sweeps=sweeps)
     return r.edges, time.perf_counter() - t0
@@ -143,7 +144,7 @@ def oracle_cols(g):
 
 
 def oracle_desc(args, sweeps):
-    sched = (f"tiled sweep (tile {TILE_NODES}, {args.rounds} rounds)" if args.variant == "tiled"
+    sched = (f"tiled sweep (tile {TILE_NODES}, {args.rounds} rounds, {TILE_WAVES} waves)" if args.variant == "tiled"
              else f"theta={args.theta} frontier sweep")
     return f"first {sweeps} {sched} sweep(s) of the cold solve on the full graph, single-threaded C oracle"
 

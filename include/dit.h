@@ -73,6 +73,10 @@ extern "C" {
                                      the next sweep (deterministic); every node holding fluid
                                      diffuses (theta is not used). */
 #define DI_TILE_NODES 512         /* node ids per tile of DI_VARIANT_TILED */
+#define DI_TILE_WAVES 2           /* DI_VARIANT_TILED on one GPU: the tiles of a sweep run in this
+                                     many waves (tile index mod waves); a wave's pushes to tiles
+                                     of later waves are taken in during the same sweep (DESIGN.md
+                                     R15).  Shards run one wave. */
 
 typedef struct di_graph di_graph;  /* opaque: device CSR + derived arrays + DI state */
 
@@ -84,7 +88,7 @@ typedef struct {
     int32_t dangling;    /* DI_DANGLING_*, default DI_DANGLING_DROP */
     int64_t max_sweeps;  /* stop after this many sweeps even if |F|_1 > tol; <= 0: 10^7 */
     double  pull_frac;   /* AUTO: use pull when frontier out-edges > pull_frac * m; default 0.25 */
-    int32_t local_rounds;/* TILED: diffusion rounds per tile per sweep (>= 1), default 3 */
+    int32_t local_rounds;/* TILED: diffusion rounds per tile per sweep (>= 1), default 4 */
     int32_t reserved;
 } di_solve_opts;
 

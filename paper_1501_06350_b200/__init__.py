@@ -39,7 +39,7 @@ class DIGraph:
         return out
 
     def solve(self, d=0.85, Z=None, tol=1e-12, out=None, theta=1.0, variant="auto", dangling="drop",
-              max_sweeps=0, pull_frac=0.25, local_rounds=3):
+              max_sweeps=0, pull_frac=0.25, local_rounds=4):
         out = self._out(out)
         res = di_solve(self.handle, d, Z, tol, out, theta=theta, variant=VARIANTS[variant],
                        dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac,
@@ -47,7 +47,7 @@ class DIGraph:
         return out, res.as_dict()
 
     def resume(self, tol=1e-12, out=None, theta=1.0, variant="auto", dangling="drop", max_sweeps=0,
-               pull_frac=0.25, local_rounds=3):
+               pull_frac=0.25, local_rounds=4):
         out = self._out(out)
         res = di_resume(self.handle, tol, out, theta=theta, variant=VARIANTS[variant],
                         dangling=DANGLING[dangling], max_sweeps=max_sweeps, pull_frac=pull_frac,

@@ -29,6 +29,7 @@ DI_W_NONE, DI_W_F32, DI_W_F64 = 0, 1, 2
 DI_DANGLING_DROP, DI_DANGLING_COMPLETE = 0, 1
 DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL, DI_VARIANT_TILED = 0, 1, 2, 3
 DI_TILE_NODES = 512   # include/dit.h
+DI_TILE_WAVES = 2     # include/dit.h (single GPU; shards run one wave)
 SHARD_TILED = True    # DI_VARIANT_TILED on shards (di_shard_* with di_shard_flush / _flush_apply)
 SHARD_TILED_FALLBACK = "pull"
 
@@ -173,7 +174,7 @@ def di_graph_info(h):
 
 
 def _opts(theta=1.0, variant=DI_VARIANT_AUTO, dangling=DI_DANGLING_DROP, max_sweeps=0, pull_frac=0.25,
-          local_rounds=3):
+          local_rounds=4):
     o = di_solve_opts_default()
     o.theta, o.variant, o.dangling, o.max_sweeps, o.pull_frac = theta, variant, dangling, max_sweeps, pull_frac
     o.local_rounds = local_rounds

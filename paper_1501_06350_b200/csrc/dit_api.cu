@@ -88,7 +88,7 @@ void di_solve_opts_default(di_solve_opts *o) {
     o->dangling = DI_DANGLING_DROP;
     o->max_sweeps = 10000000;
     o->pull_frac = 0.25;
-    o->local_rounds = 3;
+    o->local_rounds = 4;
 }
 
 const char *di_last_error(void) { return t_err.c_str(); }

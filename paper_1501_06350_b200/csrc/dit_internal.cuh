@@ -27,6 +27,7 @@ struct SweepRec {
     int use_pull, pad;
 };
 constexpr int64_t kHistCap = 1 << 16;
+constexpr int kEvPerSweep = 8;          // profiling events per sweep (tiled: 2 W + 1)
 
 // Device-resident control block: the solver loop runs without host round
 // trips; the host polls `done` once per chunk of sweeps.
@@ -128,7 +129,10 @@ struct TilePlan {
     int64_t *cfirst = nullptr;     // [nchunk+1] first segment of each chunk
     int32_t *run_h = nullptr;      // [nrun] heavy index of each run (high bit: first run of the target)
     int64_t *run_seg = nullptr;    // [nrun+1] first segment of each run
-    std::vector<int64_t> s_chunk, s_run;   // per stripe [S+1]: first chunk, first run
+    std::vector<int64_t> s_chunk, s_run;   // per (wave, stripe) group [W S + 1]: first chunk, first run
+    int waves = 1;                 // tile waves per sweep (R15): wave of tile t = t % waves
+    int64_t nstripe = 0;           // source stripes S
+    double *tpart = nullptr;       // k_tile partials [2][waves][grid]
     double *part = nullptr;        // [nseg] segment partial sums
     double *hsum = nullptr;        // [nh] remote inflow of each heavy target
     int64_t max_tile_edges = 0;    // most local in-edges of one tile

@@ -166,10 +166,9 @@ void shard_apply(di_graph *h, const double *recv, int force) {
 
 void shard_reduce(di_graph *h) {
     if (h->s.tiled_call) {
-        const int64_t k = h->s.launched;
-        mark_event(h, k, 2);
+        const int64_t k = h->s.launched;       // shards run one wave: events 0, 1, 2
         launch_tile_kernel(h, h->s.rounds);
-        mark_event(h, k, 3);
+        mark_event(h, k, 2);
         mark_event(h, k, 4);
         h->s.launched += 1;
         return;

@@ -392,25 +392,31 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
     unsigned long long prev_nodes = 0;
     for (int64_t k = 0; k < S; ++k) {
         float t[4];
-        for (int q = 0; q < 4; ++q) DI_CUDA(cudaEventElapsedTime(&t[q], s.events[5 * k + q], s.events[5 * k + q + 1]));
+        auto ev = [&](int q) { return s.events[kEvPerSweep * k + q]; };
         const SweepRec &rc = hs[k];
         const double nodes = (double)(rc.nodes_cum - prev_nodes);
         prev_nodes = rc.nodes_cum;
         if (rc.use_pull == kUseTiled) {
-            // heavy remote gather (stripe kernels) in slot 0, the fused tile kernel in slot 2
+            // waves: [2c] -> [2c+1] heavy gather of wave c, [2c+1] -> [2c+2] its tile kernel
             // (per node 66 B, per local edge 2 + w, per light record rec + 8,
-            // per heavy edge rec + 8, per heavy segment 24 B)
+            // per heavy edge rec + 8, per heavy segment / run 24 B)
             const TilePlan &tp = g.tl;
             const double rec = g.w_kind == DI_W_F64 ? 16.0 : 8.0;
-            p.pull_ms += t[0];
+            for (int c = 0; c < tp.waves; ++c) {
+                float th, tt;
+                DI_CUDA(cudaEventElapsedTime(&th, ev(2 * c), ev(2 * c + 1)));
+                DI_CUDA(cudaEventElapsedTime(&tt, ev(2 * c + 1), ev(2 * c + 2)));
+                p.pull_ms += th;
+                p.tile_ms += tt;
+            }
             p.pull_bytes += (double)tp.mh * (rec + 8.0) + 24.0 * (double)tp.nseg + 24.0 * (double)tp.nrun;
             p.pull_launches += 1;
-            p.tile_ms += t[2];
             p.tile_bytes += 66.0 * n + (double)tp.mloc * (2.0 + wb) + (double)tp.mlight * (rec + 8.0) +
                             8.0 * (double)tp.nh;
             p.tile_launches += 1;
             continue;
         }
+        for (int q = 0; q < 4; ++q) DI_CUDA(cudaEventElapsedTime(&t[q], ev(q), ev(q + 1)));
         p.select_ms += t[0];
         p.select_bytes += 8.0 * n + 48.0 * nodes + (rc.use_pull ? 8.0 * n : 16.0 * (double)rc.entries);
         p.select_launches += 1;
@@ -470,7 +476,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
 void mark_event(di_graph *h, int64_t sweep, int k) {  // profiling events (declared in dit_internal.cuh)
     State &s = h->s;
     if (!s.profile || sweep >= kHistCap) return;
-    const size_t idx = (size_t)sweep * 5 + k;
+    const size_t idx = (size_t)sweep * kEvPerSweep + k;
     while (s.events.size() <= idx) {
         cudaEvent_t e;
         DI_CUDA(cudaEventCreate(&e));

@@ -79,6 +79,11 @@ template <typename W>
 __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w; }
 
 constexpr int64_t kStripeBytes = 48ll << 20;   // outflow slice per heavy stripe (L2-resident)
+#ifndef DIT_TILE_WAVES
+#define DIT_TILE_WAVES 2
+#endif
+constexpr int kTileWaves = DIT_TILE_WAVES;      // tile waves per sweep (R15), single GPU
+__device__ __forceinline__ int tile_wave(int64_t node, int waves) { return (int)((node / kNodeTile) % waves); }
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -253,91 +258,6 @@ __global__ void k_fill_pad(uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ 
     }
 }
 
-// every in-edge (ascending source within its target) to its class: local ->
-// sliced-ELL slot; light remote -> the tile's record block; heavy remote ->
-// a record in CSC order plus its sort key (source stripe) and heavy index
-template <typename W>
-__global__ void k_split_edges(const int64_t *__restrict__ tptr, const int32_t *__restrict__ tsrc,
-                              const StoreW<W> *__restrict__ tw, int64_t n, const int64_t *__restrict__ ltile,
-                              const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
-                              const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
-                              const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
-                              const int32_t *__restrict__ hidx, int64_t stripe_nodes, int64_t nt,
-                              uint16_t *__restrict__ lsrc,
-                              StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
-                              uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval, uint32_t *__restrict__ hof) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const unsigned lane = lane_id();
-    const unsigned lt = (1u << lane) - 1u;
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    // a warp takes 32 targets: their metadata in one coalesced round of loads,
-    // then their in-edges one target at a time (32 edges per step)
-    for (int64_t base = warp * 32; base < nt; base += nw * 32) {
-        const int64_t tl = base + lane;
-        int64_t mb = 0, me = 0, mro = 0, mlb = 0, mcap = 1;
-        int32_t mhx = -1;
-        int mpf = 0;
-        if (tl < nt) {
-            mb = tptr[tl];
-            me = tptr[tl + 1];
-            mhx = hidx[tl];
-            mro = mhx >= 0 ? hptr[tl] : rptr[tl];
-            if (tl < n) {
-                const int64_t tile = tl / kNodeTile;
-                mcap = vcap[tile];
-                mpf = vfirst[tile * kVfStride + (tl - tile * kNodeTile)];
-                mlb = ltile[tile];
-            }
-        }
-        const int cntT = (int)min((int64_t)32, nt - base);
-        for (int q = 0; q < cntT; ++q) {
-            const int64_t t = base + q;
-            const int64_t b = __shfl_sync(0xffffffffu, mb, q), e = __shfl_sync(0xffffffffu, me, q);
-            const int32_t hx = __shfl_sync(0xffffffffu, mhx, q);
-            const int64_t cap = __shfl_sync(0xffffffffu, mcap, q);
-            const int pf = __shfl_sync(0xffffffffu, mpf, q);
-            const int64_t lbase = __shfl_sync(0xffffffffu, mlb, q);
-            const bool owned = t < n;
-            const int64_t tile = owned ? t / kNodeTile : -1;
-            int64_t lo = 0;
-            int64_t ro = __shfl_sync(0xffffffffu, mro, q);
-            for (int64_t k0 = b; k0 < e; k0 += 32) {
-                const int64_t k = k0 + lane;
-                const bool ok = k < e;
-                const int32_t s = ok ? tsrc[k] : 0;
-                const bool loc = ok && (s / kNodeTile == tile);
-                const unsigned bl = __ballot_sync(0xffffffffu, loc);
-                const unsigned br = __ballot_sync(0xffffffffu, ok && !loc);
-                if (loc) {
-                    // balanced sliced-ELL: local in-edge s of t is slot s % cap of its piece s / cap
-                    const int64_t qq = lo + __popc(bl & lt);
-                    const int r = plist[tile * kVRows + pf + (int)(qq / cap)];
-                    const int64_t o = lbase + vofs[tile * kVofsStride + r / 32] + 32 * (qq % cap) + (r % 32);
-                    lsrc[o] = (uint16_t)(s - tile * kNodeTile);
-                    if (kW) lw[o] = tw[k];
-                } else if (ok) {
-                    const int64_t o = ro + __popc(br & lt);
-                    RemRec<W> r{};
-                    r.src = s;
-                    if constexpr (kW) r.w = tw[k];
-                    else r.w = 1.0f;
-                    if (hx >= 0) {
-                        htmp[o] = r;
-                        hkey[o] = (uint32_t)(s / stripe_nodes);
-                        hval[o] = (uint32_t)o;
-                        hof[o] = (uint32_t)hx;
-                    } else {
-                        rrec[o] = r;
-                    }
-                }
-                lo += __popc(bl);
-                ro += __popc(br);
-            }
-        }
-    }
-}
-
 // ---- edge-parallel plan build (hub targets with millions of in-edges must not
 // serialise on one warp): target of every CSC position, local flags, their
 // exclusive scan L, so that a local in-edge's rank within its target is
@@ -374,9 +294,10 @@ __global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *_
                              const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
                              const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
                              const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
-                             const int32_t *__restrict__ hidx, int64_t stripe_nodes, uint16_t *__restrict__ lsrc,
-                             StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec, RemRec<W> *__restrict__ htmp,
-                             uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval, uint32_t *__restrict__ hof) {
+                             const int32_t *__restrict__ hidx, int64_t stripe_nodes, int64_t nstripe, int waves,
+                             uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec,
+                             RemRec<W> *__restrict__ htmp, uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval,
+                             uint32_t *__restrict__ hof) {
     constexpr bool kW = !std::is_same<W, NoW>::value;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = tkey[k];
@@ -402,7 +323,8 @@ __global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *_
             else r.w = 1.0f;
             if (hx >= 0) {
                 htmp[o] = r;
-                hkey[o] = (uint32_t)(s / stripe_nodes);
+                // heavy edges grouped by (wave of the target, stripe of the source)
+                hkey[o] = (uint32_t)((owned ? tile_wave(t, waves) : 0) * nstripe + s / stripe_nodes);
                 hval[o] = (uint32_t)o;
                 hof[o] = (uint32_t)hx;
             } else {
@@ -474,7 +396,7 @@ __global__ void k_fill_u64(unsigned long long *__restrict__ p, int64_t cnt, unsi
 template <typename W>
 __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const StoreW<W> *__restrict__ w, const double *__restrict__ inv, int64_t n,
-                               float *__restrict__ wr) {
+                               int waves, float *__restrict__ wr) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     constexpr bool kW = !std::is_same<W, NoW>::value;
@@ -482,7 +404,10 @@ __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_
         const int64_t tile = i / kNodeTile;
         double s = 0.0;
         for (int64_t e = row_ptr[i] + lane_id(); e < row_ptr[i + 1]; e += 32)
-            if (col[e] >= n || col[e] / kNodeTile != tile) s += kW ? (double)w[e] : 1.0;   // ghosts leave too
+            // leaves the tile and is still pending after the sweep (a later wave takes
+            // its pushes in during the sweep, R15); ghost targets always pending
+            if (col[e] >= n || (col[e] / kNodeTile != tile && tile_wave(col[e], waves) <= tile_wave(i, waves)))
+                s += kW ? (double)w[e] : 1.0;
         s = warp_sum(s);
         if (lane_id() == 0) wr[i] = (float)(s * inv[i]);
     }
@@ -497,7 +422,7 @@ void free_tiles(TilePlan &t) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
                     (void *)t.vofs, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
-                    (void *)t.hsum})
+                    (void *)t.hsum, (void *)t.tpart})
         cudaFree(p);
     t = TilePlan();
 }
@@ -540,7 +465,12 @@ static void build_tiles_t(di_graph *h) {
     phase_mark(st, "tiles: start");
     tp.ntile = (n + kNodeTile - 1) / kNodeTile;
     tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
-    const int64_t S = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
+    const int64_t nS = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
+    tp.nstripe = nS;
+    tp.waves = g.shard ? 1 : kTileWaves;
+    if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = g.shard ? 1 : std::max(1, atoi(e));
+    tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(tp.waves, tp.ntile));   // empty waves dropped
+    const int64_t S = tp.waves * nS;                 // heavy groups (wave, stripe)
     // ---- classes of the in-edges
     int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
     for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
@@ -605,7 +535,7 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaMallocAsync(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t), st));
     k_tile_rel<<<grid_for(h, nt + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, nt, tp.ntile, tp.rrel, tp.hidx,
                                                     tp.deg, tp.rtile);
-    k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.wr);
+    k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.waves, tp.wr);
     count_launch(2);
     phase_mark(st, "tiles: node arrays");
     // ---- edges to their classes
@@ -619,7 +549,8 @@ static void build_tiles_t(di_graph *h) {
     if (m > 0)
         k_split_flat<W><<<grid_for(h, m), 256, 0, st>>>(g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, L, m, n, tp.ltile,
                                                         tp.vofs, tp.vfirst, tp.plist, vcap, rptr, hptr, tp.hidx,
-                                                        tp.stripe_nodes, tp.lsrc, (SW *)tp.lw, (RemRec<W> *)tp.rrec,
+                                                        tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
+                                                        (RemRec<W> *)tp.rrec,
                                                         htmp, k0, v0, hof);
     DI_CUDA(cudaFreeAsync(tkey, st));
     DI_CUDA(cudaFreeAsync(L, st));
@@ -699,6 +630,7 @@ static void build_tiles_t(di_graph *h) {
     }
     phase_mark(st, "tiles: heavy sort + index");
     DI_CUDA(cudaMallocAsync(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double), st));
+    DI_CUDA(cudaMallocAsync(&tp.tpart, (2 * (size_t)tp.waves * 4096 + 64) * sizeof(double), st));
     unsigned long long *mx;
     DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
     DI_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
@@ -746,13 +678,15 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
                                                       const int64_t *__restrict__ run_seg, int64_t q0, int64_t q1,
                                                       const double *__restrict__ A0, const double *__restrict__ A1,
                                                       double *__restrict__ part, double *__restrict__ hsum,
-                                                      const Ctrl *__restrict__ ctrl, int force) {
+                                                      int wave, int waves, const Ctrl *__restrict__ ctrl, int force) {
     __shared__ double vals[kHeavyChunk];
     __shared__ int sbnd[kHeavyChunk + 1];
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
-    if (!ctrl->gather) return;
-    // the previous sweep wrote A[(sweeps - 1) & 1]
-    const double *__restrict__ A = (ctrl->sweeps & 1) ? A0 : A1;
+    const bool gather = ctrl->gather != 0;
+    if (force ? !gather : (!gather && wave == 0)) return;
+    // the previous sweep wrote A[(sweeps - 1) & 1], this sweep's earlier waves A[sweeps & 1]
+    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
+    const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
     const unsigned w = threadIdx.x >> 5, lane = lane_id();
     // fold the previous stripe's runs (lane per run; long runs by the whole warp)
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -798,8 +732,13 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
         if (threadIdx.x == 0) sbnd[ns] = cnt;
 #pragma unroll 8
         for (int k = threadIdx.x; k < cnt; k += kThreads) {
+            // a source of an earlier wave pushed this sweep; the others in the previous
+            // one (still pending); in the flush only the pending pushes are left (R15)
             const RemRec<W> r = hrec[e0 + k];
-            vals[k] = A[r.src] * rec_w(r);
+            const bool early = tile_wave(r.src, waves) < wave;
+            double v = 0.0;
+            if (force ? !early : (early || gather)) v = (early && !force ? Afresh : Aprev)[r.src] * rec_w(r);
+            vals[k] = v;
         }
         __syncthreads();
         // short segments: one thread each; long ones (>= 64 edges): the whole warp
@@ -852,6 +791,8 @@ struct TileArgs {
     unsigned long long *dbg; // optional per-CTA phase cycle counters [grid][5] (DIT_TILE_TIMING)
     int64_t n, ntile, m;
     int rounds;
+    int wave, waves;         // this launch runs tiles wave, wave + waves, ... (R15)
+    int64_t ntw;             // tiles of the wave
     int64_t edge_cap;        // bytes of shared memory for the staged local edges
 };
 
@@ -987,15 +928,21 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
     if (ctrl->done || ctrl->use_pull != kUseTiled) return;
     const double d = ctrl->d;
     const bool gather = ctrl->gather != 0;
+    // light records are needed when a previous sweep left pushes, or earlier waves of this one
+    const bool recs_on = gather || a.wave > 0;
     const unsigned long long sw = ctrl->sweeps;
     double *__restrict__ Anext = (sw & 1) ? a.A1 : a.A0;
     const double *__restrict__ Aprev = (sw & 1) ? a.A0 : a.A1;
     const int i = threadIdx.x;
     const int lane = i & 31, wp = i >> 5;
     const int64_t G = gridDim.x;
-    auto scal = [&](int64_t t) {
+    auto tid_of = [&](int64_t jt) { return (int64_t)a.wave + (int64_t)a.waves * jt; };   // the wave's jt-th tile
+    auto scal = [&](int64_t jt) {
         TileScalars ts{0, 0, 0, 0};
-        if (t < a.ntile) ts = TileScalars{a.ltile[t], a.ltile[t + 1], a.rtile[t], a.rtile[t + 1]};
+        if (jt < a.ntw) {
+            const int64_t t = tid_of(jt);
+            ts = TileScalars{a.ltile[t], a.ltile[t + 1], a.rtile[t], a.rtile[t + 1]};
+        }
         return ts;
     };
     TileScalars cur = scal(blockIdx.x), nxt = scal(blockIdx.x + G);
@@ -1005,25 +952,26 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         mbar_init(smem_u32(&bars[0]), 1);
         mbar_init(smem_u32(&bars[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (blockIdx.x < a.ntile)
-            issue_tile<W>(a, a.F, blockIdx.x, cur, gather, smem + kSharedHead, smem_u32(&bars[0]));
+        if (blockIdx.x < a.ntw)
+            issue_tile<W>(a, a.F, tid_of(blockIdx.x), cur, recs_on, smem + kSharedHead, smem_u32(&bars[0]));
     }
     __syncthreads();
     double resid = 0.0, leak = 0.0;
     unsigned long long nodes = 0, edges = 0;
     int k = 0;
-    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += G, ++k) {
+    for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
+        const int64_t tile = tid_of(jt);
         const int b = k & 1;
         unsigned char *buf = smem + kSharedHead + b * bufsz;
         // next tile's bundle into the other buffer (freed by the previous iteration)
-        const TileScalars after = scal(tile + 2 * G);
-        if (i == 0 && tile + G < a.ntile)
-            issue_tile<W>(a, a.F, tile + G, nxt, gather, smem + kSharedHead + (b ^ 1) * bufsz,
+        const TileScalars after = scal(jt + 2 * G);
+        if (i == 0 && jt + G < a.ntw)
+            issue_tile<W>(a, a.F, tid_of(jt + G), nxt, recs_on, smem + kSharedHead + (b ^ 1) * bufsz,
                           smem_u32(&bars[b ^ 1]));
         const int64_t a0 = tile * kNodeTile;
         const int nn = (int)min(kNodeTile, a.n - a0);
         const int64_t l0 = cur.l0, l1 = cur.l1;
-        const int64_t r0 = gather ? cur.r0 : 0, r1 = gather ? cur.r1 : 0;
+        const int64_t r0 = recs_on ? cur.r0 : 0, r1 = recs_on ? cur.r1 : 0;
         const int64_t rb0 = (r0 * kRS) & ~int64_t(15);
         const int64_t sb0 = (l0 * 2) & ~int64_t(15), sb1 = (l1 * 2 + 15) & ~int64_t(15);
         const int64_t wb0 = (l0 * kWB) & ~int64_t(15), wb1 = (l1 * kWB + 15) & ~int64_t(15);
@@ -1045,9 +993,10 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         long long c1 = a.dbg ? clock64() : 0;
         const bool valid = i < nn;
         const int64_t j = a0 + i;
-        // 1. remote pushes of the previous sweep: heavy sums, light records -> products in place
+        // 1. remote pushes still pending: from the previous sweep, and from this sweep's
+        //    earlier waves (R15): heavy sums, light records -> products in place
         double hs = 0.0;
-        if (valid && gather) {
+        if (valid && recs_on) {
             const int32_t hx = Xs[i];
             if (hx >= 0) hs = a.hsum[hx];
         }
@@ -1056,7 +1005,9 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
 #pragma unroll 4
         for (int q = i; q < R; q += kTileBlock) {
             const RemRec<W> r = recs[q];
-            *reinterpret_cast<double *>(&recs[q]) = Aprev[r.src] * rec_w(r);
+            const bool early = tile_wave(r.src, a.waves) < a.wave;
+            const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
+            *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
         }
         __syncthreads();
         double f = 0.0, ivi = 0.0;
@@ -1065,7 +1016,7 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
             ivi = Is[i];
             dgi = Ds[i];
             double s = 0.0;
-            if (gather) {
+            if (recs_on) {
                 const int rb = (int)Rs[i], re = i + 1 < nn ? (int)Rs[i + 1] : R;
                 for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
             }
@@ -1161,8 +1112,8 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
             x += s_c[q][0];
             y += s_c[q][1];
         }
-        a.part[blockIdx.x] = rr;
-        a.part[gridDim.x + blockIdx.x] = ll;
+        a.part[a.wave * 4096 + blockIdx.x] = rr;
+        a.part[(a.waves + a.wave) * 4096 + blockIdx.x] = ll;
         if (x) {
             atomicAdd(&ctrl->diffused_nodes, x);
             atomicAdd(&ctrl->sel_edges, y);
@@ -1174,11 +1125,22 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
     __syncthreads();
     if (!s_last || threadIdx.x != 0) return;
     __threadfence();
-    const volatile double *vp = a.part;
+    // last block of the wave: the wave's partials in a fixed order
+    volatile double *vp = a.part;
     double r = 0.0, lk = 0.0;
     for (unsigned bb = 0; bb < gridDim.x; ++bb) {
-        r += vp[bb];
-        lk += vp[gridDim.x + bb];
+        r += vp[a.wave * 4096 + bb];
+        lk += vp[(a.waves + a.wave) * 4096 + bb];
+    }
+    vp[2 * a.waves * 4096 + 2 * a.wave] = r;
+    vp[2 * a.waves * 4096 + 2 * a.wave + 1] = lk;
+    ctrl->red_blocks = 0;
+    if (a.wave + 1 < a.waves) return;                // the sweep ends with its last wave
+    r = 0.0;
+    lk = 0.0;
+    for (int c = 0; c < a.waves; ++c) {
+        r += vp[2 * a.waves * 4096 + 2 * c];
+        lk += vp[2 * a.waves * 4096 + 2 * c + 1];
     }
     end_sweep(ctrl, lk);
     ctrl->gather = 1;                                // this sweep's remote pushes are pending in A
@@ -1201,16 +1163,19 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
 template <typename W>
 __global__ void __launch_bounds__(kThreads) k_tile_flush(TileArgs<W> a, const Ctrl *__restrict__ ctrl) {
     if (!ctrl->gather) return;
-    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? a.A0 : a.A1;
+    const double *__restrict__ Alast = (ctrl->sweeps & 1) ? a.A0 : a.A1;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = j / kNodeTile;
+        const int c = tile_wave(j, a.waves);
         const int64_t base = a.rtile[t];
         const int64_t b = base + a.rrel[j];
         const int64_t e = (j + 1 < a.n && (j + 1) % kNodeTile != 0) ? base + a.rrel[j + 1] : a.rtile[t + 1];
         double s = 0.0;
         for (int64_t k = b; k < e; ++k) {
+            // only the pushes not yet taken in: sources of this or a later wave (R15)
             const RemRec<W> r = a.rrec[k];
-            s += Aprev[r.src] * rec_w(r);
+            const double v = tile_wave(r.src, a.waves) >= c ? Alast[r.src] : 0.0;
+            s += v * rec_w(r);
         }
         const int32_t hx = a.hidx[j];
         const double hs = hx >= 0 ? a.hsum[hx] : 0.0;
@@ -1242,13 +1207,16 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     a.H = s.H;
     a.A0 = s.A;
     a.A1 = s.A2;
-    a.part = s.part;
+    a.part = tp.tpart;
     a.n = g.n;
     a.ntile = tp.ntile;
     a.m = g.m;
     a.rounds = rounds;
     a.edge_cap = 0;
     a.dbg = nullptr;
+    a.wave = 0;
+    a.waves = tp.waves;
+    a.ntw = tp.ntile;
     return a;
 }
 
@@ -1263,28 +1231,28 @@ static int heavy_ctas_per_sm() {
     return v;
 }
 
-// the heavy targets' remote inflow hsum: one launch per stripe + the last fold
+// the heavy targets' remote inflow hsum of one wave: one launch per stripe + the last fold
 template <typename W>
-static void launch_heavy_t(di_graph *h, int force) {
+static void launch_heavy_t(di_graph *h, int wave, int force) {
     TilePlan &tp = h->g.tl;
     State &s = h->s;
     if (tp.nh == 0) return;
-    const int64_t S = (int64_t)tp.s_chunk.size() - 1;
+    const int64_t S = tp.nstripe, g0 = (int64_t)wave * S;
     for (int64_t st = 0; st <= S; ++st) {
-        const int64_t c0 = st < S ? tp.s_chunk[st] : 0, c1 = st < S ? tp.s_chunk[st + 1] : 0;
-        const int64_t q0 = st > 0 ? tp.s_run[st - 1] : 0, q1 = st > 0 ? tp.s_run[st] : 0;
+        const int64_t c0 = st < S ? tp.s_chunk[g0 + st] : 0, c1 = st < S ? tp.s_chunk[g0 + st + 1] : 0;
+        const int64_t q0 = st > 0 ? tp.s_run[g0 + st - 1] : 0, q1 = st > 0 ? tp.s_run[g0 + st] : 0;
         const int64_t work = std::max<int64_t>(c1 - c0, (q1 - q0 + 255) / 256);
         if (work == 0) continue;
         const int grid = (int)std::min<int64_t>(work, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
         k_heavy_s<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
                                                        tp.cfirst, c0, c1, tp.run_h, tp.run_seg, q0, q1, s.A, s.A2,
-                                                       tp.part, tp.hsum, s.ctrl, force);
+                                                       tp.part, tp.hsum, wave, tp.waves, s.ctrl, force);
         count_launch();
     }
 }
 
 template <typename W>
-static void launch_tile_kernel_t(di_graph *h, int rounds) {
+static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
     DevGraph &g = h->g;
     State &s = h->s;
     TilePlan &tp = g.tl;
@@ -1322,7 +1290,10 @@ static void launch_tile_kernel_t(di_graph *h, int rounds) {
         }
         a.dbg = g_tile_dbg;
     }
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * kTileBlocksPerSM));
+    a.wave = wave;
+    a.ntw = tp.ntile > wave ? (tp.ntile - wave + tp.waves - 1) / tp.waves : 0;
+    if (a.ntw == 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntw, (int64_t)h->num_sms * kTileBlocksPerSM));
     k_tile<W><<<grid, kTileBlock, smem, h->stream>>>(a, s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());
@@ -1331,11 +1302,12 @@ static void launch_tile_kernel_t(di_graph *h, int rounds) {
 template <typename W>
 static void launch_tile_t(di_graph *h, int rounds) {
     const int64_t k = h->s.launched;
-    launch_heavy_t<W>(h, 0);
-    mark_event(h, k, 1);
-    mark_event(h, k, 2);
-    launch_tile_kernel_t<W>(h, rounds);
-    mark_event(h, k, 3);
+    for (int c = 0; c < h->g.tl.waves; ++c) {          // events: [2c] heavy(c) [2c+1] tile(c) [2c+2]
+        launch_heavy_t<W>(h, c, 0);
+        mark_event(h, k, 2 * c + 1);
+        launch_tile_kernel_t<W>(h, rounds, c);
+        mark_event(h, k, 2 * c + 2);
+    }
 }
 
 void launch_tile_sweep(di_graph *h, int rounds) {
@@ -1351,18 +1323,18 @@ void launch_tile_sweep(di_graph *h, int rounds) {
 void launch_tile_heavy(di_graph *h, int force) {
     if (h->g.tl.ntile == 0) return;
     switch (h->g.w_kind) {
-    case DI_W_F32: launch_heavy_t<float>(h, force); break;
-    case DI_W_F64: launch_heavy_t<double>(h, force); break;
-    default: launch_heavy_t<NoW>(h, force);
+    case DI_W_F32: launch_heavy_t<float>(h, 0, force); break;
+    case DI_W_F64: launch_heavy_t<double>(h, 0, force); break;
+    default: launch_heavy_t<NoW>(h, 0, force);
     }
 }
 
 void launch_tile_kernel(di_graph *h, int rounds) {
     if (h->g.tl.ntile == 0) return;
     switch (h->g.w_kind) {
-    case DI_W_F32: launch_tile_kernel_t<float>(h, rounds); break;
-    case DI_W_F64: launch_tile_kernel_t<double>(h, rounds); break;
-    default: launch_tile_kernel_t<NoW>(h, rounds);
+    case DI_W_F32: launch_tile_kernel_t<float>(h, rounds, 0); break;
+    case DI_W_F64: launch_tile_kernel_t<double>(h, rounds, 0); break;
+    default: launch_tile_kernel_t<NoW>(h, rounds, 0);
     }
 }
 
@@ -1386,7 +1358,7 @@ void launch_take_ghost_sums(di_graph *h, double *out, int force) {
 
 template <typename W>
 static void launch_flush_t(di_graph *h) {
-    launch_heavy_t<W>(h, 1);
+    for (int c = 0; c < h->g.tl.waves; ++c) launch_heavy_t<W>(h, c, 1);
     k_tile_flush<W><<<grid_for(h, h->g.n), kThreads, 0, h->stream>>>(tile_args<W>(h, 0), h->s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());

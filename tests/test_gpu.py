@@ -309,11 +309,11 @@ def _sampled_identity(g, H, F, d, rng, k=2000):
 
 @pytest.mark.parametrize("variant", ["auto", "tiled"])
 def test_config2_full_size_sampled(eng, variant):
-    # the bench's workload and launch configuration (tiled, 3 local rounds)
+    # the bench's workload and launch configuration (tiled, 4 local rounds, 2 waves)
     spec = synth.CONFIGS[2]
     g = _config2_graph()
     G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
-    H, res = G.solve(d=D, tol=spec.tol, variant=variant, local_rounds=3)
+    H, res = G.solve(d=D, tol=spec.tol, variant=variant, local_rounds=4)
     assert res["converged"] and res["residual_l1"] <= spec.tol
     F, H2, d, leak = G.state()
     H2 = H2.cpu().numpy()

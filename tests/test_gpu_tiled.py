@@ -30,7 +30,8 @@ def test_tiled_sweeps_elementwise(eng, weighted, rounds):
     for k in (1, 2, 5):
         _, res = G.solve(d=D, tol=0.0, variant="tiled", local_rounds=rounds, max_sweeps=k)
         F, H, _, leak = G.state()
-        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=eng._lib.DI_TILE_NODES, rounds=rounds, tol=0, max_sweeps=k)
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=eng._lib.DI_TILE_NODES, rounds=rounds, tol=0, max_sweeps=k,
+                                 waves=eng._lib.DI_TILE_WAVES)
         assert res["sweeps"] == k
         assert np.allclose(H.cpu().numpy(), r.H, rtol=1e-13, atol=1e-20)
         assert np.allclose(F.cpu().numpy(), r.F, rtol=1e-11, atol=1e-20)
@@ -127,7 +128,7 @@ def test_tiled_stress_paths_elementwise(eng, wdtype):
         _, res = G.solve(d=D, tol=0.0, variant="tiled", local_rounds=3, max_sweeps=k)
         F, H, _, leak = G.state()
         r = di.tiled_sweep_run(n, cp, ri, pv, D, st.F, st.H, tile=eng._lib.DI_TILE_NODES, rounds=3, tol=0,
-                               max_sweeps=k)
+                               max_sweeps=k, waves=eng._lib.DI_TILE_WAVES)
         assert res["sweeps"] == k
         assert np.allclose(H.cpu().numpy(), r.H, rtol=1e-12, atol=1e-20)
         assert np.allclose(F.cpu().numpy(), r.F, rtol=1e-10, atol=1e-18)
