@@ -63,8 +63,9 @@ CONFIGS = {
                  p_dangling=0.12, weighted=True, seed=2, tol=1e-9),
     3: GraphSpec("web-400M-8B-sharded", 400_000_000, DEG_POWERLAW, 2.1, deg_b=3.75, deg_cap=5000,
                  p_dangling=0.12, weighted=True, seed=3, tol=1e-9),
-    4: GraphSpec("web-1M-10M-dynamic", 1_000_000, DEG_GEOMETRIC, 10, deg_cap=1000, p_dangling=0.15,
-                 seed=1, tol=1e-9),
+    # "dynamic update on the config-2 graph": configs[2]'s graph, 1% of its edges rewired
+    4: GraphSpec("web-50M-1B-weighted-dynamic", 50_000_000, DEG_POWERLAW, 2.1, deg_b=3.75, deg_cap=5000,
+                 p_dangling=0.12, weighted=True, seed=2, tol=1e-9),
 }
 
 _lib = None

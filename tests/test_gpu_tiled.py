@@ -74,7 +74,7 @@ def test_tiled_dense_hubs_and_completion(eng):
 
 
 def test_tiled_after_update(eng):
-    spec = synth.CONFIGS[4].scaled(20_000, seed=2)
+    spec = synth.CONFIGS[4].scaled(20_000, seed=2, weighted=False)
     g = synth.generate(spec)
     delta = synth.rewire(spec, g, fraction=0.01, seed=5)
     G = eng.DIGraph(g.n, g.row_ptr, g.col)
