@@ -87,7 +87,10 @@ constexpr int64_t kLightCap = 2048;     // light remote records per tile (shared
 #define DIT_HEAVY_TH 16
 #endif
 constexpr int64_t kHeavyTh = DIT_HEAVY_TH;       // remote in-degree above which a target is heavy
-constexpr int64_t kHeavyChunk = 2048;   // heavy edges per k_heavy chunk
+#ifndef DIT_HEAVY_CHUNK
+#define DIT_HEAVY_CHUNK 2048
+#endif
+constexpr int64_t kHeavyChunk = DIT_HEAVY_CHUNK;   // heavy edges per k_heavy chunk
 
 struct TilePlan {
     bool built = false;

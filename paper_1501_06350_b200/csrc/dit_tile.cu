@@ -78,7 +78,10 @@ struct RemRec<double> {
 template <typename W>
 __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w; }
 
-constexpr int64_t kStripeBytes = 48ll << 20;   // outflow slice per heavy stripe (L2-resident)
+#ifndef DIT_STRIPE_MB
+#define DIT_STRIPE_MB 48
+#endif
+constexpr int64_t kStripeBytes = (int64_t)DIT_STRIPE_MB << 20;   // outflow slice per heavy stripe (L2-resident)
 #ifndef DIT_TILE_WAVES
 #define DIT_TILE_WAVES 2
 #endif
@@ -806,12 +809,7 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     int s = 0;
     for (; s + 4 <= K; s += 4) {
         const int k = base + 32 * s;
-#ifdef DIT_EXPERIMENT_NOCONFLICT
-        const int s0 = (es[k] & 0) + (threadIdx.x & 31), s1 = (es[k + 32] & 0) + (threadIdx.x & 31),
-                  s2 = (es[k + 64] & 0) + (threadIdx.x & 31), s3 = (es[k + 96] & 0) + (threadIdx.x & 31);
-#else
         const int s0 = es[k], s1 = es[k + 32], s2 = es[k + 64], s3 = es[k + 96];
-#endif
         double v0 = gq[s0], v1 = gq[s1], v2 = gq[s2], v3 = gq[s3];
         if constexpr (kW) {
             v0 *= (double)ew[k];
@@ -845,7 +843,13 @@ constexpr int tile_fixed_smem() {
 // One tile's TMA bundle (a buffer of the double-buffered pipeline): the
 // per-node state, the tile's layout, its light records and (when they fit)
 // its local edges.
-constexpr int kNodeBytes = (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
+// DIT_LEAN_BUNDLE: the per-node rows stay out of the bundle (plain loads after an
+// L2 bulk prefetch), so that shared memory is small and L1 keeps the local edges
+#ifndef DIT_LEAN_BUNDLE
+#define DIT_LEAN_BUNDLE 0
+#endif
+constexpr bool kLean = DIT_LEAN_BUNDLE != 0;
+constexpr int kNodeBytes = kLean ? 0 : (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
 template <typename W>
 constexpr int tile_buf_fixed() {
     return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
@@ -874,21 +878,31 @@ __device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *F
     const int64_t wb0 = (ts.l0 * kWB) & ~int64_t(15), wb1 = (ts.l1 * kWB + 15) & ~int64_t(15);
     const int64_t ebytes = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0);
     const bool staged = ebytes <= a.edge_cap;
-    uint32_t bytes = 3 * n8 + 4 * n4 + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
+    uint32_t bytes = (kLean ? 0u : 3 * n8 + 4 * n4) + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
     if (staged) bytes += (uint32_t)ebytes;
     // order this CTA's earlier generic-proxy accesses of the buffer before the async writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(bar, bytes);
     unsigned char *p = buf;
     const uint32_t sb = smem_u32(buf);
-    tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
-    tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
-    tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
-    const uint32_t q = 3 * kNodeTile * 8;
-    tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
-    tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
-    tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
-    tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
+    if (kLean) {
+        tma_prefetch_l2(Fsrc + a0, n8);
+        tma_prefetch_l2(a.H + a0, n8);
+        tma_prefetch_l2(a.inv + a0, n8);
+        tma_prefetch_l2(a.deg + a0, n4);
+        tma_prefetch_l2(a.wr + a0, n4);
+        tma_prefetch_l2(a.rrel + a0, n4);
+        tma_prefetch_l2(a.hidx + a0, n4);
+    } else {
+        tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
+        tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
+        tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
+        const uint32_t q = 3 * kNodeTile * 8;
+        tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
+        tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
+        tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
+        tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
+    }
     const uint32_t m = kNodeBytes;
     tma_load(sb + m, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
     tma_load(sb + m + kVofsStride * 4, a.vfirst + tile * kVfStride, kVfStride * 2, bar);
@@ -997,7 +1011,7 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         //    earlier waves (R15): heavy sums, light records -> products in place
         double hs = 0.0;
         if (valid && recs_on) {
-            const int32_t hx = Xs[i];
+            const int32_t hx = kLean ? a.hidx[j] : Xs[i];
             if (hx >= 0) hs = a.hsum[hx];
         }
         const int R = (int)(r1 - r0);
@@ -1013,14 +1027,15 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         double f = 0.0, ivi = 0.0;
         int dgi = 0;
         if (valid) {
-            ivi = Is[i];
-            dgi = Ds[i];
+            ivi = kLean ? a.inv[j] : Is[i];
+            dgi = kLean ? a.deg[j] : Ds[i];
             double s = 0.0;
             if (recs_on) {
-                const int rb = (int)Rs[i], re = i + 1 < nn ? (int)Rs[i + 1] : R;
+                const int rb = kLean ? (int)a.rrel[j] : (int)Rs[i];
+                const int re = i + 1 < nn ? (kLean ? (int)a.rrel[j + 1] : (int)Rs[i + 1]) : R;
                 for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
             }
-            f = Fs[i] + s + hs;
+            f = (kLean ? a.F[j] : Fs[i]) + s + hs;
         }
         long long c2 = a.dbg ? clock64() : 0;
         // 2. local diffusion rounds in shared memory
@@ -1072,9 +1087,12 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         if (valid) {
             const double An = d * D * ivi;
             a.F[j] = f;
-            if (D != 0.0) a.H[j] = Hs[i] + D;
+            if (D != 0.0) {
+                if (kLean) red_add(a.H + j, D);       // one writer per node and sweep: H + D exactly
+                else a.H[j] = Hs[i] + D;
+            }
             Anext[j] = An;
-            resid += fabs(f) + fabs(An) * (double)Ws[i];
+            resid += fabs(f) + fabs(An) * (double)(kLean ? a.wr[j] : Ws[i]);
             if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
         }
         cur = nxt;
@@ -1278,6 +1296,13 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
         tp.edge_cap = cap;
         tp.tile_smem = (size_t)(kSharedHead + 2 * (fixed + cap));
         DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
+        if (kLean) {
+            // the smallest shared-memory carveout that holds the CTAs: the rest is L1,
+            // which keeps the local edges between the rounds
+            const int64_t need = kTileBlocksPerSM * ((int64_t)tp.tile_smem + fa.sharedSizeBytes + 1024);
+            const int pct = (int)std::min<int64_t>(100, (need * 100 + per_sm - 1) / per_sm);
+            DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        }
     }
     const int64_t cap = tp.edge_cap;
     const size_t smem = tp.tile_smem;
