@@ -82,7 +82,10 @@ struct PullPlan {
 // gathers itself; "heavy" targets (many remote in-edges, or tiles whose light
 // records would overflow kLightCap) are gathered by k_heavy over fixed chunks
 // of the heavy edge array (segments = target ∩ chunk), deterministic.
-constexpr int64_t kLightCap = 2048;     // light remote records per tile (shared memory)
+#ifndef DIT_LIGHT_CAP
+#define DIT_LIGHT_CAP 2048
+#endif
+constexpr int64_t kLightCap = DIT_LIGHT_CAP;   // light remote records per tile (shared memory)
 #ifndef DIT_HEAVY_TH
 #define DIT_HEAVY_TH 16
 #endif

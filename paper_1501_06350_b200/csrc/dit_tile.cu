@@ -120,6 +120,14 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS), tracked by commit/wait groups
+__device__ __forceinline__ void cp_async8(void *dst_smem, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // bulk prefetch of a global range into L2 (the TMA engine; no completion tracking)
 __device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -849,10 +857,13 @@ constexpr int tile_fixed_smem() {
 #define DIT_LEAN_BUNDLE 0
 #endif
 constexpr bool kLean = DIT_LEAN_BUNDLE != 0;
+// lean bundles come in three: the light gathers of tile k+1 (cp.async, 8 B each,
+// into the bundle's value block) fly while tile k diffuses
+constexpr int kNB = kLean ? 3 : 2;
 constexpr int kNodeBytes = kLean ? 0 : (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
 template <typename W>
 constexpr int tile_buf_fixed() {
-    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
+    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32 + (kLean ? (int)kLightCap * 8 : 0);
 }
 constexpr int kSharedHead = ((int)kNodeTile + 2) * 8 + kVRows * 8;         // gq, psum
 static_assert(kNodeBytes % 16 == 0 && kSharedHead % 16 == 0, "16-byte aligned shared buffers");
@@ -935,7 +946,8 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
     double *gq = reinterpret_cast<double *>(smem);                       // [kNodeTile + 2]: outflow, zero pad slot
     double *psum = gq + kNodeTile + 2;                                   // [kVRows]: piece sums by rank
     const int bufsz = (int)(tile_buf_fixed<W>() + a.edge_cap);
-    __shared__ __align__(8) unsigned long long bars[2];
+    __shared__ __align__(8) unsigned long long bars[kNB];
+    __shared__ TileScalars sc[kNB];                  // scalars of the tile in each buffer
     __shared__ double s_r[kTileBlockWarps], s_l[kTileBlockWarps];
     __shared__ unsigned long long s_c[kTileBlockWarps][2];
     __shared__ bool s_last;
@@ -959,34 +971,62 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         }
         return ts;
     };
-    TileScalars cur = scal(blockIdx.x), nxt = scal(blockIdx.x + G);
+    auto bufp = [&](int x) { return smem + kSharedHead + x * bufsz; };
+    auto recs_of = [&](int x, const TileScalars &ts) {
+        const int64_t r0 = recs_on ? ts.r0 : 0;
+        return reinterpret_cast<RemRec<W> *>(bufp(x) + kNodeBytes + kMetaBytes + (r0 * kRS - ((r0 * kRS) & ~int64_t(15))));
+    };
+    auto vals_of = [&](int x) {
+        return reinterpret_cast<double *>(bufp(x) + kNodeBytes + kMetaBytes + (int)kLightCap * kRS + 32);
+    };
+    // lean: the light gathers of the tile in buffer x, 8-byte cp.async into its value block
+    auto issue_gathers = [&](int x) {
+        const TileScalars ts = sc[x];
+        const int Rn = recs_on ? (int)(ts.r1 - ts.r0) : 0;
+        const RemRec<W> *rr = recs_of(x, ts);
+        double *vv = vals_of(x);
+        for (int q = i; q < Rn; q += kTileBlock) {
+            const int32_t src = rr[q].src;
+            if (tile_wave(src, a.waves) < a.wave) cp_async8(vv + q, Anext + src);
+            else if (gather) cp_async8(vv + q, Aprev + src);
+            else vv[q] = 0.0;
+        }
+        cp_async_commit();
+    };
     if (i == 0) {
         gq[kNodeTile] = 0.0;                         // padding slots read this
         gq[kNodeTile + 1] = 0.0;
-        mbar_init(smem_u32(&bars[0]), 1);
-        mbar_init(smem_u32(&bars[1]), 1);
+        for (int x = 0; x < kNB; ++x) mbar_init(smem_u32(&bars[x]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (blockIdx.x < a.ntw)
-            issue_tile<W>(a, a.F, tid_of(blockIdx.x), cur, recs_on, smem + kSharedHead, smem_u32(&bars[0]));
+        for (int x = 0; x + 1 < kNB; ++x) {
+            sc[x] = scal(blockIdx.x + x * G);
+            if (blockIdx.x + x * G < a.ntw)
+                issue_tile<W>(a, a.F, tid_of(blockIdx.x + x * G), sc[x], recs_on, bufp(x), smem_u32(&bars[x]));
+        }
     }
     __syncthreads();
+    if (kLean && blockIdx.x < a.ntw) {
+        mbar_wait(smem_u32(&bars[0]), 0u);
+        issue_gathers(0);
+    }
     double resid = 0.0, leak = 0.0;
     unsigned long long nodes = 0, edges = 0;
     int k = 0;
     for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
         const int64_t tile = tid_of(jt);
-        const int b = k & 1;
-        unsigned char *buf = smem + kSharedHead + b * bufsz;
-        // next tile's bundle into the other buffer (freed by the previous iteration)
-        const TileScalars after = scal(jt + 2 * G);
-        if (i == 0 && jt + G < a.ntw)
-            issue_tile<W>(a, a.F, tid_of(jt + G), nxt, recs_on, smem + kSharedHead + (b ^ 1) * bufsz,
-                          smem_u32(&bars[b ^ 1]));
+        const int b = k % kNB;
+        unsigned char *buf = bufp(b);
+        // the bundle kNB-1 tiles ahead into the buffer the previous iteration freed
+        if (i == 0 && jt + (kNB - 1) * G < a.ntw) {
+            const int x = (k + kNB - 1) % kNB;
+            sc[x] = scal(jt + (kNB - 1) * G);
+            issue_tile<W>(a, a.F, tid_of(jt + (kNB - 1) * G), sc[x], recs_on, bufp(x), smem_u32(&bars[x]));
+        }
+        const TileScalars cur = sc[b];
         const int64_t a0 = tile * kNodeTile;
         const int nn = (int)min(kNodeTile, a.n - a0);
         const int64_t l0 = cur.l0, l1 = cur.l1;
         const int64_t r0 = recs_on ? cur.r0 : 0, r1 = recs_on ? cur.r1 : 0;
-        const int64_t rb0 = (r0 * kRS) & ~int64_t(15);
         const int64_t sb0 = (l0 * 2) & ~int64_t(15), sb1 = (l1 * 2 + 15) & ~int64_t(15);
         const int64_t wb0 = (l0 * kWB) & ~int64_t(15), wb1 = (l1 * kWB + 15) & ~int64_t(15);
         const bool staged = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0) <= a.edge_cap;
@@ -1000,29 +1040,41 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         const uint32_t *vofs_s = reinterpret_cast<const uint32_t *>(buf + kNodeBytes);
         const uint16_t *vf_s = reinterpret_cast<const uint16_t *>(vofs_s + kVofsStride);
         const uint16_t *pl_s = vf_s + kVfStride;
-        unsigned char *rbuf = buf + kNodeBytes + kMetaBytes;
         unsigned char *ebuf = buf + tile_buf_fixed<W>();
         long long c0 = a.dbg ? clock64() : 0;
-        mbar_wait(smem_u32(&bars[b]), (uint32_t)((k >> 1) & 1));
-        long long c1 = a.dbg ? clock64() : 0;
+        mbar_wait(smem_u32(&bars[b]), (uint32_t)((k / kNB) & 1));
         const bool valid = i < nn;
         const int64_t j = a0 + i;
+        const int R = (int)(r1 - r0);
+        RemRec<W> *recs = recs_of(b, cur);
+        const double *vals = vals_of(b);
         // 1. remote pushes still pending: from the previous sweep, and from this sweep's
-        //    earlier waves (R15): heavy sums, light records -> products in place
+        //    earlier waves (R15): heavy sums and the light records' gathered outflow
         double hs = 0.0;
         if (valid && recs_on) {
             const int32_t hx = kLean ? a.hidx[j] : Xs[i];
             if (hx >= 0) hs = a.hsum[hx];
         }
-        const int R = (int)(r1 - r0);
-        RemRec<W> *recs = reinterpret_cast<RemRec<W> *>(rbuf + (r0 * kRS - rb0));
+        if (kLean) {
+            // the next tile's gathers go out now (they land while this tile diffuses)
+            if (jt + G < a.ntw) {
+                const int x = (k + 1) % kNB;
+                mbar_wait(smem_u32(&bars[x]), (uint32_t)(((k + 1) / kNB) & 1));
+                issue_gathers(x);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+        } else {
 #pragma unroll 4
-        for (int q = i; q < R; q += kTileBlock) {
-            const RemRec<W> r = recs[q];
-            const bool early = tile_wave(r.src, a.waves) < a.wave;
-            const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
-            *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
+            for (int q = i; q < R; q += kTileBlock) {
+                const RemRec<W> r = recs[q];
+                const bool early = tile_wave(r.src, a.waves) < a.wave;
+                const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
+                *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
+            }
         }
+        long long c1 = a.dbg ? clock64() : 0;
         __syncthreads();
         double f = 0.0, ivi = 0.0;
         int dgi = 0;
@@ -1033,7 +1085,14 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
             if (recs_on) {
                 const int rb = kLean ? (int)a.rrel[j] : (int)Rs[i];
                 const int re = i + 1 < nn ? (kLean ? (int)a.rrel[j + 1] : (int)Rs[i + 1]) : R;
-                for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
+                if (kLean) {
+                    for (int q = rb; q < re; ++q) {
+                        const double v = vals[q] * rec_w(recs[q]);
+                        s += v;
+                    }
+                } else {
+                    for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
+                }
             }
             f = (kLean ? a.F[j] : Fs[i]) + s + hs;
         }
@@ -1095,9 +1154,7 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
             resid += fabs(f) + fabs(An) * (double)(kLean ? a.wr[j] : Ws[i]);
             if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
         }
-        cur = nxt;
-        nxt = after;
-        __syncthreads();                             // buffer b free for the bundle after next
+        __syncthreads();                             // buffer b free for the bundle kNB-1 ahead
         if (a.dbg && i == 0) {
             const long long c4 = clock64();
             unsigned long long *qd = a.dbg + blockIdx.x * 5;
@@ -1286,7 +1343,7 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
         int optin = 0;
         DI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
         const int64_t per_cta = std::min<int64_t>(optin, (int64_t)per_sm / kTileBlocksPerSM - 1024);
-        const int64_t budget = (per_cta - (int64_t)fa.sharedSizeBytes - kSharedHead) / 2;
+        const int64_t budget = (per_cta - (int64_t)fa.sharedSizeBytes - kSharedHead) / kNB;
         const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
         int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
         cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
@@ -1294,7 +1351,7 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
         // edges from L1/L2 (prefetched to L2 with the bundle)
         if (kTileBlocksPerSM > 1 || getenv("DIT_NO_EDGE_STAGING")) cap = 0;
         tp.edge_cap = cap;
-        tp.tile_smem = (size_t)(kSharedHead + 2 * (fixed + cap));
+        tp.tile_smem = (size_t)(kSharedHead + kNB * (fixed + cap));
         DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
         if (kLean) {
             // the smallest shared-memory carveout that holds the CTAs: the rest is L1,
