@@ -61,7 +61,8 @@ struct Ctrl {
 // A CSC (targets -> in-edges, ascending source) and its pull work plan:
 // pieces of <= 64 in-edges that never cross a 2048-edge tile, split targets.
 struct PullPlan {
-    bool built = false;
+    bool built = false;            // CSC ready
+    bool pieces_built = false;     // pull work plan ready (built on the first pull-variant call)
     int64_t nt = 0, m = 0;         // targets, edges
     int64_t *ptr = nullptr;        // [nt+1]
     int32_t *src = nullptr;        // [m] source row of each in-edge

@@ -246,7 +246,7 @@ void build_plan_pieces(di_graph *h, PullPlan &pd) {
     DI_CUDA(cudaFreeAsync(po, st));
     DI_CUDA(cudaStreamSynchronize(st));
     pd.nfix = (int64_t)nfix;
-    pd.built = true;
+    pd.pieces_built = true;
 }
 
 void free_plan(PullPlan &p) {
@@ -329,8 +329,7 @@ void build_transpose(di_graph *h) {
 
     phase_mark(st, "transpose: gather");    exclusive_scan_i64(cnt, T.ptr, nt, st);
     DI_CUDA(cudaFreeAsync(cnt, st));
-    build_plan_pieces(h, T);
-    phase_mark(st, "transpose: pull pieces");
+    T.built = true;                      // the pull work plan follows on first use (build_plan_pieces)
 }
 
 // ---------------------------------------------------------------- pull sweep

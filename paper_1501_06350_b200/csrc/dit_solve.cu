@@ -447,6 +447,9 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
         if (o.variant == DI_VARIANT_TILED) {
             build_tiles(h);
             if (!s.A2) DI_CUDA(cudaMallocAsync(&s.A2, g.n * sizeof(double), h->stream));
+        } else if (!g.t.pieces_built) {
+            build_plan_pieces(h, g.t);
+            phase_mark(h->stream, "transpose: pull pieces");
         }
         if (!s.A) DI_CUDA(cudaMallocAsync(&s.A, g.n * sizeof(double), h->stream));
     }
@@ -461,7 +464,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     c.theta = o.theta;
     c.tol = tol;
     c.max_sweeps = (unsigned long long)(o.max_sweeps > 0 ? o.max_sweeps : 10000000LL);
-    c.variant = g.t.built ? o.variant : DI_VARIANT_PUSH;
+    c.variant = g.t.built && (o.variant == DI_VARIANT_TILED || g.t.pieces_built) ? o.variant : DI_VARIANT_PUSH;
     if (o.variant == DI_VARIANT_TILED && !g.tl.built) c.variant = DI_VARIANT_PUSH;
     c.pull_edges = o.pull_frac * (double)g.m;
     c.hist = s.hist;
@@ -495,11 +498,11 @@ void launch_sweep(di_graph *h) {
         return;
     }
     launch_select(h, false);
-    if (h->g.t.built) launch_select(h, true);
+    if (h->g.t.pieces_built) launch_select(h, true);
     mark_event(h, k, 1);
     launch_push(h);
     mark_event(h, k, 2);
-    if (h->g.t.built) launch_pull(h);
+    if (h->g.t.pieces_built) launch_pull(h);
     mark_event(h, k, 3);
 }
 
