@@ -273,6 +273,9 @@ def run_ours(args):
     res = results[-1]
     assert res["converged"], res
     roofline = roofline_from(prof_tot, spec.name, args.variant)
+    tiled_plan = _lib.di_plan_stats(G.handle) if args.variant == "tiled" else None
+    G.close()                                      # the e2e graphs below reuse its pooled memory
+    torch.cuda.synchronize()
     # e2e through the C ABI with host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -313,7 +316,7 @@ def run_ours(args):
                        "push_sweeps": res["push_sweeps"], "pull_sweeps": res["pull_sweeps"],
                        "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",
                        "generate_s": round(gen_s, 2),
-                       "tiled_plan": _lib.di_plan_stats(G.handle) if args.variant == "tiled" else None},
+                       "tiled_plan": tiled_plan},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks}
     print(json.dumps(line), flush=True)

@@ -11,6 +11,9 @@
 // bitwise reproducible run to run on a given graph.
 #include "dit_internal.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
+
 #include <utility>
 
 
@@ -288,19 +291,39 @@ void build_transpose(di_graph *h) {
         const int grid = h->num_sms * 8;
         k_iota_keys<<<grid, kThreads, 0, st>>>(g.col, m, k0, v0, wide);
         count_launch();
-        const int64_t ntiles = (m + kSortTile - 1) / kSortTile;
-        int64_t *hc, *ho;
-        DI_CUDA(cudaMallocAsync(&hc, (int64_t)kRadix * ntiles * sizeof(int64_t), st));
-        DI_CUDA(cudaMallocAsync(&ho, ((int64_t)kRadix * ntiles + 1) * sizeof(int64_t), st));
         int bits = 1;
         while (bits < 31 && ((int64_t)1 << bits) < nt) ++bits;
-        for (int shift = 0; shift < bits; shift += kRadixBits) {
-            radix_sort_pass_launch(k0, v0, k1, v1, m, shift, ntiles, hc, ho, wide, st);
-            std::swap(k0, k1);
-            std::swap(v0, v1);
+        if (m < (int64_t)0x7fffffff && !getenv("DIT_OWN_RADIX")) {
+            // graph-builder plumbing: the toolkit's (CUB) stable radix sort of the edge
+            // indices by target -- the sweep kernels are all our own
+            cub::DoubleBuffer<uint32_t> kb(k0, k1);
+            cub::DoubleBuffer<uint32_t> vb((uint32_t *)v0, (uint32_t *)v1);
+            size_t tmp_bytes = 0;
+            DI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int)m, 0, bits, st));
+            // its scratch outside the stream-ordered pool, which keeps the big builder
+            // temporaries cached in a stable layout
+            void *tmp = nullptr;
+            DI_CUDA(cudaMalloc(&tmp, tmp_bytes));
+            DI_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, (int)m, 0, bits, st));
+            DI_CUDA(cudaStreamSynchronize(st));
+            cudaFree(tmp);
+            if (kb.Current() != k0) {
+                std::swap(k0, k1);
+                std::swap(v0, v1);
+            }
+        } else {
+            const int64_t ntiles = (m + kSortTile - 1) / kSortTile;
+            int64_t *hc, *ho;
+            DI_CUDA(cudaMallocAsync(&hc, (int64_t)kRadix * ntiles * sizeof(int64_t), st));
+            DI_CUDA(cudaMallocAsync(&ho, ((int64_t)kRadix * ntiles + 1) * sizeof(int64_t), st));
+            for (int shift = 0; shift < bits; shift += kRadixBits) {
+                radix_sort_pass_launch(k0, v0, k1, v1, m, shift, ntiles, hc, ho, wide, st);
+                std::swap(k0, k1);
+                std::swap(v0, v1);
+            }
+            DI_CUDA(cudaFreeAsync(hc, st));
+            DI_CUDA(cudaFreeAsync(ho, st));
         }
-        DI_CUDA(cudaFreeAsync(hc, st));
-        DI_CUDA(cudaFreeAsync(ho, st));
         // in-degrees -> ptr
         phase_mark(st, "transpose: radix sort");
         k_run_bounds<<<grid, kThreads, 0, st>>>(k0, m, cnt);

@@ -12,7 +12,7 @@ g = synth.generate(spec)
 rp, col, w = pin(g.row_ptr), pin(g.col), pin(g.w)
 Hh = pin(np.empty(g.n))
 stream = torch.cuda.current_stream()
-for it in range(3):
+for it in range(5):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     h = _lib.di_graph_create(g.n, rp, col, w, device=0, stream=stream)
     torch.cuda.synchronize(); t1 = time.perf_counter()
