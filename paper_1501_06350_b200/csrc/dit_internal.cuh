@@ -111,7 +111,8 @@ struct TilePlan {
     // tile has <= 2 x kNodeTile pieces); pieces are ranked by length (longest
     // first) and cut into 32 virtual warps of 32; real warp w runs virtual
     // warps w and 31-w (longest with shortest).  Slot s of the piece of rank r
-    // sits at ltile[t] + vofs[t*33 + r/32] + 32 s + r%32 (padding: source
+    // sits at ltile[t] + vofs[t*33 + r/32] + ell_slot(s, r%32, K) (dit_tile.cu:
+    // runs of 4 slots per lane for s < K - K%4, then 32 s + r%32; padding: source
     // kNodeTile, weight 0).  A target's pieces, in edge order, are the ranks
     // plist[t*1024 + vfirst[t*513 + i] ...  vfirst[t*513 + i + 1]).
     uint32_t *vofs = nullptr;      // [ntile*33]

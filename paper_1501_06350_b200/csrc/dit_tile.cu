@@ -63,6 +63,19 @@ static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per warp");
 template <typename W>
 using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
 
+// sliced-ELL slot groups: the first K - K % kSlotGroup slots of a lane sit in runs
+// of kSlotGroup (one vector load each), the rest one per row of 32
+#ifndef DIT_SLOT_GROUP
+#define DIT_SLOT_GROUP 4
+#endif
+constexpr int kSlotGroup = DIT_SLOT_GROUP;
+static_assert(kSlotGroup == 1 || kSlotGroup == 2 || kSlotGroup == 4, "slot group 1, 2 or 4");
+// offset of slot s of lane `lane` in a virtual warp of K slots per lane
+__host__ __device__ __forceinline__ int64_t ell_slot(int64_t s, int lane, int64_t K) {
+    const int64_t Kg = K - K % kSlotGroup;
+    return s < Kg ? 32 * kSlotGroup * (s / kSlotGroup) + kSlotGroup * lane + (s % kSlotGroup) : 32 * s + lane;
+}
+
 // remote record: source and raw weight of one remote in-edge
 template <typename W>
 struct RemRec {
@@ -322,7 +335,8 @@ __global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *_
             const int64_t cap = vcap[tile];
             const int pf = vfirst[tile * kVfStride + (t - tile * kNodeTile)];
             const int r = plist[tile * kVRows + pf + (int)(lrank / cap)];
-            const int64_t o = ltile[tile] + vofs[tile * kVofsStride + r / 32] + 32 * (lrank % cap) + (r % 32);
+            const uint32_t v0 = vofs[tile * kVofsStride + r / 32], v1 = vofs[tile * kVofsStride + r / 32 + 1];
+            const int64_t o = ltile[tile] + v0 + ell_slot(lrank % cap, r % 32, (v1 - v0) / 32);
             lsrc[o] = (uint16_t)(s - tile * kNodeTile);
             if constexpr (kW) lw[o] = tw[k];
         } else {
@@ -815,6 +829,51 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     constexpr bool kW = !std::is_same<W, NoW>::value;
     double acc = 0.0;
     int s = 0;
+    if constexpr (kSlotGroup > 1) {
+        // grouped slots: kSlotGroup sources (and weights) per vector load, in slot order
+        const int lane = base & 31, o0 = base - lane;
+        const int Kg = K - K % kSlotGroup;
+        for (; s < Kg; s += kSlotGroup) {
+            const int k = o0 + 32 * s + kSlotGroup * lane;
+            if constexpr (kSlotGroup == 4) {
+                const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
+                double v0 = gq[e.x & 0xffffu], v1 = gq[e.x >> 16], v2 = gq[e.y & 0xffffu], v3 = gq[e.y >> 16];
+                if constexpr (kW) {
+                    if constexpr (sizeof(StoreW<W>) == 4) {
+                        const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
+                        v0 *= (double)w4.x;
+                        v1 *= (double)w4.y;
+                        v2 *= (double)w4.z;
+                        v3 *= (double)w4.w;
+                    } else {
+                        v0 *= (double)ew[k];
+                        v1 *= (double)ew[k + 1];
+                        v2 *= (double)ew[k + 2];
+                        v3 *= (double)ew[k + 3];
+                    }
+                }
+                acc += v0;
+                acc += v1;
+                acc += v2;
+                acc += v3;
+            } else {
+                const uint32_t e = *reinterpret_cast<const uint32_t *>(es + k);
+                double v0 = gq[e & 0xffffu], v1 = gq[e >> 16];
+                if constexpr (kW) {
+                    if constexpr (sizeof(StoreW<W>) == 4) {
+                        const float2 w2 = *reinterpret_cast<const float2 *>(ew + k);
+                        v0 *= (double)w2.x;
+                        v1 *= (double)w2.y;
+                    } else {
+                        v0 *= (double)ew[k];
+                        v1 *= (double)ew[k + 1];
+                    }
+                }
+                acc += v0;
+                acc += v1;
+            }
+        }
+    }
     for (; s + 4 <= K; s += 4) {
         const int k = base + 32 * s;
         const int s0 = es[k], s1 = es[k + 32], s2 = es[k + 64], s3 = es[k + 96];
