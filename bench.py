@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--rounds", type=int, default=4, help="local rounds per sweep (variant tiled)")
     p.add_argument("--theta", type=float, default=1.0)
     p.add_argument("--tol", type=float, default=None)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--scale-n", type=int, default=None, help="override n (debug only)")
     return p.parse_args()
@@ -292,6 +292,8 @@ def run_ours(args):
             b.record(stream)
             torch.cuda.synchronize()
             _lib.di_graph_destroy(h)
+            print(f"[bench] e2e step {it}: {a.elapsed_time(b):.1f} ms" + (" (untimed)" if it == 0 else ""),
+                  file=sys.stderr, flush=True)
             if it == 0:
                 continue
             e_ms += a.elapsed_time(b)

@@ -4,6 +4,8 @@
 #include "dit_internal.cuh"
 
 #include <chrono>
+#include <string>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -103,10 +105,30 @@ void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStre
     DI_CUDA(cudaGetLastError());
 }
 
-// DIT_BUILD_TIMING=1: print the time since the previous mark (stream synchronised)
+// DIT_BUILD_TIMING=1: print the time since the previous mark (stream synchronised);
+// =2: CUDA events only (no synchronisation), printed at the plan's "done" mark
 void phase_mark(cudaStream_t st, const char *name) {
-    static const bool on = getenv("DIT_BUILD_TIMING") != nullptr;
+    static const char *env = getenv("DIT_BUILD_TIMING");
+    static const bool on = env != nullptr;
     if (!on) return;
+    if (env[0] == '2') {
+        static std::vector<std::pair<cudaEvent_t, std::string>> marks;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        marks.emplace_back(ev, name);
+        if (std::string(name).find("done") != std::string::npos) {
+            cudaEventSynchronize(ev);
+            for (size_t i = 1; i < marks.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, marks[i - 1].first, marks[i].first);
+                fprintf(stderr, "[dit] ev %-25s %9.2f ms\n", marks[i].second.c_str(), ms);
+            }
+            for (auto &m : marks) cudaEventDestroy(m.first);
+            marks.clear();
+        }
+        return;
+    }
     static auto last = std::chrono::steady_clock::now();
     cudaStreamSynchronize(st);
     const auto now = std::chrono::steady_clock::now();
