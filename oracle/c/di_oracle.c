@@ -225,17 +225,32 @@ int64_t orc_power_iteration(int64_t n, const int64_t *col_ptr, const int32_t *ro
  *         linear in the diffused amount) -- a tile of a later wave takes them
  *         in during this sweep, any other tile in the next one.
  *      c. H += D; l += D(i) for dangling i (§3.3).
+ *   3. (partitions, R16) with nb > 1 partition bounds
+ *      bounds[0] = 0 < bounds[1] < ... < bounds[nb-1] = n, a push of step 2b
+ *      whose source and target lie in different partitions is held back and
+ *      added to F after the sweep's last wave (the ranks exchange once a sweep).
  * waves = 1, rounds = 1 is the theta = 0 sweep of orc_sweep_run.
  * ---------------------------------------------------------------------- */
+static int64_t part_of(const int64_t *bounds, int64_t nb, int64_t x)
+{
+    int64_t p = 0;                                /* largest p with bounds[p] <= x */
+    while (p + 1 < nb - 1 && bounds[p + 1] <= x) ++p;
+    return p;
+}
+
 int64_t orc_tiled_sweep_run(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, const double *pval,
                             double d, int64_t tile, int rounds, int waves, double tol, int64_t max_sweeps,
                             double *F, double *H, double *leak, int64_t *edges, int64_t *nodes,
-                            double *residual_out)
+                            double *residual_out, const int64_t *bounds, int64_t nb)
 {
     int64_t sweeps = 0;
     double *D = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double *f = (double *)malloc(sizeof(double) * (size_t)(tile > 0 ? tile : 1));
     double *fn = (double *)malloc(sizeof(double) * (size_t)(tile > 0 ? tile : 1));
+    double *Fx = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));   /* held-back cross-partition pushes */
+    int64_t *pt = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    const int parted = bounds != NULL && nb > 2;
+    for (int64_t i = 0; i < n; ++i) pt[i] = parted ? part_of(bounds, nb, i) : 0;
     double r = 0.0;
     if (waves < 1) waves = 1;
     for (;;) {
@@ -270,13 +285,22 @@ int64_t orc_tiled_sweep_run(int64_t n, const int64_t *col_ptr, const int32_t *ro
                 if (col_ptr[i] == col_ptr[i + 1]) *leak += D[i];
                 for (int64_t e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
                     int64_t t = row_idx[e];
-                    if (t < a || t >= z) F[t] += d * D[i] * pval[e];
+                    if (t >= a && t < z) continue;
+                    if (pt[t] != pt[i]) Fx[t] += d * D[i] * pval[e];
+                    else F[t] += d * D[i] * pval[e];
                 }
                 H[i] += D[i];
             }
         }
+        if (parted)
+            for (int64_t i = 0; i < n; ++i) {
+                F[i] += Fx[i];
+                Fx[i] = 0.0;
+            }
         ++sweeps;
     }
+    free(Fx);
+    free(pt);
     free(D);
     free(f);
     free(fn);

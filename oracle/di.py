@@ -124,7 +124,7 @@ def _clib():
         lib.orc_sweep_run.restype = I64
         lib.orc_power_iteration.argtypes = [I64, P, P, P, D, P, D, I64, P, P]
         lib.orc_tiled_sweep_run.argtypes = [I64, P, P, P, D, I64, ctypes.c_int, ctypes.c_int, D, I64, P, P, P, P, P,
-                                            P]
+                                            P, P, I64]
         lib.orc_tiled_sweep_run.restype = I64
         lib.orc_power_iteration.restype = I64
         _lib = lib
@@ -185,10 +185,11 @@ def sweep_run(n, col_ptr, row_idx, pval, d, F, H, theta=1.0, tol=1e-12,
 
 
 def tiled_sweep_run(n, col_ptr, row_idx, pval, d, F, H, tile=1024, rounds=4, tol=1e-12,
-                    max_sweeps=1_000_000, leak=0.0, waves=1):
+                    max_sweeps=1_000_000, leak=0.0, waves=1, bounds=None):
     """Tile-local sweeps (readings R12, R15) from (F, H); tiles run in
     `waves` waves (tile index mod waves), a wave's remote pushes reaching later
-    waves of the same sweep."""
+    waves of the same sweep.  `bounds` (partition starts + n, R16): pushes
+    between partitions reach their target after the sweep."""
     cp, ri, pv = _cols(col_ptr, row_idx, pval)
     F = np.array(F, dtype=np.float64, copy=True)
     H = np.array(H, dtype=np.float64, copy=True)
@@ -196,8 +197,9 @@ def tiled_sweep_run(n, col_ptr, row_idx, pval, d, F, H, tile=1024, rounds=4, tol
     ed = np.zeros(1, dtype=np.int64)
     nd = np.zeros(1, dtype=np.int64)
     res = np.zeros(1, dtype=np.float64)
+    bd = np.ascontiguousarray(bounds if bounds is not None else [0, n], dtype=np.int64)
     s = _clib().orc_tiled_sweep_run(n, _p(cp), _p(ri), _p(pv), d, tile, rounds, waves, tol, max_sweeps,
-                                    _p(F), _p(H), _p(lk), _p(ed), _p(nd), _p(res))
+                                    _p(F), _p(H), _p(lk), _p(ed), _p(nd), _p(res), _p(bd), len(bd))
     return RunResult(F=F, H=H, leak=float(lk[0]), steps=int(s), edges=int(ed[0]),
                      nodes=int(nd[0]), residual=float(res[0]))
 

@@ -385,9 +385,50 @@ def test_tiled_waves_absorb_in_the_same_sweep():
     assert r.H[0] == f0 and r.F[0] == pytest.approx(d * f0, rel=1e-15)
 
 
-@pytest.mark.parametrize("tile,rounds,waves", [(16, 2, 1), (64, 5, 1), (1024, 3, 1), (16, 2, 2), (32, 3, 3),
-                                               (16, 1, 5)])
-def test_tiled_conservation_and_convergence(tile, rounds, waves):
+def test_tiled_partitions_defer_cross_pushes():
+    # R16: the same tile-0 -> tile-1 push with the tiles in different partitions
+    # reaches node 4 only after the sweep, even with two waves
+    n, d = 8, 0.85
+    rp, c, _ = csr_from_edges(n, [(0, 4)])
+    cp, ri, pv = graph.column_entries(n, rp, c)
+    f0 = (1 - d) / n
+    st = di.di_init(n, d)
+    r = di.tiled_sweep_run(n, cp, ri, pv, d, st.F, st.H, tile=4, rounds=1, tol=0, max_sweeps=1, waves=2,
+                           bounds=[0, 4, 8])
+    assert r.H[4] == f0 and r.F[4] == pytest.approx(d * f0, rel=1e-15) and r.F.sum() == r.F[4]
+    # partition bound inside a tile: the local push 1 -> 2 (same tile) is still local
+    rp, c, _ = csr_from_edges(n, [(1, 2)])
+    cp, ri, pv = graph.column_entries(n, rp, c)
+    r = di.tiled_sweep_run(n, cp, ri, pv, d, st.F, st.H, tile=4, rounds=2, tol=0, max_sweeps=1, waves=2,
+                           bounds=[0, 2, 8])
+    assert r.H[2] == pytest.approx(f0 * (1 + d), rel=1e-15) and np.all(r.F == 0)
+
+
+@pytest.mark.parametrize("waves", [1, 2, 3])
+def test_tiled_partition_limits(waves):
+    g = small_graph(320, 21, weighted=True)
+    cp, ri, pv = cols_of(g)
+    st = di.di_init(g.n, D)
+    T = 16
+    for k in (1, 4):
+        base = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=2, tol=0, max_sweeps=k, waves=waves)
+        # one partition: the unpartitioned schedule, bit for bit
+        one = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=2, tol=0, max_sweeps=k, waves=waves,
+                                 bounds=[0, g.n])
+        assert np.array_equal(one.H, base.H) and np.array_equal(one.F, base.F)
+        # a partition per tile: every remote push waits for the sweep's end, so the
+        # waves no longer matter -- the one-wave schedule (up to summation order)
+        per = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=2, tol=0, max_sweeps=k, waves=waves,
+                                 bounds=list(range(0, g.n, T)) + [g.n])
+        w1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=2, tol=0, max_sweeps=k, waves=1)
+        assert np.allclose(per.H, w1.H, rtol=1e-13, atol=0) and np.allclose(per.F, w1.F, rtol=1e-12, atol=1e-20)
+        assert per.edges == w1.edges
+
+
+@pytest.mark.parametrize("tile,rounds,waves,bounds", [(16, 2, 1, None), (64, 5, 1, None), (1024, 3, 1, None),
+                                                      (16, 2, 2, None), (32, 3, 3, None), (16, 1, 5, None),
+                                                      (16, 2, 2, (0, 64, 130, 200)), (32, 3, 3, (0, 96, 200))])
+def test_tiled_conservation_and_convergence(tile, rounds, waves, bounds):
     g = small_graph(200, 13)
     cp, ri, pv = cols_of(g)
     P = graph.dense_P(g.n, cp, ri, pv)
@@ -395,13 +436,13 @@ def test_tiled_conservation_and_convergence(tile, rounds, waves):
     F, H, lk = st.F, st.H, 0.0
     for _ in range(6):
         r = di.tiled_sweep_run(g.n, cp, ri, pv, D, F, H, tile=tile, rounds=rounds, tol=0, max_sweeps=1, leak=lk,
-                               waves=waves)
+                               waves=waves, bounds=bounds)
         F, H, lk = r.F, r.H, r.leak
         assert np.abs(H + F - st.F0 - D * (P @ H)).max() <= 1e-15           # Eq. (12)
         assert lk == pytest.approx(H[graph.dangling_mask(g.n, g.row_ptr)].sum(), abs=1e-15)
     x = dense.dense_solve(P, D, synth.uniform_Z(g.n))
-    r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=rounds, tol=1e-13, waves=waves)
+    r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=rounds, tol=1e-13, waves=waves, bounds=bounds)
     assert np.abs(r.H - x).sum() <= 1e-12
     # more local rounds never need more sweeps than one round
-    r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13, waves=waves)
+    r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13, waves=waves, bounds=bounds)
     assert r.steps <= r1.steps
