@@ -235,8 +235,9 @@ void build_tiles(di_graph *h);
 void free_tiles(TilePlan &t);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
-void launch_tile_heavy(di_graph *h, int force);
-void launch_tile_kernel(di_graph *h, int rounds);
+void launch_tile_heavy(di_graph *h, int force, int wave = 0);
+void launch_tile_kernel(di_graph *h, int rounds, int wave = 0);
+int tile_waves(const di_graph *h);
 void launch_take_ghost_sums(di_graph *h, double *out, int force);
 void launch_reduce_exact(di_graph *h);
 void mark_event(di_graph *h, int64_t sweep, int k);

@@ -129,10 +129,11 @@ __global__ void k_apply_seg(double *__restrict__ F, const int32_t *__restrict__ 
 __global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m, int force);
 
 // Tiled shards: the ghost slots are heavy targets of the tile
-// plan.  di_shard_sweep runs the heavy gather of the previous sweep's pushes
-// (ghost sums -> send buffer), the caller exchanges them, di_shard_apply adds
-// the received fluid to F, and di_shard_reduce runs the tile kernel (local
-// rounds, residual estimate of reading R13 -> stats).
+// plan's first wave.  di_shard_sweep runs wave 0's heavy gather (the previous
+// sweep's pushes; ghost sums -> send buffer), the caller exchanges them,
+// di_shard_apply adds the received fluid to F, and di_shard_reduce runs wave
+// 0's tile kernel, then each later wave's heavy gather and tile kernel (R15,
+// R16; local rounds, residual estimate of reading R13 -> stats).
 void shard_sweep(di_graph *h, double *ghost_out) {
     if (h->s.tiled_call) {
         const int64_t k = h->s.launched;
@@ -166,10 +167,15 @@ void shard_apply(di_graph *h, const double *recv, int force) {
 
 void shard_reduce(di_graph *h) {
     if (h->s.tiled_call) {
-        const int64_t k = h->s.launched;       // shards run one wave: events 0, 1, 2
-        launch_tile_kernel(h, h->s.rounds);
+        const int64_t k = h->s.launched;       // events as launch_tile_sweep: [2c] heavy(c) [2c+1] tile(c)
+        launch_tile_kernel(h, h->s.rounds, 0);
         mark_event(h, k, 2);
-        mark_event(h, k, 4);
+        for (int c = 1; c < tile_waves(h); ++c) {
+            launch_tile_heavy(h, 0, c);
+            mark_event(h, k, 2 * c + 1);
+            launch_tile_kernel(h, h->s.rounds, c);
+            mark_event(h, k, 2 * c + 2);
+        }
         h->s.launched += 1;
         return;
     }

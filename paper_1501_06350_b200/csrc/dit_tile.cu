@@ -492,8 +492,8 @@ static void build_tiles_t(di_graph *h) {
     tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
     const int64_t nS = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
     tp.nstripe = nS;
-    tp.waves = g.shard ? 1 : kTileWaves;
-    if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = g.shard ? 1 : std::max(1, atoi(e));
+    tp.waves = kTileWaves;                           // shards too (R16: cross-rank pushes wait a sweep)
+    if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = std::max(1, atoi(e));
     tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(tp.waves, tp.ntile));   // empty waves dropped
     const int64_t S = tp.waves * nS;                 // heavy groups (wave, stripe)
     // ---- classes of the in-edges
@@ -1461,23 +1461,25 @@ void launch_tile_sweep(di_graph *h, int rounds) {
 }
 
 // shard sweeps run the two halves separately, the ghost exchange in between
-void launch_tile_heavy(di_graph *h, int force) {
+void launch_tile_heavy(di_graph *h, int force, int wave) {
     if (h->g.tl.ntile == 0) return;
     switch (h->g.w_kind) {
-    case DI_W_F32: launch_heavy_t<float>(h, 0, force); break;
-    case DI_W_F64: launch_heavy_t<double>(h, 0, force); break;
-    default: launch_heavy_t<NoW>(h, 0, force);
+    case DI_W_F32: launch_heavy_t<float>(h, wave, force); break;
+    case DI_W_F64: launch_heavy_t<double>(h, wave, force); break;
+    default: launch_heavy_t<NoW>(h, wave, force);
     }
 }
 
-void launch_tile_kernel(di_graph *h, int rounds) {
+void launch_tile_kernel(di_graph *h, int rounds, int wave) {
     if (h->g.tl.ntile == 0) return;
     switch (h->g.w_kind) {
-    case DI_W_F32: launch_tile_kernel_t<float>(h, rounds, 0); break;
-    case DI_W_F64: launch_tile_kernel_t<double>(h, rounds, 0); break;
-    default: launch_tile_kernel_t<NoW>(h, rounds, 0);
+    case DI_W_F32: launch_tile_kernel_t<float>(h, rounds, wave); break;
+    case DI_W_F64: launch_tile_kernel_t<double>(h, rounds, wave); break;
+    default: launch_tile_kernel_t<NoW>(h, rounds, wave);
     }
 }
+
+int tile_waves(const di_graph *h) { return h->g.tl.waves; }
 
 // ghost slots' inflow (heavy sums of the last sweep's pushes) -> the send buffer
 __global__ void k_take_ghost_sums(const int32_t *__restrict__ hidx, const double *__restrict__ hsum, int64_t n,

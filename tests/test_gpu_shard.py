@@ -105,15 +105,16 @@ def test_lockstep_theta0_sweeps_elementwise(gpu):
     assert np.allclose(torch.cat(Hs).cpu().numpy(), r.H, rtol=1e-13, atol=1e-18)
 
 
-@pytest.mark.parametrize("weighted", [False, True])
-def test_lockstep_tiled_sweeps_elementwise(gpu, weighted):
-    # shard bounds on tile boundaries: the sharded tiled schedule is exactly the
-    # oracle's tiled sweep (cross-shard pushes are remote pushes, R12/R13)
+@pytest.mark.parametrize("weighted,world", [(False, 2), (True, 2), (True, 3)])
+def test_lockstep_tiled_sweeps_elementwise(gpu, weighted, world):
+    # shard bounds on multiples of W tiles: the sharded tiled schedule is exactly
+    # the oracle's tiled sweep with the shards as partitions (cross-shard pushes
+    # land after the sweep, R12/R13/R15/R16)
     from paper_1501_06350_b200 import _lib, dist
-    T = _lib.DI_TILE_NODES
-    spec = synth.CONFIGS[1].scaled(2 * 7 * T, seed=12, weighted=weighted)
-    shards, bounds = _shards(spec, 2)
-    assert bounds[1] % T == 0
+    T, W = _lib.DI_TILE_NODES, _lib.DI_TILE_WAVES
+    spec = synth.CONFIGS[1].scaled(world * 4 * W * T, seed=12, weighted=weighted)
+    shards, bounds = _shards(spec, world)
+    assert all(b % (W * T) == 0 for b in bounds)
     coll = LockstepCollectives()
     coll.plan(shards, bounds)
     g = synth.generate(spec)
@@ -121,7 +122,8 @@ def test_lockstep_tiled_sweeps_elementwise(gpu, weighted):
     st = di.di_init(g.n, D)
     for k in (1, 3):
         Hs, res = dist.solve(shards, coll, d=D, tol=0.0, variant=3, local_rounds=3, max_sweeps=k)
-        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=3, tol=0, max_sweeps=k)
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=T, rounds=3, tol=0, max_sweeps=k, waves=W,
+                               bounds=list(bounds))
         assert all(x["sweeps"] == k for x in res)
         assert np.allclose(torch.cat(Hs).cpu().numpy(), r.H, rtol=1e-12, atol=1e-20)
         assert sum(x["diffused_edges"] for x in res) == r.edges
