@@ -9,6 +9,6 @@ sw = int(os.environ.get("MAX_SWEEPS", "21"))
 for it in range(4):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(); a.record()
-    H, r = G.solve(d=spec.d, tol=spec.tol, variant="tiled", local_rounds=4, max_sweeps=sw)
+    H, r = G.solve(d=spec.d, tol=spec.tol, variant="tiled", local_rounds=int(os.environ.get("ROUNDS", "4")), max_sweeps=sw)
     b.record(); torch.cuda.synchronize()
     if it: print(os.environ.get("TAG", ""), "sweeps", r["sweeps"], "ms", round(a.elapsed_time(b), 2))
