@@ -133,39 +133,12 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
-// 8-byte asynchronous global -> shared copy (LDGSTS), tracked by commit/wait groups
-__device__ __forceinline__ void cp_async8(void *dst_smem, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 // bulk prefetch of a global range into L2 (the TMA engine; no completion tracking)
 __device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // ---------------------------------------------------------------- build
-// per target: local / remote in-edge counts from the transpose
-// (shard: targets t >= n are ghost slots, every in-edge of a ghost is remote)
-__global__ void k_count_local(const int64_t *__restrict__ tptr, const int32_t *__restrict__ tsrc, int64_t n,
-                              int64_t nt, int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = warp; t < nt; t += nw) {
-        const int64_t b = tptr[t], e = tptr[t + 1];
-        const int64_t tile = t < n ? t / kNodeTile : -1;
-        int64_t c = 0;
-        for (int64_t k = b + lane_id(); k < e; k += 32) c += (tsrc[k] / kNodeTile == tile);
-        c = warp_sum(c);
-        if (lane_id() == 0) {
-            lc[t] = c;
-            rc[t] = (e - b) - c;
-        }
-    }
-}
-
 // light / heavy split of the remote in-edges, one thread per tile
 __global__ void k_classify(const int64_t *__restrict__ rc, int64_t n, int64_t ntile, int64_t *__restrict__ lrc,
                            int64_t *__restrict__ hc, int64_t *__restrict__ hflag) {
@@ -910,19 +883,11 @@ constexpr int tile_fixed_smem() {
 // One tile's TMA bundle (a buffer of the double-buffered pipeline): the
 // per-node state, the tile's layout, its light records and (when they fit)
 // its local edges.
-// DIT_LEAN_BUNDLE: the per-node rows stay out of the bundle (plain loads after an
-// L2 bulk prefetch), so that shared memory is small and L1 keeps the local edges
-#ifndef DIT_LEAN_BUNDLE
-#define DIT_LEAN_BUNDLE 0
-#endif
-constexpr bool kLean = DIT_LEAN_BUNDLE != 0;
-// lean bundles come in three: the light gathers of tile k+1 (cp.async, 8 B each,
-// into the bundle's value block) fly while tile k diffuses
-constexpr int kNB = kLean ? 3 : 2;
-constexpr int kNodeBytes = kLean ? 0 : (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
+constexpr int kNB = 2;                           // bundle buffers (double buffering)
+constexpr int kNodeBytes = (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
 template <typename W>
 constexpr int tile_buf_fixed() {
-    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32 + (kLean ? (int)kLightCap * 8 : 0);
+    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
 }
 constexpr int kSharedHead = ((int)kNodeTile + 2) * 8 + kVRows * 8;         // gq, psum
 static_assert(kNodeBytes % 16 == 0 && kSharedHead % 16 == 0, "16-byte aligned shared buffers");
@@ -948,31 +913,20 @@ __device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *F
     const int64_t wb0 = (ts.l0 * kWB) & ~int64_t(15), wb1 = (ts.l1 * kWB + 15) & ~int64_t(15);
     const int64_t ebytes = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0);
     const bool staged = ebytes <= a.edge_cap;
-    uint32_t bytes = (kLean ? 0u : 3 * n8 + 4 * n4) + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
+    uint32_t bytes = 3 * n8 + 4 * n4 + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
     if (staged) bytes += (uint32_t)ebytes;
     // order this CTA's earlier generic-proxy accesses of the buffer before the async writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(bar, bytes);
-    unsigned char *p = buf;
     const uint32_t sb = smem_u32(buf);
-    if (kLean) {
-        tma_prefetch_l2(Fsrc + a0, n8);
-        tma_prefetch_l2(a.H + a0, n8);
-        tma_prefetch_l2(a.inv + a0, n8);
-        tma_prefetch_l2(a.deg + a0, n4);
-        tma_prefetch_l2(a.wr + a0, n4);
-        tma_prefetch_l2(a.rrel + a0, n4);
-        tma_prefetch_l2(a.hidx + a0, n4);
-    } else {
-        tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
-        tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
-        tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
-        const uint32_t q = 3 * kNodeTile * 8;
-        tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
-        tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
-        tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
-        tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
-    }
+    tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
+    tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
+    tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
+    const uint32_t q = 3 * kNodeTile * 8;
+    tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
+    tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
+    tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
+    tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
     const uint32_t m = kNodeBytes;
     tma_load(sb + m, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
     tma_load(sb + m + kVofsStride * 4, a.vfirst + tile * kVfStride, kVfStride * 2, bar);
@@ -991,7 +945,6 @@ __device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *F
             tma_load(sb + eofs + (uint32_t)(sb1 - sb0), reinterpret_cast<const unsigned char *>(a.lw) + wb0,
                      (uint32_t)(wb1 - wb0), bar);
     }
-    (void)p;
 }
 
 // Persistent kernel, one 512-thread CTA per SM, tiles round-robin; the next
@@ -1035,23 +988,6 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         const int64_t r0 = recs_on ? ts.r0 : 0;
         return reinterpret_cast<RemRec<W> *>(bufp(x) + kNodeBytes + kMetaBytes + (r0 * kRS - ((r0 * kRS) & ~int64_t(15))));
     };
-    auto vals_of = [&](int x) {
-        return reinterpret_cast<double *>(bufp(x) + kNodeBytes + kMetaBytes + (int)kLightCap * kRS + 32);
-    };
-    // lean: the light gathers of the tile in buffer x, 8-byte cp.async into its value block
-    auto issue_gathers = [&](int x) {
-        const TileScalars ts = sc[x];
-        const int Rn = recs_on ? (int)(ts.r1 - ts.r0) : 0;
-        const RemRec<W> *rr = recs_of(x, ts);
-        double *vv = vals_of(x);
-        for (int q = i; q < Rn; q += kTileBlock) {
-            const int32_t src = rr[q].src;
-            if (tile_wave(src, a.waves) < a.wave) cp_async8(vv + q, Anext + src);
-            else if (gather) cp_async8(vv + q, Aprev + src);
-            else vv[q] = 0.0;
-        }
-        cp_async_commit();
-    };
     if (i == 0) {
         gq[kNodeTile] = 0.0;                         // padding slots read this
         gq[kNodeTile + 1] = 0.0;
@@ -1064,10 +1000,6 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         }
     }
     __syncthreads();
-    if (kLean && blockIdx.x < a.ntw) {
-        mbar_wait(smem_u32(&bars[0]), 0u);
-        issue_gathers(0);
-    }
     double resid = 0.0, leak = 0.0;
     unsigned long long nodes = 0, edges = 0;
     int k = 0;
@@ -1106,54 +1038,34 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         const int64_t j = a0 + i;
         const int R = (int)(r1 - r0);
         RemRec<W> *recs = recs_of(b, cur);
-        const double *vals = vals_of(b);
         // 1. remote pushes still pending: from the previous sweep, and from this sweep's
         //    earlier waves (R15): heavy sums and the light records' gathered outflow
         double hs = 0.0;
         if (valid && recs_on) {
-            const int32_t hx = kLean ? a.hidx[j] : Xs[i];
+            const int32_t hx = Xs[i];
             if (hx >= 0) hs = a.hsum[hx];
         }
-        if (kLean) {
-            // the next tile's gathers go out now (they land while this tile diffuses)
-            if (jt + G < a.ntw) {
-                const int x = (k + 1) % kNB;
-                mbar_wait(smem_u32(&bars[x]), (uint32_t)(((k + 1) / kNB) & 1));
-                issue_gathers(x);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-        } else {
 #pragma unroll 4
-            for (int q = i; q < R; q += kTileBlock) {
-                const RemRec<W> r = recs[q];
-                const bool early = tile_wave(r.src, a.waves) < a.wave;
-                const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
-                *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
-            }
+        for (int q = i; q < R; q += kTileBlock) {
+            const RemRec<W> r = recs[q];
+            const bool early = tile_wave(r.src, a.waves) < a.wave;
+            const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
+            *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
         }
         long long c1 = a.dbg ? clock64() : 0;
         __syncthreads();
         double f = 0.0, ivi = 0.0;
         int dgi = 0;
         if (valid) {
-            ivi = kLean ? a.inv[j] : Is[i];
-            dgi = kLean ? a.deg[j] : Ds[i];
+            ivi = Is[i];
+            dgi = Ds[i];
             double s = 0.0;
             if (recs_on) {
-                const int rb = kLean ? (int)a.rrel[j] : (int)Rs[i];
-                const int re = i + 1 < nn ? (kLean ? (int)a.rrel[j + 1] : (int)Rs[i + 1]) : R;
-                if (kLean) {
-                    for (int q = rb; q < re; ++q) {
-                        const double v = vals[q] * rec_w(recs[q]);
-                        s += v;
-                    }
-                } else {
-                    for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
-                }
+                const int rb = (int)Rs[i];
+                const int re = i + 1 < nn ? (int)Rs[i + 1] : R;
+                for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
             }
-            f = (kLean ? a.F[j] : Fs[i]) + s + hs;
+            f = Fs[i] + s + hs;
         }
         long long c2 = a.dbg ? clock64() : 0;
         // 2. local diffusion rounds in shared memory
@@ -1205,12 +1117,9 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
         if (valid) {
             const double An = d * D * ivi;
             a.F[j] = f;
-            if (D != 0.0) {
-                if (kLean) red_add(a.H + j, D);       // one writer per node and sweep: H + D exactly
-                else a.H[j] = Hs[i] + D;
-            }
+            if (D != 0.0) a.H[j] = Hs[i] + D;
             Anext[j] = An;
-            resid += fabs(f) + fabs(An) * (double)(kLean ? a.wr[j] : Ws[i]);
+            resid += fabs(f) + fabs(An) * (double)Ws[i];
             if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
         }
         __syncthreads();                             // buffer b free for the bundle kNB-1 ahead
@@ -1412,13 +1321,6 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
         tp.edge_cap = cap;
         tp.tile_smem = (size_t)(kSharedHead + kNB * (fixed + cap));
         DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
-        if (kLean) {
-            // the smallest shared-memory carveout that holds the CTAs: the rest is L1,
-            // which keeps the local edges between the rounds
-            const int64_t need = kTileBlocksPerSM * ((int64_t)tp.tile_smem + fa.sharedSizeBytes + 1024);
-            const int pct = (int)std::min<int64_t>(100, (need * 100 + per_sm - 1) / per_sm);
-            DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        }
     }
     const int64_t cap = tp.edge_cap;
     const size_t smem = tp.tile_smem;
