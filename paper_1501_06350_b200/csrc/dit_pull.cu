@@ -263,6 +263,78 @@ void free_plan(PullPlan &p) {
     p = PullPlan();
 }
 
+// sort payload (source id, f32 weight bits) of every edge, keys = targets
+__global__ void k_pack_keys(const int32_t *__restrict__ col, const int32_t *__restrict__ esrc,
+                            const float *__restrict__ w, int64_t m, uint32_t *__restrict__ keys,
+                            unsigned long long *__restrict__ vals) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        keys[e] = (uint32_t)col[e];
+        vals[e] = ((unsigned long long)(uint32_t)esrc[e] << 32) | (w ? __float_as_uint(w[e]) : 0u);
+    }
+}
+
+__global__ void k_unpack_t(const unsigned long long *__restrict__ vals, int64_t m, int32_t *__restrict__ src,
+                           float *__restrict__ w) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long v = vals[k];
+        src[k] = (int32_t)(v >> 32);
+        if (w) w[k] = __uint_as_float((uint32_t)v);
+    }
+}
+
+// CUB's sort scratch: one buffer per device kept for the process (grown on demand,
+// outside the stream-ordered pool so the builders' temporaries keep a stable
+// layout there; a cudaMalloc / cudaFree pair per build cost up to 0.6 s when the
+// driver had to make room).
+static void *cub_scratch(int device, size_t bytes) {
+    static void *buf[64] = {};
+    static size_t cap[64] = {};
+    if (device < 0 || device >= 64) device = 0;
+    if (bytes > cap[device]) {
+        if (buf[device]) DI_CUDA(cudaFree(buf[device]));
+        buf[device] = nullptr;
+        cap[device] = 0;
+        DI_CUDA(cudaMalloc(&buf[device], bytes));
+        cap[device] = bytes;
+    }
+    return buf[device];
+}
+
+// Transpose with the sources and f32 weights riding in the sort (CUB, m < 2^31):
+// no gather through the permutation afterwards.
+static void build_transpose_packed(di_graph *h, int64_t *cnt) {
+    DevGraph &g = h->g;
+    PullPlan &T = g.t;
+    cudaStream_t st = h->stream;
+    const int64_t n = g.n, m = g.m, nt = g.nt;
+    const int grid = h->num_sms * 8;
+    uint32_t *k0, *k1;
+    unsigned long long *v0, *v1;
+    int32_t *esrc;
+    DI_CUDA(cudaMallocAsync(&esrc, m * 4, st));
+    k_edge_src<<<grid, kThreads, 0, st>>>(g.row_ptr, n, esrc);
+    DI_CUDA(cudaMallocAsync(&k0, m * 4, st));
+    DI_CUDA(cudaMallocAsync(&v0, m * 8, st));
+    k_pack_keys<<<grid, kThreads, 0, st>>>(g.col, esrc, (const float *)g.w, m, k0, v0);
+    count_launch(2);
+    DI_CUDA(cudaFreeAsync(esrc, st));
+    DI_CUDA(cudaMallocAsync(&k1, m * 4, st));
+    DI_CUDA(cudaMallocAsync(&v1, m * 8, st));
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < nt) ++bits;
+    cub::DoubleBuffer<uint32_t> kb(k0, k1);
+    cub::DoubleBuffer<unsigned long long> vb(v0, v1);
+    size_t tmp_bytes = 0;
+    DI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int)m, 0, bits, st));
+    DI_CUDA(cub::DeviceRadixSort::SortPairs(cub_scratch(h->device, tmp_bytes), tmp_bytes, kb, vb, (int)m, 0, bits, st));
+    phase_mark(st, "transpose: radix sort");
+    k_run_bounds<<<grid, kThreads, 0, st>>>(kb.Current(), m, cnt);
+    k_unpack_t<<<grid, kThreads, 0, st>>>(vb.Current(), m, T.src, (float *)T.w);
+    count_launch(2);
+    for (uint32_t *p : {k0, k1}) DI_CUDA(cudaFreeAsync(p, st));
+    for (unsigned long long *p : {v0, v1}) DI_CUDA(cudaFreeAsync(p, st));
+}
+
 void build_transpose(di_graph *h) {
     DevGraph &g = h->g;
     PullPlan &T = g.t;
@@ -280,7 +352,10 @@ void build_transpose(di_graph *h) {
     int64_t *cnt = nullptr;
     DI_CUDA(cudaMallocAsync(&cnt, (nt + 1) * sizeof(int64_t), st));
     DI_CUDA(cudaMemsetAsync(cnt, 0, (nt + 1) * sizeof(int64_t), st));
-    if (m > 0) {
+    if (m > 0 && m < (int64_t)0x7fffffff && g.w_kind != DI_W_F64 && !getenv("DIT_OWN_RADIX") &&
+        !getenv("DIT_TRANSPOSE_GATHER")) {
+        build_transpose_packed(h, cnt);
+    } else if (m > 0) {
         uint32_t *k0, *k1;
         void *v0, *v1;
         int32_t *esrc;
@@ -300,13 +375,8 @@ void build_transpose(di_graph *h) {
             cub::DoubleBuffer<uint32_t> vb((uint32_t *)v0, (uint32_t *)v1);
             size_t tmp_bytes = 0;
             DI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int)m, 0, bits, st));
-            // its scratch outside the stream-ordered pool, which keeps the big builder
-            // temporaries cached in a stable layout
-            void *tmp = nullptr;
-            DI_CUDA(cudaMalloc(&tmp, tmp_bytes));
-            DI_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, (int)m, 0, bits, st));
-            DI_CUDA(cudaStreamSynchronize(st));
-            cudaFree(tmp);
+            DI_CUDA(cub::DeviceRadixSort::SortPairs(cub_scratch(h->device, tmp_bytes), tmp_bytes, kb, vb, (int)m, 0,
+                                                    bits, st));
             if (kb.Current() != k0) {
                 std::swap(k0, k1);
                 std::swap(v0, v1);
