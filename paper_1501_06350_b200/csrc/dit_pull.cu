@@ -286,7 +286,7 @@ __global__ void k_unpack_t(const unsigned long long *__restrict__ vals, int64_t 
 // outside the stream-ordered pool so the builders' temporaries keep a stable
 // layout there; a cudaMalloc / cudaFree pair per build cost up to 0.6 s when the
 // driver had to make room).
-static void *cub_scratch(int device, size_t bytes) {
+void *cub_scratch(int device, size_t bytes) {
     static void *buf[64] = {};
     static size_t cap[64] = {};
     if (device < 0 || device >= 64) device = 0;

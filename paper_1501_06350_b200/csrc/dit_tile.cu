@@ -38,6 +38,7 @@
 // reproducible run to run.
 #include "dit_internal.cuh"
 
+#include <cub/device/device_scan.cuh>
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -266,15 +267,21 @@ __global__ void k_fill_tkey(const int64_t *__restrict__ tptr, int64_t nt, uint32
         for (int64_t k = tptr[t] + lane_id(); k < tptr[t + 1]; k += 32) tkey[k] = (uint32_t)t;
 }
 
+template <typename LT>
 __global__ void k_local_flags(const uint32_t *__restrict__ tkey, const int32_t *__restrict__ tsrc, int64_t m,
-                              int64_t n, int64_t *__restrict__ flag) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+                              int64_t n, LT *__restrict__ flag) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= m; k += (int64_t)gridDim.x * blockDim.x) {
+        if (k == m) {
+            flag[k] = 0;
+            continue;
+        }
         const int64_t t = tkey[k];
         flag[k] = (t < n && tsrc[k] / kNodeTile == t / kNodeTile) ? 1 : 0;
     }
 }
 
-__global__ void k_counts_from_scan(const int64_t *__restrict__ tptr, const int64_t *__restrict__ L, int64_t nt,
+template <typename LT>
+__global__ void k_counts_from_scan(const int64_t *__restrict__ tptr, const LT *__restrict__ L, int64_t nt,
                                    int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = tptr[t], e = tptr[t + 1];
@@ -284,10 +291,10 @@ __global__ void k_counts_from_scan(const int64_t *__restrict__ tptr, const int64
 }
 
 // every in-edge to its class, one thread per CSC position (see k_split_edges)
-template <typename W>
+template <typename W, typename LT>
 __global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *__restrict__ tkey,
                              const int32_t *__restrict__ tsrc, const StoreW<W> *__restrict__ tw,
-                             const int64_t *__restrict__ L, int64_t m, int64_t n, const int64_t *__restrict__ ltile,
+                             const LT *__restrict__ L, int64_t m, int64_t n, const int64_t *__restrict__ ltile,
                              const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
                              const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
                              const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
@@ -300,7 +307,7 @@ __global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *_
         const int64_t t = tkey[k];
         const int32_t s = tsrc[k];
         const int64_t b = tptr[t];
-        const int64_t lrank = L[k] - L[b];
+        const int64_t lrank = (int64_t)(L[k] - L[b]);
         const bool owned = t < n;
         const int64_t tile = owned ? t / kNodeTile : -1;
         if (owned && s / kNodeTile == tile) {
@@ -390,24 +397,47 @@ __global__ void k_fill_u64(unsigned long long *__restrict__ p, int64_t cnt, unsi
         p[i] = v;
 }
 
-// share of every source's out-weight that leaves its tile (warp per source)
+// share of every source's out-weight that leaves its tile: a thread per source
+// (rows of more than 32 edges by the whole warp)
 template <typename W>
 __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const StoreW<W> *__restrict__ w, const double *__restrict__ inv, int64_t n,
                                int waves, float *__restrict__ wr) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    for (int64_t i = warp; i < n; i += nw) {
-        const int64_t tile = i / kNodeTile;
-        double s = 0.0;
-        for (int64_t e = row_ptr[i] + lane_id(); e < row_ptr[i + 1]; e += 32)
-            // leaves the tile and is still pending after the sweep (a later wave takes
-            // its pushes in during the sweep, R15); ghost targets always pending
-            if (col[e] >= n || (col[e] / kNodeTile != tile && tile_wave(col[e], waves) <= tile_wave(i, waves)))
-                s += kW ? (double)w[e] : 1.0;
-        s = warp_sum(s);
-        if (lane_id() == 0) wr[i] = (float)(s * inv[i]);
+    const int lane = lane_id();
+    // leaves the tile and is still pending after the sweep (a later wave takes its
+    // pushes in during the sweep, R15); ghost targets always pending
+    auto pending = [&](int64_t i, int64_t e) {
+        const int64_t t = col[e];
+        return t >= n || (t / kNodeTile != i / kNodeTile && tile_wave(t, waves) <= tile_wave(i, waves));
+    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        int64_t b = 0, e = 0;
+        if (i < n) {
+            b = row_ptr[i];
+            e = row_ptr[i + 1];
+        }
+        const bool big = e - b > 32;
+        if (i < n && !big) {
+            double s = 0.0;
+            for (int64_t q = b; q < e; ++q)
+                if (pending(i, q)) s += kW ? (double)w[q] : 1.0;
+            wr[i] = (float)(s * inv[i]);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, big);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t il = __shfl_sync(0xffffffffu, i, l), bl = __shfl_sync(0xffffffffu, b, l),
+                          el = __shfl_sync(0xffffffffu, e, l);
+            double s = 0.0;
+            for (int64_t q = bl + lane; q < el; q += 32)
+                if (pending(il, q)) s += kW ? (double)w[q] : 1.0;
+            s = warp_sum(s);
+            if (lane == 0) wr[il] = (float)(s * inv[il]);
+        }
     }
 }
 
@@ -475,16 +505,33 @@ static void build_tiles_t(di_graph *h) {
         DI_CUDA(cudaMallocAsync(p, (nt + 1) * sizeof(int64_t), st));
     const int64_t m = g.m;
     uint32_t *tkey = nullptr;
-    int64_t *lflag = nullptr, *L = nullptr;
     DI_CUDA(cudaMallocAsync(&tkey, (m > 0 ? m : 1) * sizeof(uint32_t), st));
-    DI_CUDA(cudaMallocAsync(&lflag, (m + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMallocAsync(&L, (m + 1) * sizeof(int64_t), st));
     k_fill_tkey<<<grid, 256, 0, st>>>(g.t.ptr, nt, tkey);
-    if (m > 0) k_local_flags<<<grid_for(h, m), 256, 0, st>>>(tkey, g.t.src, m, n, lflag);
-    count_launch(2);
-    exclusive_scan_i64(lflag, L, m, st);
-    DI_CUDA(cudaFreeAsync(lflag, st));
-    k_counts_from_scan<<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, L, nt, lc, rc);
+    count_launch();
+    // local rank of every CSC position among its target's local in-edges: a scan of
+    // local flags (32-bit through CUB when m < 2^31, else 64-bit)
+    const bool l32 = m < (int64_t)0x7fffffff;
+    void *L = nullptr;
+    {
+        const size_t ls = l32 ? sizeof(uint32_t) : sizeof(int64_t);
+        void *lflag = nullptr;
+        DI_CUDA(cudaMallocAsync(&lflag, (m + 1) * ls, st));
+        DI_CUDA(cudaMallocAsync(&L, (m + 1) * ls, st));
+        if (l32) {
+            k_local_flags<uint32_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (uint32_t *)lflag);
+            size_t tb = 0;
+            DI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (uint32_t *)lflag, (uint32_t *)L, (int)(m + 1), st));
+            DI_CUDA(cub::DeviceScan::ExclusiveSum(cub_scratch(h->device, tb), tb, (uint32_t *)lflag, (uint32_t *)L,
+                                                  (int)(m + 1), st));
+            k_counts_from_scan<uint32_t><<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, (const uint32_t *)L, nt, lc, rc);
+        } else {
+            k_local_flags<int64_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (int64_t *)lflag);
+            exclusive_scan_i64((const int64_t *)lflag, (int64_t *)L, m, st);
+            k_counts_from_scan<int64_t><<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, (const int64_t *)L, nt, lc, rc);
+        }
+        count_launch(2);
+        DI_CUDA(cudaFreeAsync(lflag, st));
+    }
     k_classify<<<grid_for(h, tp.ntile), 256, 0, st>>>(rc, n, tp.ntile, lrc, hc, hflag);
     count_launch(2);
     if (nt > n) {
@@ -533,7 +580,7 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaMallocAsync(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t), st));
     k_tile_rel<<<grid_for(h, nt + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, nt, tp.ntile, tp.rrel, tp.hidx,
                                                     tp.deg, tp.rtile);
-    k_remote_share<W><<<grid, 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.waves, tp.wr);
+    k_remote_share<W><<<grid_for(h, n), 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.waves, tp.wr);
     count_launch(2);
     phase_mark(st, "tiles: node arrays");
     // ---- edges to their classes
@@ -544,12 +591,16 @@ static void build_tiles_t(di_graph *h) {
     uint32_t *k0, *v0, *k1, *v1, *hof, *hh;
     DI_CUDA(cudaMallocAsync(&htmp, mh1 * rs, st));
     for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
-    if (m > 0)
-        k_split_flat<W><<<grid_for(h, m), 256, 0, st>>>(g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, L, m, n, tp.ltile,
-                                                        tp.vofs, tp.vfirst, tp.plist, vcap, rptr, hptr, tp.hidx,
-                                                        tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
-                                                        (RemRec<W> *)tp.rrec,
-                                                        htmp, k0, v0, hof);
+    if (m > 0 && l32)
+        k_split_flat<W, uint32_t><<<grid_for(h, m), 256, 0, st>>>(
+            g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, (const uint32_t *)L, m, n, tp.ltile, tp.vofs, tp.vfirst,
+            tp.plist, vcap, rptr, hptr, tp.hidx, tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
+            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
+    else if (m > 0)
+        k_split_flat<W, int64_t><<<grid_for(h, m), 256, 0, st>>>(
+            g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, (const int64_t *)L, m, n, tp.ltile, tp.vofs, tp.vfirst,
+            tp.plist, vcap, rptr, hptr, tp.hidx, tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
+            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
     DI_CUDA(cudaFreeAsync(tkey, st));
     DI_CUDA(cudaFreeAsync(L, st));
     count_launch();
