@@ -169,6 +169,31 @@ __global__ void k_classify_ghosts(const int64_t *__restrict__ rc, int64_t n, int
 }
 
 // balanced sliced-ELL layout of a tile's local in-edges: CTA per tile
+// 512-thread block reductions for the layout kernel (fixed order: deterministic)
+__device__ __forceinline__ int64_t block_sum_512(int64_t v, int64_t *red) {
+    v = warp_sum(v);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t s = 0;
+    for (int w = 0; w < (int)kNodeTile / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+__device__ __forceinline__ int block_exscan_512(int v, int *sc) {
+    const int lane = (int)lane_id(), w = (int)(threadIdx.x >> 5);
+    int x = v;                                       // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sc[w] = x;
+    __syncthreads();
+    int base = 0;
+    for (int q = 0; q < w; ++q) base += sc[q];
+    __syncthreads();
+    return base + x - v;
+}
+
 __global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__restrict__ lc, int64_t n,
                                                                int64_t ntile, uint32_t *__restrict__ vofs,
                                                                uint16_t *__restrict__ vfirst,
@@ -178,27 +203,25 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__r
     __shared__ int32_t len_s[kVRows], lenr_s[kVRows];
     __shared__ uint16_t vf_s[kNodeTile + 1], rank_s[kVRows];
     __shared__ int s_V;
+    __shared__ int64_t s_red[kNodeTile / 32 + 1];
+    __shared__ int s_scan[kNodeTile / 32 + 1];
     const int k = threadIdx.x;
     for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
         const int64_t a0 = t * kNodeTile;
         const int nn = (int)min(kNodeTile, n - a0);
-        d_s[k] = k < nn ? lc[a0 + k] : 0;
-        __syncthreads();
-        if (k == 0) {
-            // cap: at most kVRows pieces (E / cap + nonzero rows <= kVRows)
-            int64_t E = 0, nz = 0;
-            for (int i = 0; i < (int)kNodeTile; ++i) {
-                E += d_s[i];
-                nz += d_s[i] > 0;
-            }
-            const int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
-            int V = 0;
-            for (int i = 0; i < (int)kNodeTile; ++i) {
-                vf_s[i] = (uint16_t)V;
-                for (int64_t b = 0; b < d_s[i]; b += cap) len_s[V++] = (int32_t)min(cap, d_s[i] - b);
-            }
-            vf_s[kNodeTile] = (uint16_t)V;
-            s_V = V;
+        const int64_t dk = k < nn ? lc[a0 + k] : 0;
+        d_s[k] = dk;
+        // cap: at most kVRows pieces (E / cap + nonzero rows <= kVRows); block sums
+        const int64_t E = block_sum_512(dk, s_red), nz = block_sum_512((int64_t)(dk > 0), s_red);
+        const int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
+        // node k's pieces: its slots in node order (exclusive scan of the piece counts)
+        const int np = (int)((dk + cap - 1) / cap);
+        const int first = block_exscan_512(np, s_scan);
+        vf_s[k] = (uint16_t)first;
+        for (int q = 0; q < np; ++q) len_s[first + q] = (int32_t)min(cap, dk - (int64_t)q * cap);
+        if (k == kNodeTile - 1) {
+            vf_s[kNodeTile] = (uint16_t)(first + np);
+            s_V = first + np;
             vcap[t] = (int32_t)cap;
         }
         __syncthreads();
