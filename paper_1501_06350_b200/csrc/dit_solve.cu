@@ -15,6 +15,8 @@
 // a chunk of sweeps can be enqueued (or graph-launched) without host syncs.
 #include "dit_internal.cuh"
 
+#include <cmath>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -556,6 +558,8 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
     if (h->g.n > 0) {
         launch_reduce(h, 1);
         int chunk = 2;
+        double r_prev = -1.0;
+        unsigned long long s_prev = 0;
         for (;;) {
             for (int k = 0; k < chunk; ++k) {
                 launch_sweep(h);
@@ -569,7 +573,20 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
                 launch_reduce_exact(h);
                 if (poll_done(h)) break;
             }
-            chunk = std::min(chunk * 2, 64);
+            // next chunk: the sweeps the residual's decay over the last chunk still
+            // needs to reach tol, plus one (doubling while no decay is measurable);
+            // fewer dead sweeps enqueued past convergence
+            const double r = s.ctrl_host->resid;
+            const unsigned long long sw = s.ctrl_host->sweeps;
+            int next = std::min(chunk * 2, 64);
+            if (r_prev > 0.0 && r > 0.0 && r < r_prev && sw > s_prev && tol > 0.0) {
+                const double rate = std::pow(r / r_prev, 1.0 / (double)(sw - s_prev));
+                const double need = std::log(tol / r) / std::log(rate);
+                if (std::isfinite(need)) next = (int)std::min(64.0, std::max(1.0, std::ceil(need) + 1.0));
+            }
+            r_prev = r;
+            s_prev = sw;
+            chunk = next;
         }
     } else {
         s.ctrl_host->done = 1;
