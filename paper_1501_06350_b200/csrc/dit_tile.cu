@@ -741,26 +741,12 @@ void build_tiles(di_graph *h) {
 // stripe; a target's first run sets, later stripes add: fixed order), then
 // the chunks of stripe s: CTA per chunk stages A(src) w of its edges in
 // shared memory, warp per segment sums (lane-strided + fixed butterfly).
-template <typename W>
-__global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restrict__ hrec,
-                                                      const int64_t *__restrict__ chunk_start,
-                                                      const int64_t *__restrict__ seg_start,
-                                                      const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
-                                                      const int32_t *__restrict__ run_h,
-                                                      const int64_t *__restrict__ run_seg, int64_t q0, int64_t q1,
-                                                      const double *__restrict__ A0, const double *__restrict__ A1,
-                                                      double *__restrict__ part, double *__restrict__ hsum,
-                                                      int wave, int waves, const Ctrl *__restrict__ ctrl, int force) {
-    __shared__ double vals[kHeavyChunk];
-    __shared__ int sbnd[kHeavyChunk + 1];
-    if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
-    const bool gather = ctrl->gather != 0;
-    if (force ? !gather : (!gather && wave == 0)) return;
-    // the previous sweep wrote A[(sweeps - 1) & 1], this sweep's earlier waves A[sweeps & 1]
-    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
-    const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
-    const unsigned w = threadIdx.x >> 5, lane = lane_id();
-    // fold the previous stripe's runs (lane per run; long runs by the whole warp)
+// fold the runs [q0, q1) of a finished stripe into hsum (lane per run; long runs
+// by the whole warp): a target's first run sets, later stripes add (fixed order)
+__device__ __forceinline__ void heavy_fold(int64_t q0, int64_t q1, const int32_t *__restrict__ run_h,
+                                           const int64_t *__restrict__ run_seg, const double *__restrict__ part,
+                                           double *__restrict__ hsum) {
+    const unsigned lane = lane_id();
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t base = q0 + gw * 32; base < q1; base += nw * 32) {
@@ -794,7 +780,19 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
             }
         }
     }
-    // this stripe's chunks: products and segment bounds staged in shared memory
+}
+
+// the chunks [c0, c1) of one stripe: CTA per chunk stages A(src) w of its edges in
+// shared memory, then one thread per short segment / one warp per long one sums it
+template <typename W>
+__device__ __forceinline__ void heavy_chunks(const RemRec<W> *__restrict__ hrec,
+                                             const int64_t *__restrict__ chunk_start,
+                                             const int64_t *__restrict__ seg_start,
+                                             const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
+                                             const double *__restrict__ Aprev, const double *__restrict__ Afresh,
+                                             bool gather, int wave, int waves, int force, double *__restrict__ part,
+                                             double *vals, int *sbnd) {
+    const unsigned w = threadIdx.x >> 5, lane = lane_id();
     for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
         const int64_t e0 = chunk_start[c];
         const int cnt = (int)(chunk_start[c + 1] - e0);
@@ -813,7 +811,6 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
             vals[k] = v;
         }
         __syncthreads();
-        // short segments: one thread each; long ones (>= 64 edges): the whole warp
         for (int q0 = (int)(w * 32); q0 < ns; q0 += kThreads) {
             const int q = q0 + (int)lane;
             int b = 0, e = 0;
@@ -839,6 +836,31 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
         }
         __syncthreads();
     }
+}
+
+// One launch per stripe s (and one more after the last): first the previous
+// stripe's runs are folded into hsum, then the chunks of stripe s.
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restrict__ hrec,
+                                                      const int64_t *__restrict__ chunk_start,
+                                                      const int64_t *__restrict__ seg_start,
+                                                      const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
+                                                      const int32_t *__restrict__ run_h,
+                                                      const int64_t *__restrict__ run_seg, int64_t q0, int64_t q1,
+                                                      const double *__restrict__ A0, const double *__restrict__ A1,
+                                                      double *__restrict__ part, double *__restrict__ hsum,
+                                                      int wave, int waves, const Ctrl *__restrict__ ctrl, int force) {
+    __shared__ double vals[kHeavyChunk];
+    __shared__ int sbnd[kHeavyChunk + 1];
+    if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
+    const bool gather = ctrl->gather != 0;
+    if (force ? !gather : (!gather && wave == 0)) return;
+    // the previous sweep wrote A[(sweeps - 1) & 1], this sweep's earlier waves A[sweeps & 1]
+    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
+    const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
+    heavy_fold(q0, q1, run_h, run_seg, part, hsum);
+    heavy_chunks<W>(hrec, chunk_start, seg_start, cfirst, c0, c1, Aprev, Afresh, gather, wave, waves, force, part,
+                    vals, sbnd);
 }
 
 // ---------------------------------------------------------------- tile kernel
