@@ -154,3 +154,33 @@ def test_nccl_world1(gpu):
         shards[0].close()
     finally:
         tdist.destroy_process_group()
+
+
+def test_lockstep_tiled_full_size_sampled(gpu):
+    # BASELINE configs[2] at full size (50M nodes, ~1B weighted edges) split over two
+    # lock-step shards, in the sharded bench's schedule (tiled, 4 local rounds, 2 waves
+    # per rank): converged to tol, and Eq. (12) H + F = F0 + d P H on sampled nodes
+    # (the oracle's float64 arithmetic over the global CSR)
+    from paper_1501_06350_b200 import _lib, dist
+    from tests.test_gpu import _config2_graph, _sampled_identity
+    spec = synth.CONFIGS[2]
+    g = _config2_graph()
+    bounds = dist.node_ranges(g.n, 2)
+    shards = [dist.CudaShard(g.n, lo, hi, g.row_ptr[lo:hi + 1] - g.row_ptr[lo],
+                             g.col[g.row_ptr[lo]:g.row_ptr[hi]], g.w[g.row_ptr[lo]:g.row_ptr[hi]],
+                             stream=torch.cuda.current_stream())
+              for lo, hi in zip(bounds[:-1], bounds[1:])]
+    coll = LockstepCollectives()
+    coll.plan(shards, bounds)
+    Hs, res = dist.solve(shards, coll, d=D, tol=spec.tol, variant=3, local_rounds=4)
+    assert all(r["converged"] for r in res)
+    F = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    H = torch.empty_like(F)
+    for s, lo, hi in zip(shards, bounds[:-1], bounds[1:]):
+        _lib.di_get_state(s.h, F[lo:hi], H[lo:hi])
+    F, H = F.cpu().numpy(), H.cpu().numpy()
+    assert np.abs(F).sum() <= spec.tol
+    assert np.array_equal(torch.cat(Hs).cpu().numpy(), H)
+    assert _sampled_identity(g, H, F, D, np.random.default_rng(2)) < 1e-15
+    for s in shards:
+        s.close()
