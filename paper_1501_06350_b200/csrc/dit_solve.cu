@@ -15,7 +15,9 @@
 // a chunk of sweeps can be enqueued (or graph-launched) without host syncs.
 #include "dit_internal.cuh"
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 
 #include <algorithm>
 #include <cstdlib>
@@ -551,12 +553,25 @@ static void set_l2_fetch() {
     if (e && *e) DI_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
 }
 
+// DIT_SOLVE_TIMING=1 (debug): host-side phase times of a solve (stream synchronised)
+static void solve_mark(cudaStream_t st, const char *name) {
+    static const bool on = getenv("DIT_SOLVE_TIMING") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[dit] solve %-22s %8.3f ms\n", name, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res) {
     State &s = h->s;
     set_l2_fetch();
+    solve_mark(h->stream, "init");
     prepare_call(h, tol, o, nullptr);
     if (h->g.n > 0) {
         launch_reduce(h, 1);
+        solve_mark(h->stream, "prepare + reduce");
         int chunk = 2;
         double r_prev = -1.0;
         unsigned long long s_prev = 0;
@@ -565,24 +580,32 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
                 launch_sweep(h);
                 launch_sweep_reduce(h);
             }
-            if (poll_done(h)) {
+            const bool dn = poll_done(h);
+            if (getenv("DIT_SOLVE_TIMING"))
+                fprintf(stderr, "[dit] chunk of %d: sweeps %llu resid %.3e done %d\n", chunk,
+                        (unsigned long long)s.ctrl_host->sweeps, s.ctrl_host->resid, (int)dn);
+            solve_mark(h->stream, "chunk");
+            if (dn) {
                 if (!s.tiled_call || !s.ctrl_host->gather) break;
                 // TILED: the last sweep's remote pushes are still pending in A;
                 // gather them into F and take the exact residual
                 launch_tile_flush(h);
                 launch_reduce_exact(h);
-                if (poll_done(h)) break;
+                const bool dn2 = poll_done(h);
+                solve_mark(h->stream, "flush");
+                if (dn2) break;
             }
             // next chunk: the sweeps the residual's decay over the last chunk still
-            // needs to reach tol, plus one (doubling while no decay is measurable);
-            // fewer dead sweeps enqueued past convergence
+            // needs to reach tol (doubling while no decay is measurable): a sweep
+            // enqueued past convergence costs more (~0.5 ms of early-exit launches)
+            // than one more poll when the estimate falls a sweep short
             const double r = s.ctrl_host->resid;
             const unsigned long long sw = s.ctrl_host->sweeps;
             int next = std::min(chunk * 2, 64);
             if (r_prev > 0.0 && r > 0.0 && r < r_prev && sw > s_prev && tol > 0.0) {
                 const double rate = std::pow(r / r_prev, 1.0 / (double)(sw - s_prev));
                 const double need = std::log(tol / r) / std::log(rate);
-                if (std::isfinite(need)) next = (int)std::min(64.0, std::max(1.0, std::ceil(need) + 1.0));
+                if (std::isfinite(need)) next = (int)std::min(64.0, std::max(1.0, std::ceil(need - 1e-3)));
             }
             r_prev = r;
             s_prev = sw;
@@ -592,6 +615,7 @@ void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res)
         s.ctrl_host->done = 1;
     }
     fill_result(h, o, tol, res);
+    solve_mark(h->stream, "result");
 }
 
 void write_H(di_graph *h, double factor, double *H_out, int mem) {

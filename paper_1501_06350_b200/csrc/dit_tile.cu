@@ -1215,7 +1215,9 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
             a.F[j] = f;
             if (D != 0.0) a.H[j] = Hs[i] + D;
             Anext[j] = An;
-            resid += fabs(f) + fabs(An) * (double)Ws[i];
+            // R13: the pushes still pending carry d D(i) P_{t,i} over the pending
+            // out-edges t, i.e. |d D(i)| wr(i) with wr(i) = inv(i) sum_pending w
+            resid += fabs(f) + fabs(d * D) * (double)Ws[i];
             if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
         }
         __syncthreads();                             // buffer b free for the bundle kNB-1 ahead

@@ -183,14 +183,14 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
         if any(done):
             raise RuntimeError("ranks disagree on convergence")
         # next chunk from the decay of the global residual (identical on every rank,
-        # so the ranks stay in lock step): the sweeps still needed to reach tol, + 1
+        # so the ranks stay in lock step): the sweeps still needed to reach tol
         r = float(shards[0].gstats[0].item())
         nxt = min(chunk * 2, max_chunk)
         if r_prev is not None and 0.0 < r < r_prev and tol > 0.0:
             rate = (r / r_prev) ** (1.0 / (swept - s_prev))
             need = math.log(tol / r) / math.log(rate)
             if math.isfinite(need):
-                nxt = int(min(max_chunk, max(1, math.ceil(need) + 1)))
+                nxt = int(min(max_chunk, max(1, math.ceil(need - 1e-3))))
         r_prev, s_prev, chunk = r, swept, nxt
     outs = [s.finish(tol, **opts) for s in shards]
     return [o[0] for o in outs], [o[1] for o in outs]
