@@ -69,8 +69,9 @@ static void reserve_pool(int device, int64_t n, int64_t m, cudaStream_t st) {
     uint64_t cur = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur);
     const uint64_t want = std::min<uint64_t>((uint64_t)(56 * (double)m + 256 * (double)n), (uint64_t)(0.6 * (double)fr));
+    if (want < ((uint64_t)1 << 30)) return;         // small graphs: a later big one may still reserve
     done[device] = true;
-    if (want <= cur || want < ((uint64_t)1 << 30)) return;
+    if (want <= cur) return;
     void *p = nullptr;
     if (cudaMallocAsync(&p, want, st) != cudaSuccess) {
         cudaGetLastError();
