@@ -254,8 +254,8 @@ def test_config1_full_size(eng):
     spec = synth.CONFIGS[1]
     g = synth.generate(spec)
     r = oracle_solve(g, tol=1e-12)
-    for variant in ("push", "auto", "tiled"):
-        G, H, res = gpu_solve(eng, g, tol=1e-12, variant=variant, local_rounds=3)
+    for variant, rounds in (("push", 4), ("auto", 4), ("tiled", 3), ("tiled", 4)):
+        G, H, res = gpu_solve(eng, g, tol=1e-12, variant=variant, local_rounds=rounds)
         assert res["converged"]
         assert np.abs(H - r.H).sum() <= L1_BAR
         assert_topk(H, r.H, 1000, 2 * (res["bound"] + r.residual / (1 - D)))
