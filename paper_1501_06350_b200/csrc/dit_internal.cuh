@@ -84,7 +84,7 @@ struct PullPlan {
 // records would overflow kLightCap) are gathered by k_heavy over fixed chunks
 // of the heavy edge array (segments = target ∩ chunk), deterministic.
 #ifndef DIT_LIGHT_CAP
-#define DIT_LIGHT_CAP 2048
+#define DIT_LIGHT_CAP 1344
 #endif
 constexpr int64_t kLightCap = DIT_LIGHT_CAP;   // light remote records per tile (shared memory)
 #ifndef DIT_HEAVY_TH
