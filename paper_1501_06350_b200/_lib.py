@@ -35,7 +35,8 @@ SHARD_TILED_FALLBACK = "pull"
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",
-           "di_kernel_launches", "di_profile_enable", "di_profile_get", "di_sweep_history", "di_plan_stats"]
+           "di_kernel_launches", "di_profile_enable", "di_profile_get", "di_sweep_history", "di_plan_stats",
+           "di_release_memory"]
 
 
 class di_profile(ctypes.Structure):
@@ -83,6 +84,7 @@ _lib.di_profile_enable.argtypes = [_P, _I32]
 _lib.di_profile_get.argtypes = [_P, ctypes.POINTER(di_profile)]
 _lib.di_sweep_history.argtypes = [_P, _I64, _P, _P, _P, _P, ctypes.POINTER(_I64)]
 _lib.di_plan_stats.argtypes = [_P, _P, ctypes.c_int32]
+_lib.di_release_memory.argtypes = [_I32]
 _lib.di_last_error.restype = ctypes.c_char_p
 _lib.di_kernel_launches.restype = _I64
 for _name in EXPORTS:
@@ -147,6 +149,11 @@ def di_last_error():
 
 def di_kernel_launches():
     return int(_lib.di_kernel_launches())
+
+
+def di_release_memory(device=0):
+    """Return the engine's cached device memory (pool, sort scratch) to the driver."""
+    _check(_lib.di_release_memory(device))
 
 
 def di_graph_create(n, row_ptr, col, weights=None, device=0, stream=None):

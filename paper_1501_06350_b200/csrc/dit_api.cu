@@ -59,8 +59,10 @@ static void keep_pool_memory(int device) {
 // per edge + 256 B per node, at most 60% of the free memory): the builders then
 // carve their temporaries out of one mapped chunk instead of growing the pool
 // piecemeal (which costs ~0.1 s of mapping whenever fragmentation forces it).
+static bool g_reserved[64] = {};   // reserve_pool done (reset by di_release_memory)
+
 static void reserve_pool(int device, int64_t n, int64_t m, cudaStream_t st) {
-    static bool done[64] = {};
+    bool *done = g_reserved;
     if (device < 0 || device >= 64 || done[device] || getenv("DIT_NO_POOL_RESERVE")) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
@@ -120,6 +122,18 @@ void di_solve_opts_default(di_solve_opts *o) {
 const char *di_last_error(void) { return t_err.c_str(); }
 
 int64_t di_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+int di_release_memory(int32_t device) {
+    return guarded([&] {
+        DI_CUDA(cudaSetDevice(device));
+        DI_CUDA(cudaDeviceSynchronize());
+        release_cub_scratch(device);
+        if (device >= 0 && device < 64) g_reserved[device] = false;
+        cudaMemPool_t pool;
+        DI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        DI_CUDA(cudaMemPoolTrimTo(pool, 0));
+    });
+}
 
 int di_graph_create(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col, const void *weights,
                     int32_t w_dtype, int32_t mem, int32_t device, void *stream, di_graph **out) {

@@ -236,6 +236,7 @@ void free_tiles(TilePlan &t);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
 void *cub_scratch(int device, size_t bytes);   // dit_pull.cu: CUB scratch cached per device
+void release_cub_scratch(int device);
 void launch_tile_heavy(di_graph *h, int force, int wave = 0);
 void launch_tile_kernel(di_graph *h, int rounds, int wave = 0);
 int tile_waves(const di_graph *h);

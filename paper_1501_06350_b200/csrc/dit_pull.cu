@@ -286,9 +286,19 @@ __global__ void k_unpack_t(const unsigned long long *__restrict__ vals, int64_t 
 // outside the stream-ordered pool so the builders' temporaries keep a stable
 // layout there; a cudaMalloc / cudaFree pair per build cost up to 0.6 s when the
 // driver had to make room).
+static void *g_cub_buf[64] = {};
+static size_t g_cub_cap[64] = {};
+
+void release_cub_scratch(int device) {
+    if (device < 0 || device >= 64 || !g_cub_buf[device]) return;
+    cudaFree(g_cub_buf[device]);
+    g_cub_buf[device] = nullptr;
+    g_cub_cap[device] = 0;
+}
+
 void *cub_scratch(int device, size_t bytes) {
-    static void *buf[64] = {};
-    static size_t cap[64] = {};
+    void **buf = g_cub_buf;
+    size_t *cap = g_cub_cap;
     if (device < 0 || device >= 64) device = 0;
     if (bytes > cap[device]) {
         if (buf[device]) DI_CUDA(cudaFree(buf[device]));

@@ -353,3 +353,20 @@ def test_config2_full_size_sampled(eng, variant):
     assert _sampled_identity(g, H2, F, D, np.random.default_rng(0)) < 1e-15
     # Theorem 1 through Eq. (12): sum H = (|F0| - |F| - l)/(1-d) for nonnegative F
     assert H2.sum() == pytest.approx((1 - D - F.sum() - D * leak) / (1 - D), abs=1e-9)
+
+
+def test_release_memory_then_rebuild(eng):
+    # the cached pool / sort scratch go back to the driver; a later graph builds and
+    # solves as before (configs[1] at full size, tiled)
+    from paper_1501_06350_b200 import _lib
+    spec = synth.CONFIGS[1]
+    g = synth.generate(spec)
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    H1, r1 = G.solve(d=D, tol=spec.tol, variant="tiled")
+    H1 = H1.cpu().numpy()
+    G.close()
+    _lib.di_release_memory(0)
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    H2, r2 = G.solve(d=D, tol=spec.tol, variant="tiled")
+    assert np.array_equal(H1, H2.cpu().numpy()) and r1["sweeps"] == r2["sweeps"]
+    G.close()
