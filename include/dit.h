@@ -294,7 +294,7 @@ int64_t di_kernel_launches(void);
  * Give the device memory the library keeps cached back to the driver.  The
  * engine allocates from the device's stream-ordered default pool with an
  * unlimited release threshold, reserves it once for the plan builder's peak
- * (about 56 B per edge + 256 B per node) and keeps CUB's sort scratch:
+ * (about 64 B per edge + 256 B per node) and keeps CUB's sort scratch:
  * repeated graph builds then reuse mapped memory.  Call this (with no
  * solve running on the device) when other allocators in the process need
  * that memory.  device: CUDA ordinal.  Returns DI_OK or DI_ERR_CUDA.

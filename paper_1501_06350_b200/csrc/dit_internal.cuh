@@ -74,6 +74,8 @@ struct PullPlan {
     double *pbuf = nullptr;        // [npieces] partial sums of split targets
     int64_t *tile_start = nullptr; // [ntiles+1] first piece of each 2048-edge tile
     int64_t ntiles = 0;
+    uint32_t *tkey = nullptr;      // [m] target of each in-edge (the sort's keys), kept for the
+                                   // tile plan's build and freed by it
 };
 
 // Tile-local schedule (R12, §5): node tiles of kNodeTile ids.  An

@@ -215,6 +215,10 @@ std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uin
 // Work plan of a CSC (pieces, tiles, split-target fixups) for k_pull.
 void build_plan_pieces(di_graph *h, PullPlan &pd) {
     cudaStream_t st = h->stream;
+    if (pd.tkey && h->g.tl.built) {                  // the tile plan is built: nobody needs the keys
+        DI_CUDA(cudaFreeAsync(pd.tkey, st));
+        pd.tkey = nullptr;
+    }
     const int64_t nt = pd.nt, m = pd.m;
     int64_t *pc, *po;
     DI_CUDA(cudaMallocAsync(&pc, (nt + 1) * sizeof(int64_t), st));
@@ -260,6 +264,7 @@ void free_plan(PullPlan &p) {
     cudaFree(p.fix);
     cudaFree(p.pbuf);
     cudaFree(p.tile_start);
+    cudaFree(p.tkey);
     p = PullPlan();
 }
 
@@ -341,7 +346,8 @@ static void build_transpose_packed(di_graph *h, int64_t *cnt) {
     k_run_bounds<<<grid, kThreads, 0, st>>>(kb.Current(), m, cnt);
     k_unpack_t<<<grid, kThreads, 0, st>>>(vb.Current(), m, T.src, (float *)T.w);
     count_launch(2);
-    for (uint32_t *p : {k0, k1}) DI_CUDA(cudaFreeAsync(p, st));
+    T.tkey = kb.Current();                  // the tile plan reads the sorted keys (and frees them)
+    DI_CUDA(cudaFreeAsync(kb.Alternate(), st));
     for (unsigned long long *p : {v0, v1}) DI_CUDA(cudaFreeAsync(p, st));
 }
 

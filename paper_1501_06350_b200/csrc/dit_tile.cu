@@ -527,10 +527,13 @@ static void build_tiles_t(di_graph *h) {
     for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
         DI_CUDA(cudaMallocAsync(p, (nt + 1) * sizeof(int64_t), st));
     const int64_t m = g.m;
-    uint32_t *tkey = nullptr;
-    DI_CUDA(cudaMallocAsync(&tkey, (m > 0 ? m : 1) * sizeof(uint32_t), st));
-    k_fill_tkey<<<grid, 256, 0, st>>>(g.t.ptr, nt, tkey);
-    count_launch();
+    uint32_t *tkey = g.t.tkey;                       // the transpose's sorted keys when it kept them
+    g.t.tkey = nullptr;
+    if (!tkey) {
+        DI_CUDA(cudaMallocAsync(&tkey, (m > 0 ? m : 1) * sizeof(uint32_t), st));
+        k_fill_tkey<<<grid, 256, 0, st>>>(g.t.ptr, nt, tkey);
+        count_launch();
+    }
     // local rank of every CSC position among its target's local in-edges: a scan of
     // local flags (32-bit through CUB when m < 2^31, else 64-bit)
     const bool l32 = m < (int64_t)0x7fffffff;
