@@ -294,7 +294,8 @@ int64_t di_kernel_launches(void);
  * Give the device memory the library keeps cached back to the driver.  The
  * engine allocates from the device's stream-ordered default pool with an
  * unlimited release threshold, reserves it once for the plan builder's peak
- * (about 64 B per edge + 256 B per node) and keeps CUB's sort scratch:
+ * (about 40 B per edge + 256 B per node) and keeps the transpose's sort
+ * buffers (24 B per edge) and CUB's scratch outside the pool:
  * repeated graph builds then reuse mapped memory.  Call this (with no
  * solve running on the device) when other allocators in the process need
  * that memory.  device: CUDA ordinal.  Returns DI_OK or DI_ERR_CUDA.

@@ -55,7 +55,7 @@ static void keep_pool_memory(int device) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
-// One up-front reservation of the pool for the graph builder's peak (about 64 B
+// One up-front reservation of the pool for the graph builder's peak (about 40 B
 // per edge + 256 B per node, at most 60% of the free memory): the builders then
 // carve their temporaries out of one mapped chunk instead of growing the pool
 // piecemeal (which costs ~0.1 s of mapping whenever fragmentation forces it).
@@ -70,7 +70,7 @@ static void reserve_pool(int device, int64_t n, int64_t m, cudaStream_t st) {
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return;
     uint64_t cur = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur);
-    const uint64_t want = std::min<uint64_t>((uint64_t)(64 * (double)m + 256 * (double)n), (uint64_t)(0.6 * (double)fr));
+    const uint64_t want = std::min<uint64_t>((uint64_t)(40 * (double)m + 256 * (double)n), (uint64_t)(0.6 * (double)fr));
     if (want < ((uint64_t)1 << 30)) return;         // small graphs: a later big one may still reserve
     done[device] = true;
     if (want <= cur) return;

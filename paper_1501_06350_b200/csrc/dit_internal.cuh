@@ -2,6 +2,7 @@
 // The C ABI is include/dit.h; DESIGN.md describes the data layout and kernels.
 #pragma once
 
+#include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -239,6 +240,7 @@ void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
 void *cub_scratch(int device, size_t bytes);   // dit_pull.cu: CUB scratch cached per device
 void release_cub_scratch(int device);
+std::mutex &scratch_mutex(int device);         // builds on one device take turns on the cached scratch
 void launch_tile_heavy(di_graph *h, int force, int wave = 0);
 void launch_tile_kernel(di_graph *h, int rounds, int wave = 0);
 int tile_waves(const di_graph *h);

@@ -13,6 +13,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdlib>
+#include <mutex>
 
 #include <utility>
 
@@ -291,19 +292,22 @@ __global__ void k_unpack_t(const unsigned long long *__restrict__ vals, int64_t 
 // outside the stream-ordered pool so the builders' temporaries keep a stable
 // layout there; a cudaMalloc / cudaFree pair per build cost up to 0.6 s when the
 // driver had to make room).
-static void *g_cub_buf[64] = {};
-static size_t g_cub_cap[64] = {};
+// slot 0: CUB scratch; slot 1: the packed transpose's sort buffers
+static void *g_cub_buf[2][64] = {};
+static size_t g_cub_cap[2][64] = {};
 
 void release_cub_scratch(int device) {
-    if (device < 0 || device >= 64 || !g_cub_buf[device]) return;
-    cudaFree(g_cub_buf[device]);
-    g_cub_buf[device] = nullptr;
-    g_cub_cap[device] = 0;
+    if (device < 0 || device >= 64) return;
+    for (int sl = 0; sl < 2; ++sl) {
+        if (g_cub_buf[sl][device]) cudaFree(g_cub_buf[sl][device]);
+        g_cub_buf[sl][device] = nullptr;
+        g_cub_cap[sl][device] = 0;
+    }
 }
 
-void *cub_scratch(int device, size_t bytes) {
-    void **buf = g_cub_buf;
-    size_t *cap = g_cub_cap;
+static void *cached_scratch(int slot, int device, size_t bytes) {
+    void **buf = g_cub_buf[slot];
+    size_t *cap = g_cub_cap[slot];
     if (device < 0 || device >= 64) device = 0;
     if (bytes > cap[device]) {
         if (buf[device]) DI_CUDA(cudaFree(buf[device]));
@@ -315,6 +319,13 @@ void *cub_scratch(int device, size_t bytes) {
     return buf[device];
 }
 
+void *cub_scratch(int device, size_t bytes) { return cached_scratch(0, device, bytes); }
+
+std::mutex &scratch_mutex(int device) {
+    static std::mutex mu[64];
+    return mu[(device >= 0 && device < 64) ? device : 0];
+}
+
 // Transpose with the sources and f32 weights riding in the sort (CUB, m < 2^31):
 // no gather through the permutation afterwards.
 static void build_transpose_packed(di_graph *h, int64_t *cnt) {
@@ -323,18 +334,19 @@ static void build_transpose_packed(di_graph *h, int64_t *cnt) {
     cudaStream_t st = h->stream;
     const int64_t n = g.n, m = g.m, nt = g.nt;
     const int grid = h->num_sms * 8;
-    uint32_t *k0, *k1;
-    unsigned long long *v0, *v1;
-    int32_t *esrc;
-    DI_CUDA(cudaMallocAsync(&esrc, m * 4, st));
+    // the four sort buffers: one block cached per device outside the pool (a 24 GB
+    // request at configs[2]; from the pool it sometimes cost 20-50 ms of mapping).
+    // Builds on one device take turns on it (and on the CUB scratch).
+    const size_t mv = ((size_t)m * 8 + 255) & ~(size_t)255, mk = ((size_t)m * 4 + 255) & ~(size_t)255;
+    std::lock_guard<std::mutex> lock(scratch_mutex(h->device));
+    unsigned char *blk = (unsigned char *)cached_scratch(1, h->device, 2 * mv + 2 * mk);
+    unsigned long long *v0 = (unsigned long long *)blk, *v1 = (unsigned long long *)(blk + mv);
+    uint32_t *k0 = (uint32_t *)(blk + 2 * mv), *k1 = (uint32_t *)(blk + 2 * mv + mk);
+    int32_t *esrc = (int32_t *)k1;                   // the second key buffer is free until the sort
     k_edge_src<<<grid, kThreads, 0, st>>>(g.row_ptr, n, esrc);
-    DI_CUDA(cudaMallocAsync(&k0, m * 4, st));
-    DI_CUDA(cudaMallocAsync(&v0, m * 8, st));
     k_pack_keys<<<grid, kThreads, 0, st>>>(g.col, esrc, (const float *)g.w, m, k0, v0);
     count_launch(2);
-    DI_CUDA(cudaFreeAsync(esrc, st));
-    DI_CUDA(cudaMallocAsync(&k1, m * 4, st));
-    DI_CUDA(cudaMallocAsync(&v1, m * 8, st));
+    phase_mark(st, "transpose: pack");
     int bits = 1;
     while (bits < 31 && ((int64_t)1 << bits) < nt) ++bits;
     cub::DoubleBuffer<uint32_t> kb(k0, k1);
@@ -346,9 +358,10 @@ static void build_transpose_packed(di_graph *h, int64_t *cnt) {
     k_run_bounds<<<grid, kThreads, 0, st>>>(kb.Current(), m, cnt);
     k_unpack_t<<<grid, kThreads, 0, st>>>(vb.Current(), m, T.src, (float *)T.w);
     count_launch(2);
-    T.tkey = kb.Current();                  // the tile plan reads the sorted keys (and frees them)
-    DI_CUDA(cudaFreeAsync(kb.Alternate(), st));
-    for (unsigned long long *p : {v0, v1}) DI_CUDA(cudaFreeAsync(p, st));
+    // the tile plan reads the sorted keys (and frees them): copy them out of the block
+    DI_CUDA(cudaMallocAsync(&T.tkey, (size_t)m * 4, st));
+    DI_CUDA(cudaMemcpyAsync(T.tkey, kb.Current(), (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
+    DI_CUDA(cudaStreamSynchronize(st));              // the block is free for the next build
 }
 
 void build_transpose(di_graph *h) {
@@ -391,8 +404,12 @@ void build_transpose(di_graph *h) {
             cub::DoubleBuffer<uint32_t> vb((uint32_t *)v0, (uint32_t *)v1);
             size_t tmp_bytes = 0;
             DI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int)m, 0, bits, st));
-            DI_CUDA(cub::DeviceRadixSort::SortPairs(cub_scratch(h->device, tmp_bytes), tmp_bytes, kb, vb, (int)m, 0,
-                                                    bits, st));
+            {
+                std::lock_guard<std::mutex> lock(scratch_mutex(h->device));
+                DI_CUDA(cub::DeviceRadixSort::SortPairs(cub_scratch(h->device, tmp_bytes), tmp_bytes, kb, vb, (int)m,
+                                                        0, bits, st));
+                DI_CUDA(cudaStreamSynchronize(st));
+            }
             if (kb.Current() != k0) {
                 std::swap(k0, k1);
                 std::swap(v0, v1);

@@ -547,8 +547,12 @@ static void build_tiles_t(di_graph *h) {
             k_local_flags<uint32_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (uint32_t *)lflag);
             size_t tb = 0;
             DI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (uint32_t *)lflag, (uint32_t *)L, (int)(m + 1), st));
-            DI_CUDA(cub::DeviceScan::ExclusiveSum(cub_scratch(h->device, tb), tb, (uint32_t *)lflag, (uint32_t *)L,
-                                                  (int)(m + 1), st));
+            {
+                std::lock_guard<std::mutex> lock(scratch_mutex(h->device));
+                DI_CUDA(cub::DeviceScan::ExclusiveSum(cub_scratch(h->device, tb), tb, (uint32_t *)lflag, (uint32_t *)L,
+                                                      (int)(m + 1), st));
+                DI_CUDA(cudaStreamSynchronize(st));
+            }
             k_counts_from_scan<uint32_t><<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, (const uint32_t *)L, nt, lc, rc);
         } else {
             k_local_flags<int64_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (int64_t *)lflag);
