@@ -156,16 +156,17 @@ def test_nccl_world1(gpu):
         tdist.destroy_process_group()
 
 
-def test_lockstep_tiled_full_size_sampled(gpu):
-    # BASELINE configs[2] at full size (50M nodes, ~1B weighted edges) split over two
-    # lock-step shards, in the sharded bench's schedule (tiled, 4 local rounds, 2 waves
+@pytest.mark.parametrize("world", [2, 4])
+def test_lockstep_tiled_full_size_sampled(gpu, world):
+    # BASELINE configs[2] at full size (50M nodes, ~1B weighted edges) split over
+    # `world` lock-step shards, in the sharded bench's schedule (tiled, 4 local rounds, 2 waves
     # per rank): converged to tol, and Eq. (12) H + F = F0 + d P H on sampled nodes
     # (the oracle's float64 arithmetic over the global CSR)
     from paper_1501_06350_b200 import _lib, dist
     from tests.test_gpu import _config2_graph, _sampled_identity
     spec = synth.CONFIGS[2]
     g = _config2_graph()
-    bounds = dist.node_ranges(g.n, 2)
+    bounds = dist.node_ranges(g.n, world)
     shards = [dist.CudaShard(g.n, lo, hi, g.row_ptr[lo:hi + 1] - g.row_ptr[lo],
                              g.col[g.row_ptr[lo]:g.row_ptr[hi]], g.w[g.row_ptr[lo]:g.row_ptr[hi]],
                              stream=torch.cuda.current_stream())
