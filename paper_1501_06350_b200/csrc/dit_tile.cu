@@ -17,8 +17,8 @@
 // Step 1 of sweep k+1 completes the remote pushes of sweep k, so the sequence
 // of Eq. (8) updates is exactly the oracle's (orc_tiled_sweep_run: rounds in
 // every tile, then the remote pushes).  The stop test after sweep k uses
-// |F|_1 = sum_t |f_t| + sum_i |d D(i) inv(i)| wr(i) (wr = share of i's out-weight
-// that leaves its tile): exact for non-negative fluid, an upper bound for
+// |F|_1 = sum_t |f_t| + sum_i |d D(i)| wr(i) (wr = share of i's out-weight whose
+// pushes are still pending): exact for non-negative fluid, an upper bound for
 // signed fluid (§3.5), so stopping on it keeps Theorem 1's guarantee; after the
 // last sweep the pending pushes are flushed into F and the exact |F|_1 taken.
 //
@@ -30,9 +30,11 @@
 // (a random 8-byte read from HBM costs a 64-byte DRAM access on B200).
 //
 // Kernels (B200): k_tile -- one 512-thread CTA per tile, 2 CTAs per SM; the
-// tile's light records and its local edges (sliced-ELL, coalesced across the
-// warp) staged by TMA bulk copies (cp.async.bulk + mbarrier) while the
-// per-node state streams into registers.  k_heavy_s -- per stripe: CTA per
+// tile's per-node state, piece layout and light records staged by TMA bulk
+// copies (cp.async.bulk + mbarrier, double-buffered), its local edges
+// (sliced-ELL, runs of four slots per lane) prefetched into L2 and read
+// through L1 by the rounds (staged in shared memory too with one 1024-thread
+// CTA per SM, DIT_TILE_BLOCK=1024).  k_heavy_s -- per stripe: CTA per
 // 2048-edge chunk, warp per segment; then the stripe's runs folded into
 // hsum in stripe order.  Every summation has a fixed order: bitwise
 // reproducible run to run.
