@@ -22,7 +22,7 @@ INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", f"-I{INCLUDE}"]
+         "--expt-relaxed-constexpr", f"-I{INCLUDE}"] + os.environ.get("DIT_NVCC_FLAGS", "").split()
 
 
 def _deps():

@@ -147,8 +147,7 @@ struct TilePlan {
     double *part = nullptr;        // [nseg] segment partial sums
     double *hsum = nullptr;        // [nh] remote inflow of each heavy target
     int64_t max_tile_edges = 0;    // most local in-edges of one tile
-    int64_t edge_cap = 0;          // k_tile launch configuration (set on first launch)
-    size_t tile_smem = 0;
+    int32_t *lstage = nullptr;     // [ntile] first slot (relative to ltile) that k_tile stages in shared memory
 };
 
 // Per-node weight-scale storage and raw weights.

@@ -47,21 +47,22 @@
 
 namespace dit {
 
-constexpr int kTileThreads = (int)kNodeTile;     // thread i owns node i of the tile
+constexpr int kTileThreads = (int)kNodeTile;     // build kernels: thread i owns node i of the tile
+// k_tile: one 1024-thread CTA per SM, 16 round warps (thread i owns node i) and
+// 16 prep warps (the next tile's inflow)
+constexpr int kRW = (int)kNodeTile;
+constexpr int kPWt = (int)kNodeTile / 2;           // two nodes per prep thread
+constexpr int kPN = (int)kNodeTile / kPWt;
+constexpr int kTileBlock = kRW + kPWt;
 constexpr int kTileWarps = kTileThreads / 32;
-// k_tile launch shape: 1024 threads (32 warps, one per virtual warp of pieces)
-// and one CTA per SM, or 512 threads (two virtual warps each) and two per SM
-#ifndef DIT_TILE_BLOCK
-#define DIT_TILE_BLOCK 512
-#endif
-constexpr int kTileBlock = DIT_TILE_BLOCK;
-constexpr int kTileBlocksPerSM = kTileBlock == 1024 ? 1 : 2;
-constexpr int kTileBlockWarps = kTileBlock / 32;
 constexpr int kVRows = 2 * (int)kNodeTile;       // local-edge pieces per tile (at most)
-constexpr int kVWarps = kVRows / 32;             // virtual warps: real warp w runs w and kVWarps-1-w
+constexpr int kVWarps = kVRows / 32;             // virtual warps: round warp w runs w and kVWarps-1-w
 constexpr int kVofsStride = 36;                  // u32 per tile (kVWarps + 1, padded to 16 B)
 constexpr int kVfStride = 520;                   // u16 per tile (kNodeTile + 1, padded to 16 B)
-static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per warp");
+constexpr int kMetaBytes = kVofsStride * 4 + kVfStride * 2 + kVRows * 2;   // per-tile layout, TMA-staged
+constexpr int64_t kGqSlots = kNodeTile + 16;     // outflow per node + one zero slot per bank pair (ELL padding)
+constexpr int kTileSmemBudget = 227 * 1024 - 2048;   // dynamic shared memory of k_tile (static arrays aside)
+static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per round warp");
 
 template <typename W>
 using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
@@ -93,6 +94,28 @@ struct RemRec<double> {
 };
 template <typename W>
 __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w; }
+
+// Shared memory of k_tile (one CTA per SM, everything double-buffered by tile
+// parity): gq / psum of the rounds, the prepared per-node rows P, the light
+// records R (prep warps) and the edge bundles E = {layout, staged slots} (round warps).
+struct PrepRow {
+    double f, ivi, H;        // inflow-completed fluid, 1/sum w, history
+    float wr;                // pending share of the out-weight (R13)
+    int32_t deg;             // out-degree
+};
+static_assert(sizeof(PrepRow) == 32, "32-byte prepared rows");
+constexpr int kOffPsum = ((int)kGqSlots * 8 + 127) & ~127;
+constexpr int kOffP = kOffPsum + kVRows * 8;
+constexpr int kOffR = kOffP + 2 * (int)kNodeTile * (int)sizeof(PrepRow);
+template <typename W>
+constexpr int tile_rec_buf() { return (((int)kLightCap * (int)sizeof(RemRec<W>) + 32) + 127) & ~127; }
+template <typename W>
+constexpr int tile_off_e() { return kOffR + 2 * tile_rec_buf<W>(); }
+template <typename W>
+constexpr int tile_e_buf() { return ((kTileSmemBudget - tile_off_e<W>()) / 2) & ~127; }
+template <typename W>
+constexpr int tile_smem_bytes() { return tile_off_e<W>() + 2 * tile_e_buf<W>(); }
+static_assert(kOffP % 16 == 0 && kOffR % 128 == 0 && kMetaBytes % 16 == 0, "aligned shared buffers");
 
 #ifndef DIT_STRIPE_MB
 #define DIT_STRIPE_MB 48
@@ -126,8 +149,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
 }
 // bounded wait: a byte-count mismatch becomes a trap (an error), never a hung GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin)
+    for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin) {
+        if (spin > 8) __nanosleep(64);               // long waits: leave the issue slots to others
         if (spin > (1ll << 26)) __trap();
+    }
 }
 // bulk global -> shared copy (the TMA engine), completion counted on `bar`
 __device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
@@ -197,10 +222,11 @@ __device__ __forceinline__ int block_exscan_512(int v, int *sc) {
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__restrict__ lc, int64_t n,
-                                                               int64_t ntile, uint32_t *__restrict__ vofs,
+                                                               int64_t ntile, int eb, int64_t stage_cap,
+                                                               uint32_t *__restrict__ vofs,
                                                                uint16_t *__restrict__ vfirst,
                                                                uint16_t *__restrict__ plist, int32_t *__restrict__ vcap,
-                                                               int64_t *__restrict__ pcnt) {
+                                                               int64_t *__restrict__ pcnt, int32_t *__restrict__ lstage) {
     __shared__ int64_t d_s[kNodeTile];
     __shared__ int32_t len_s[kVRows], lenr_s[kVRows];
     __shared__ uint16_t vf_s[kNodeTile + 1], rank_s[kVRows];
@@ -249,6 +275,11 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__r
             }
             for (int vw = kVWarps; vw < kVofsStride; ++vw) vofs[t * kVofsStride + vw] = off;
             pcnt[t] = off;
+            // shared-memory staging (k_tile): the longest suffix of virtual warps whose
+            // slots (eb bytes each) fit the edge buffer; the others are read from L2
+            int v = 0;
+            while (v < kVWarps && (int64_t)(off - vofs[t * kVofsStride + v]) * eb > stage_cap) ++v;
+            lstage[t] = (int32_t)(v < kVWarps ? vofs[t * kVofsStride + v] : off);
         }
         __syncthreads();
     }
@@ -466,6 +497,122 @@ __global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_
     }
 }
 
+// Bank-aware slot order: the rounds gather gq[src] for 32
+// pieces at once, one slot row per load; a 64-bit shared load is served per
+// half-warp, one wavefront per distinct bank pair (src mod 16) hit twice.  The
+// order of a piece's slots is free (any fixed order is a valid summation
+// order, R14), so each virtual warp's rows are refilled greedily: per row, the
+// lanes of a half-warp claim distinct bank pairs, the most frequent remaining
+// ones first; padding slots (zero outflow) take a free pair.  One warp per
+// virtual warp of <= kBalMaxK slots per lane (longer ones keep edge order).
+constexpr int kBalMaxK = 32, kBalWarps = 4;
+template <typename W>
+__global__ void __launch_bounds__(kBalWarps * 32) k_ell_balance(const int64_t *__restrict__ ltile,
+                                                                const uint32_t *__restrict__ vofs, int64_t ntile,
+                                                                uint16_t *__restrict__ lsrc,
+                                                                StoreW<W> *__restrict__ lw) {
+    constexpr bool kW = !std::is_same<W, NoW>::value;
+    __shared__ uint16_t es[kBalWarps][kBalMaxK][32];
+    __shared__ StoreW<W> ew[kBalWarps][kW ? kBalMaxK : 1][32];
+    __shared__ uint8_t ord[kBalWarps][kBalMaxK][32];
+    __shared__ int cnt[kBalWarps][2][16];
+    const int wb = threadIdx.x >> 5, lane = lane_id(), half = lane >> 4;
+    const int64_t nitem = ntile * kVWarps;
+    for (int64_t item = (int64_t)blockIdx.x * kBalWarps + wb; item < nitem; item += (int64_t)gridDim.x * kBalWarps) {
+        const int64_t tile = item / kVWarps;
+        const int vw = (int)(item % kVWarps);
+        const uint32_t o0 = vofs[tile * kVofsStride + vw];
+        const int K = (int)((vofs[tile * kVofsStride + vw + 1] - o0) >> 5);
+        if (K < 2 || K > kBalMaxK) continue;           // warp-uniform
+        const int64_t base = ltile[tile] + o0;
+        if (lane < 16) cnt[wb][0][lane] = cnt[wb][1][lane] = 0;
+        __syncwarp();
+        for (int s = 0; s < K; ++s) {
+            const int64_t pos = base + ell_slot(s, lane, K);
+            const int src = lsrc[pos];
+            es[wb][s][lane] = (uint16_t)src;
+            if constexpr (kW) ew[wb][s][lane] = lw[pos];
+            if (src < (int)kNodeTile) atomicAdd(&cnt[wb][half][src & 15], 1);
+        }
+        __syncwarp();
+        uint32_t rem = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
+        for (int r = 0; r < K; ++r) {
+            unsigned used = 0;
+            int choice = -1, cb = -1;
+            for (int it = 0; it < 4; ++it) {
+                int best = -1, bb = -1, bc = -1;
+                if (choice < 0)
+                    for (uint32_t m = rem; m; m &= m - 1) {
+                        const int e = __ffs(m) - 1;
+                        const int src = es[wb][e][lane];
+                        if (src >= (int)kNodeTile) continue;
+                        const int b = src & 15;
+                        if ((used >> b) & 1u) continue;
+                        const int c = cnt[wb][half][b];
+                        if (c > bc) {
+                            bc = c;
+                            best = e;
+                            bb = b;
+                        }
+                    }
+                const bool prop = choice < 0 && best >= 0;
+                const unsigned peers = __match_any_sync(0xffffffffu, prop ? half * 16 + bb : 64 + lane);
+                const bool win = prop && lane == __ffs(peers) - 1;
+                if (win) {
+                    choice = best;
+                    cb = bb;
+                }
+                unsigned bits = win ? (1u << bb) : 0u;
+                for (int o = 8; o; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+                used |= bits;
+            }
+            // left over: a padding slot takes a free bank pair, else the most frequent remaining entry
+            int pad = -1;
+            if (choice < 0)
+                for (uint32_t m = rem; m; m &= m - 1) {
+                    const int e = __ffs(m) - 1;
+                    if (es[wb][e][lane] >= (int)kNodeTile) {
+                        pad = e;
+                        break;
+                    }
+                }
+            const unsigned padl = __ballot_sync(0xffffffffu, pad >= 0) & (half ? 0xffff0000u : 0x0000ffffu);
+            if (pad >= 0) {
+                int k = __popc(padl & ((1u << lane) - 1u));
+                unsigned fr = ~used & 0xffffu;
+                int b = 0;
+                for (; fr && k > 0; --k) fr &= fr - 1;
+                if (fr) b = __ffs(fr) - 1;
+                choice = pad;
+                es[wb][pad][lane] = (uint16_t)(kNodeTile + b);
+            } else if (choice < 0) {
+                int bc = -1;
+                for (uint32_t m = rem; m; m &= m - 1) {
+                    const int e = __ffs(m) - 1;
+                    const int b = es[wb][e][lane] & 15;
+                    if (cnt[wb][half][b] > bc) {
+                        bc = cnt[wb][half][b];
+                        choice = e;
+                        cb = b;
+                    }
+                }
+            }
+            __syncwarp();
+            if (pad < 0) atomicSub(&cnt[wb][half][cb], 1);
+            ord[wb][r][lane] = (uint8_t)choice;
+            rem &= ~(1u << choice);
+            __syncwarp();
+        }
+        for (int r = 0; r < K; ++r) {
+            const int e = ord[wb][r][lane];
+            const int64_t pos = base + ell_slot(r, lane, K);
+            lsrc[pos] = es[wb][e][lane];
+            if constexpr (kW) lw[pos] = ew[wb][e][lane];
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntile, unsigned long long *__restrict__ mx) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntile; t += (int64_t)gridDim.x * blockDim.x)
         atomicMax(mx, (unsigned long long)(ltile[t + 1] - ltile[t]));
@@ -473,7 +620,7 @@ __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntil
 
 void free_tiles(TilePlan &t) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
-                    (void *)t.vofs, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
+                    (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
                     (void *)t.hsum, (void *)t.tpart})
         cudaFree(p);
@@ -590,8 +737,10 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaMallocAsync(&tp.vfirst, tp.ntile * kVfStride * sizeof(uint16_t), st));
     DI_CUDA(cudaMallocAsync(&tp.plist, tp.ntile * kVRows * sizeof(uint16_t), st));
     DI_CUDA(cudaMallocAsync(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&tp.lstage, (tp.ntile + 1) * sizeof(int32_t), st));
     k_tile_layout<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
-        lc, n, tp.ntile, tp.vofs, tp.vfirst, tp.plist, vcap, pcnt);
+        lc, n, tp.ntile, (int)(2 + (kW ? sizeof(SW) : 0)), (int64_t)(tile_e_buf<W>() - kMetaBytes), tp.vofs,
+        tp.vfirst, tp.plist, vcap, pcnt, tp.lstage);
     count_launch();
     exclusive_scan_i64(pcnt, tp.ltile, tp.ntile, st);
     tp.mpad = read_i64(tp.ltile + tp.ntile, st);
@@ -636,6 +785,12 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaFreeAsync(tkey, st));
     DI_CUDA(cudaFreeAsync(L, st));
     count_launch();
+    if (tp.mpad > 0 && !getenv("DIT_NO_BANK_ORDER")) {
+        k_ell_balance<W><<<(int)std::min<int64_t>(tp.ntile * kVWarps / kBalWarps + 1, (int64_t)h->num_sms * 16),
+                           kBalWarps * 32, 0, st>>>(
+            tp.ltile, tp.vofs, tp.ntile, tp.lsrc, (SW *)tp.lw);
+        count_launch();
+    }
     phase_mark(st, "tiles: split edges");
     // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
     tp.s_chunk.assign(S + 1, 0);
@@ -875,13 +1030,14 @@ __global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restric
 // ---------------------------------------------------------------- tile kernel
 // DIT_TILE_TIMING (debug): per-CTA phase cycle counters of k_tile
 static unsigned long long *g_tile_dbg = nullptr;
+constexpr int kDbg = 48;                         // counters per CTA (see di_debug_tile_timing)
 
 template <typename W>
 struct TileArgs {
     const uint32_t *vofs;
     const uint16_t *vfirst, *plist;
     const uint32_t *rrel;
-    const int32_t *hidx, *deg;
+    const int32_t *hidx, *deg, *lstage;
     const float *wr;
     const double *inv;
     const int64_t *ltile, *rtile;
@@ -891,182 +1047,239 @@ struct TileArgs {
     const double *hsum;
     double *F, *H, *A0, *A1;
     double *part;            // per-CTA partials: resid [grid], leak [grid]
-    unsigned long long *dbg; // optional per-CTA phase cycle counters [grid][5] (DIT_TILE_TIMING)
+    unsigned long long *dbg; // optional per-CTA phase cycle counters [grid][kDbg] (DIT_TILE_TIMING)
     int64_t n, ntile, m;
     int rounds;
     int wave, waves;         // this launch runs tiles wave, wave + waves, ... (R15)
     int64_t ntw;             // tiles of the wave
-    int64_t edge_cap;        // bytes of shared memory for the staged local edges
+    int diag;                // DIT_TILE_DIAG (debug): bit 0 = skip the unstaged local sums (wrong results)
 };
 
 // one target's local pushes in its sliced-ELL column: slots base, base+32, ...
-// (coalesced across the warp), sources in ascending order (Eq. (8) order)
+// (coalesced across the warp); es / ew point into shared memory (staged
+// virtual warps) or global memory (the rest), each call site one of them
 template <typename W>
 __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> *ew, const double *gq, int base,
                                             int K) {
     constexpr bool kW = !std::is_same<W, NoW>::value;
-    double acc = 0.0;
+    // four partial sums (slot mod 4), combined in a fixed order at the end: no
+    // serial chain of dependent adds (R14: a fixed, deterministic order)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int s = 0;
-    if constexpr (kSlotGroup > 1) {
-        // grouped slots: kSlotGroup sources (and weights) per vector load, in slot order
-        const int lane = base & 31, o0 = base - lane;
-        const int Kg = K - K % kSlotGroup;
-        for (; s < Kg; s += kSlotGroup) {
-            const int k = o0 + 32 * s + kSlotGroup * lane;
-            if constexpr (kSlotGroup == 4) {
-                const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
-                double v0 = gq[e.x & 0xffffu], v1 = gq[e.x >> 16], v2 = gq[e.y & 0xffffu], v3 = gq[e.y >> 16];
-                if constexpr (kW) {
-                    if constexpr (sizeof(StoreW<W>) == 4) {
-                        const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
-                        v0 *= (double)w4.x;
-                        v1 *= (double)w4.y;
-                        v2 *= (double)w4.z;
-                        v3 *= (double)w4.w;
-                    } else {
-                        v0 *= (double)ew[k];
-                        v1 *= (double)ew[k + 1];
-                        v2 *= (double)ew[k + 2];
-                        v3 *= (double)ew[k + 3];
-                    }
-                }
-                acc += v0;
-                acc += v1;
-                acc += v2;
-                acc += v3;
+    // grouped slots: four sources (and weights) per vector load
+    const int lane = base & 31, o0 = base - lane;
+    const int Kg = K - K % kSlotGroup;
+#pragma unroll 2
+    for (; s < Kg; s += kSlotGroup) {
+        const int k = o0 + 32 * s + kSlotGroup * lane;
+        const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
+        const double v0 = gq[e.x & 0xffffu], v1 = gq[e.x >> 16], v2 = gq[e.y & 0xffffu], v3 = gq[e.y >> 16];
+        if constexpr (kW) {
+            if constexpr (sizeof(StoreW<W>) == 4) {
+                const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
+                a0 = fma(v0, (double)w4.x, a0);
+                a1 = fma(v1, (double)w4.y, a1);
+                a2 = fma(v2, (double)w4.z, a2);
+                a3 = fma(v3, (double)w4.w, a3);
             } else {
-                const uint32_t e = *reinterpret_cast<const uint32_t *>(es + k);
-                double v0 = gq[e & 0xffffu], v1 = gq[e >> 16];
-                if constexpr (kW) {
-                    if constexpr (sizeof(StoreW<W>) == 4) {
-                        const float2 w2 = *reinterpret_cast<const float2 *>(ew + k);
-                        v0 *= (double)w2.x;
-                        v1 *= (double)w2.y;
-                    } else {
-                        v0 *= (double)ew[k];
-                        v1 *= (double)ew[k + 1];
-                    }
+                a0 = fma(v0, (double)ew[k], a0);
+                a1 = fma(v1, (double)ew[k + 1], a1);
+                a2 = fma(v2, (double)ew[k + 2], a2);
+                a3 = fma(v3, (double)ew[k + 3], a3);
+            }
+        } else {
+            a0 += v0;
+            a1 += v1;
+            a2 += v2;
+            a3 += v3;
+        }
+    }
+    // the last K % 4 slots (one per row of 32): their loads issued together
+    const int t = K - s;
+    if (t > 0) {
+        const int k = base + 32 * s;
+        const int s0 = es[k], s1 = t > 1 ? es[k + 32] : (int)kNodeTile, s2 = t > 2 ? es[k + 64] : (int)kNodeTile;
+        const double v0 = gq[s0], v1 = gq[s1], v2 = gq[s2];
+        if constexpr (kW) {
+            a0 = fma(v0, (double)ew[k], a0);
+            if (t > 1) a1 = fma(v1, (double)ew[k + 32], a1);
+            if (t > 2) a2 = fma(v2, (double)ew[k + 64], a2);
+        } else {
+            a0 += v0;
+            a1 += v1;
+            a2 += v2;                                 // padding slot reads a zero
+        }
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+// A round warp's two virtual warps (A = the longer, B) from shared memory as one
+// software-pipelined walk over steps of four slots per lane: the sources and
+// weights of step j + 1 are loaded while step j's outflow gathers are in flight.
+// Four partial sums per virtual warp (slot mod 4), combined in a fixed order (R14).
+#ifndef DIT_PAIR
+#define DIT_PAIR 0
+#endif
+template <typename W>
+__device__ __forceinline__ void local_sum_pair(const uint16_t *es, const StoreW<W> *ew, const double *gq, int oA,
+                                               int KA, int oB, int KB, int lane, double &rA, double &rB) {
+    constexpr bool kW = !std::is_same<W, NoW>::value;
+    using SW = StoreW<W>;
+    const int SA = (KA + 3) >> 2, S = SA + ((KB + 3) >> 2);
+    auto load = [&](int j, int (&sv)[4], SW (&wv)[4]) {
+        const bool inA = j < SA;
+        const int o = inA ? oA : oB, K = inA ? KA : KB, g = inA ? j : j - SA;
+        const int Kg = K & ~3;
+        if (4 * g < Kg) {                              // runs of four slots per lane
+            const int k = o + 128 * g + 4 * lane;
+            const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
+            sv[0] = (int)(e.x & 0xffffu);
+            sv[1] = (int)(e.x >> 16);
+            sv[2] = (int)(e.y & 0xffffu);
+            sv[3] = (int)(e.y >> 16);
+            if constexpr (kW) {
+                if constexpr (sizeof(SW) == 4) {
+                    const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
+                    wv[0] = w4.x;
+                    wv[1] = w4.y;
+                    wv[2] = w4.z;
+                    wv[3] = w4.w;
+                } else {
+                    for (int u = 0; u < 4; ++u) wv[u] = ew[k + u];
                 }
-                acc += v0;
-                acc += v1;
+            }
+        } else {                                       // the last K % 4 slots, one per row of 32
+            const int t = K - Kg, k = o + 32 * Kg + lane;
+            sv[0] = es[k];
+            sv[1] = t > 1 ? (int)es[k + 32] : (int)kNodeTile;
+            sv[2] = t > 2 ? (int)es[k + 64] : (int)kNodeTile;
+            sv[3] = (int)kNodeTile;                     // zero outflow
+            if constexpr (kW) {
+                wv[0] = ew[k];
+                wv[1] = t > 1 ? ew[k + 32] : SW(0);
+                wv[2] = t > 2 ? ew[k + 64] : SW(0);
+                wv[3] = SW(0);
             }
         }
-    }
-    for (; s + 4 <= K; s += 4) {
-        const int k = base + 32 * s;
-        const int s0 = es[k], s1 = es[k + 32], s2 = es[k + 64], s3 = es[k + 96];
-        double v0 = gq[s0], v1 = gq[s1], v2 = gq[s2], v3 = gq[s3];
+    };
+    int sv[4];
+    SW wv[4] = {SW(1), SW(1), SW(1), SW(1)};
+    rA = 0.0;
+    rB = 0.0;
+    if (S == 0) return;
+    load(0, sv, wv);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int j = 0; j < S; ++j) {
+        int sn[4] = {0, 0, 0, 0};
+        SW wn[4] = {SW(1), SW(1), SW(1), SW(1)};
+        if (j + 1 < S) load(j + 1, sn, wn);
+        const double v0 = gq[sv[0]], v1 = gq[sv[1]], v2 = gq[sv[2]], v3 = gq[sv[3]];
         if constexpr (kW) {
-            v0 *= (double)ew[k];
-            v1 *= (double)ew[k + 32];
-            v2 *= (double)ew[k + 64];
-            v3 *= (double)ew[k + 96];
+            a0 = fma(v0, (double)wv[0], a0);
+            a1 = fma(v1, (double)wv[1], a1);
+            a2 = fma(v2, (double)wv[2], a2);
+            a3 = fma(v3, (double)wv[3], a3);
+        } else {
+            a0 += v0;
+            a1 += v1;
+            a2 += v2;
+            a3 += v3;
         }
-        acc += v0;
-        acc += v1;
-        acc += v2;
-        acc += v3;
+        if (j == SA - 1) {
+            rA = (a0 + a1) + (a2 + a3);
+            a0 = a1 = a2 = a3 = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sv[u] = sn[u];
+            wv[u] = wn[u];
+        }
     }
-    for (; s < K; ++s) {
-        const int k = base + 32 * s;
-        double v = gq[es[k]];
-        if constexpr (kW) v *= (double)ew[k];
-        acc += v;
-    }
-    return acc;
+    if (S > SA) rB = (a0 + a1) + (a2 + a3);
 }
-
-constexpr int kMetaBytes = kVofsStride * 4 + kVfStride * 2 + kVRows * 2;   // per-tile layout, TMA-staged
-constexpr int kRecOff = ((int)kNodeTile + 2) * 8 + kVRows * 8 + kMetaBytes;  // light records after gq, psum, meta
-static_assert(kRecOff % 16 == 0 && kMetaBytes % 16 == 0, "16-byte aligned shared buffers");
-
-template <typename W>
-constexpr int tile_fixed_smem() {
-    return kRecOff + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
-}
-
-// One tile's TMA bundle (a buffer of the double-buffered pipeline): the
-// per-node state, the tile's layout, its light records and (when they fit)
-// its local edges.
-constexpr int kNB = 2;                           // bundle buffers (double buffering)
-constexpr int kNodeBytes = (int)kNodeTile * (8 + 8 + 8 + 4 + 4 + 4 + 4);   // F, H, inv, deg, wr, rrel, hidx
-template <typename W>
-constexpr int tile_buf_fixed() {
-    return kNodeBytes + kMetaBytes + (int)kLightCap * (int)sizeof(RemRec<W>) + 32;
-}
-constexpr int kSharedHead = ((int)kNodeTile + 2) * 8 + kVRows * 8;         // gq, psum
-static_assert(kNodeBytes % 16 == 0 && kSharedHead % 16 == 0, "16-byte aligned shared buffers");
 
 struct TileScalars {
-    int64_t l0, l1, r0, r1;
+    int64_t l0, l1;
+    int32_t st, pad;
 };
 
-// thread 0: issue tile `tile`'s bundle into buffer `buf` (bytes counted on `bar`)
+// named barriers (0 is __syncthreads): 1 = the round warps, 2 = the prep warps,
+// 3 + x = "P[x] full" (prep arrives, rounds sync), 5 + x = "P[x] read" (rounds
+// arrive, prep syncs): a warp waiting at a hardware barrier issues nothing
+constexpr int kBarRW = 1, kBarPW = 2, kBarPFull = 3, kBarPEmpty = 5;
+
+__device__ __forceinline__ void bar_sync_n(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// round-warp thread 0: tile `tile`'s edge bundle {layout, staged slots} into E buffer `buf`
 template <typename W>
-__device__ __forceinline__ void issue_tile(const TileArgs<W> &a, const double *Fsrc, int64_t tile,
-                                           const TileScalars &ts, bool gather, unsigned char *buf,
-                                           uint32_t bar) {
+__device__ __forceinline__ void issue_edges(const TileArgs<W> &a, int64_t tile, const TileScalars &ts,
+                                            unsigned char *buf, uint32_t bar) {
     constexpr bool kW = !std::is_same<W, NoW>::value;
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
-    constexpr int kRS = (int)sizeof(RemRec<W>);
-    const int64_t a0 = tile * kNodeTile;
-    const int nn = (int)min(kNodeTile, a.n - a0);
-    const uint32_t n8 = (uint32_t)((nn * 8 + 15) & ~15), n4 = (uint32_t)((nn * 4 + 15) & ~15);
-    const int64_t r0 = gather ? ts.r0 : 0, r1 = gather ? ts.r1 : 0;
-    const int64_t rb0 = (r0 * kRS) & ~int64_t(15), rb1 = (r1 * kRS + 15) & ~int64_t(15);
-    const int64_t sb0 = (ts.l0 * 2) & ~int64_t(15), sb1 = (ts.l1 * 2 + 15) & ~int64_t(15);
-    const int64_t wb0 = (ts.l0 * kWB) & ~int64_t(15), wb1 = (ts.l1 * kWB + 15) & ~int64_t(15);
-    const int64_t ebytes = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0);
-    const bool staged = ebytes <= a.edge_cap;
-    uint32_t bytes = 3 * n8 + 4 * n4 + (uint32_t)kMetaBytes + (uint32_t)(rb1 - rb0);
-    if (staged) bytes += (uint32_t)ebytes;
-    // order this CTA's earlier generic-proxy accesses of the buffer before the async writes
+    const int64_t cnt = ts.l1 - ts.l0 - ts.st;       // staged slots: multiples of 32 (16-byte aligned)
+    const uint32_t bytes = (uint32_t)(kMetaBytes + cnt * (2 + kWB));
+    // order this CTA's earlier generic-proxy reads of the buffer before the async writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(bar, bytes);
     const uint32_t sb = smem_u32(buf);
-    tma_load(sb + 0 * kNodeTile * 8, Fsrc + a0, n8, bar);
-    tma_load(sb + 1 * kNodeTile * 8, a.H + a0, n8, bar);
-    tma_load(sb + 2 * kNodeTile * 8, a.inv + a0, n8, bar);
-    const uint32_t q = 3 * kNodeTile * 8;
-    tma_load(sb + q + 0 * kNodeTile * 4, a.deg + a0, n4, bar);
-    tma_load(sb + q + 1 * kNodeTile * 4, a.wr + a0, n4, bar);
-    tma_load(sb + q + 2 * kNodeTile * 4, a.rrel + a0, n4, bar);
-    tma_load(sb + q + 3 * kNodeTile * 4, a.hidx + a0, n4, bar);
-    const uint32_t m = kNodeBytes;
-    tma_load(sb + m, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
-    tma_load(sb + m + kVofsStride * 4, a.vfirst + tile * kVfStride, kVfStride * 2, bar);
-    tma_load(sb + m + kVofsStride * 4 + kVfStride * 2, a.plist + tile * kVRows, kVRows * 2, bar);
-    const uint32_t rofs = kNodeBytes + kMetaBytes;
-    if (rb1 > rb0)
-        tma_load(sb + rofs, reinterpret_cast<const unsigned char *>(a.rrec) + rb0, (uint32_t)(rb1 - rb0), bar);
-    const uint32_t eofs = tile_buf_fixed<W>();
-    if (!staged) {                                   // rounds read them from global: bring them to L2 now
-        if (sb1 > sb0) tma_prefetch_l2(reinterpret_cast<const unsigned char *>(a.lsrc) + sb0, (uint32_t)(sb1 - sb0));
-        if (kW && wb1 > wb0) tma_prefetch_l2(reinterpret_cast<const unsigned char *>(a.lw) + wb0, (uint32_t)(wb1 - wb0));
+    tma_load(sb, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
+    tma_load(sb + kVofsStride * 4, a.vfirst + tile * kVfStride, kVfStride * 2, bar);
+    tma_load(sb + kVofsStride * 4 + kVfStride * 2, a.plist + tile * kVRows, kVRows * 2, bar);
+    if (cnt > 0) {
+        tma_load(sb + kMetaBytes, a.lsrc + ts.l0 + ts.st, (uint32_t)(cnt * 2), bar);
+        if constexpr (kW) tma_load(sb + kMetaBytes + (uint32_t)(cnt * 2), a.lw + ts.l0 + ts.st, (uint32_t)(cnt * kWB), bar);
     }
-    if (staged) {
-        if (sb1 > sb0) tma_load(sb + eofs, reinterpret_cast<const unsigned char *>(a.lsrc) + sb0, (uint32_t)(sb1 - sb0), bar);
-        if (kW && wb1 > wb0)
-            tma_load(sb + eofs + (uint32_t)(sb1 - sb0), reinterpret_cast<const unsigned char *>(a.lw) + wb0,
-                     (uint32_t)(wb1 - wb0), bar);
+    // the unstaged (longest) virtual warps are read through L2 by the rounds
+    if (ts.st > 0) {
+        tma_prefetch_l2(a.lsrc + ts.l0, (uint32_t)(ts.st * 2));
+        if constexpr (kW) tma_prefetch_l2(a.lw + ts.l0, (uint32_t)(ts.st * kWB));
     }
 }
 
-// Persistent kernel, one 512-thread CTA per SM, tiles round-robin; the next
-// tile's bundle streams in (TMA) while the current tile gathers and diffuses.
+// prep-warp thread 0: the light records [r0, r1) (16-byte aligned superset) into R buffer `buf`
 template <typename W>
-__global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
+__device__ __forceinline__ void issue_records(const TileArgs<W> &a, int64_t r0, int64_t r1, unsigned char *buf,
+                                              uint32_t bar) {
+    constexpr int kRS = (int)sizeof(RemRec<W>);
+    const int64_t rb0 = (r0 * kRS) & ~int64_t(15), rb1 = (r1 * kRS + 15) & ~int64_t(15);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(bar, (uint32_t)(rb1 - rb0));
+    if (rb1 > rb0)
+        tma_load(smem_u32(buf), reinterpret_cast<const unsigned char *>(a.rrec) + rb0, (uint32_t)(rb1 - rb0), bar);
+}
+
+// Persistent kernel, one 1024-thread CTA per SM, warp-specialised:
+//   round warps 0-15 -- thread i owns node i of the current tile: the `rounds`
+//     Jacobi rounds over the tile's local in-edges (Eq. (8) pushes, sliced-ELL
+//     slots from shared memory), then F, H += D, A = d D inv out;
+//   prep warps 16-31 -- meanwhile the NEXT tile's inflow: the remote pushes still
+//     pending (heavy sums, light records' gathered outflow) added to F, into P.
+// TMA bulk copies bring each tile's edge bundle (round warps) and light records
+// (prep warps) into the buffer of its parity; mbarriers hand P between the groups.
+template <typename W, bool kProf>
+__global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool kW = !std::is_same<W, NoW>::value;
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     constexpr int kRS = (int)sizeof(RemRec<W>);
-    double *gq = reinterpret_cast<double *>(smem);                       // [kNodeTile + 2]: outflow, zero pad slot
-    double *psum = gq + kNodeTile + 2;                                   // [kVRows]: piece sums by rank
-    const int bufsz = (int)(tile_buf_fixed<W>() + a.edge_cap);
-    __shared__ __align__(8) unsigned long long bars[kNB];
-    __shared__ TileScalars sc[kNB];                  // scalars of the tile in each buffer
-    __shared__ double s_r[kTileBlockWarps], s_l[kTileBlockWarps];
-    __shared__ unsigned long long s_c[kTileBlockWarps][2];
+    double *gq = reinterpret_cast<double *>(smem);                       // [kGqSlots]: outflow, zero pad slots
+    double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kVRows]: piece sums by rank
+    PrepRow *Pbuf = reinterpret_cast<PrepRow *>(smem + kOffP);           // [2][kNodeTile]
+    auto rbuf = [&](int x) { return smem + kOffR + x * tile_rec_buf<W>(); };
+    auto ebuf = [&](int x) { return smem + tile_off_e<W>() + x * tile_e_buf<W>(); };
+    // E_full, R_full: TMA completion (count 1)
+    __shared__ __align__(8) unsigned long long bars[4];
+    __shared__ TileScalars sc[2];                    // scalars of the tile in each E buffer
+    __shared__ double s_r[kTileBlock / 32], s_l[kTileBlock / 32];
+    __shared__ unsigned long long s_c[kTileBlock / 32][2];
     __shared__ bool s_last;
     if (ctrl->done || ctrl->use_pull != kUseTiled) return;
     const double d = ctrl->d;
@@ -1076,197 +1289,303 @@ __global__ void __launch_bounds__(kTileBlock, kTileBlocksPerSM) k_tile(TileArgs<
     const unsigned long long sw = ctrl->sweeps;
     double *__restrict__ Anext = (sw & 1) ? a.A1 : a.A0;
     const double *__restrict__ Aprev = (sw & 1) ? a.A0 : a.A1;
-    const int i = threadIdx.x;
-    const int lane = i & 31, wp = i >> 5;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int64_t G = gridDim.x;
+    const bool is_rw = tid < kRW;
     auto tid_of = [&](int64_t jt) { return (int64_t)a.wave + (int64_t)a.waves * jt; };   // the wave's jt-th tile
-    auto scal = [&](int64_t jt) {
-        TileScalars ts{0, 0, 0, 0};
-        if (jt < a.ntw) {
-            const int64_t t = tid_of(jt);
-            ts = TileScalars{a.ltile[t], a.ltile[t + 1], a.rtile[t], a.rtile[t + 1]};
+    auto E_full = [&](int x) { return smem_u32(&bars[x]); };
+    auto R_full = [&](int x) { return smem_u32(&bars[2 + x]); };
+    if (tid == 0) {
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(E_full(x), 1);
+            mbar_init(R_full(x), 1);
         }
-        return ts;
-    };
-    auto bufp = [&](int x) { return smem + kSharedHead + x * bufsz; };
-    auto recs_of = [&](int x, const TileScalars &ts) {
-        const int64_t r0 = recs_on ? ts.r0 : 0;
-        return reinterpret_cast<RemRec<W> *>(bufp(x) + kNodeBytes + kMetaBytes + (r0 * kRS - ((r0 * kRS) & ~int64_t(15))));
-    };
-    if (i == 0) {
-        gq[kNodeTile] = 0.0;                         // padding slots read this
-        gq[kNodeTile + 1] = 0.0;
-        for (int x = 0; x < kNB; ++x) mbar_init(smem_u32(&bars[x]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int x = 0; x + 1 < kNB; ++x) {
-            sc[x] = scal(blockIdx.x + x * G);
-            if (blockIdx.x + x * G < a.ntw)
-                issue_tile<W>(a, a.F, tid_of(blockIdx.x + x * G), sc[x], recs_on, bufp(x), smem_u32(&bars[x]));
-        }
     }
+    if (tid < (int)(kGqSlots - kNodeTile)) gq[kNodeTile + tid] = 0.0;   // ELL padding reads these
     __syncthreads();
     double resid = 0.0, leak = 0.0;
-    unsigned long long nodes = 0, edges = 0;
-    int k = 0;
-    for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
-        const int64_t tile = tid_of(jt);
-        const int b = k % kNB;
-        unsigned char *buf = bufp(b);
-        // the bundle kNB-1 tiles ahead into the buffer the previous iteration freed
-        if (i == 0 && jt + (kNB - 1) * G < a.ntw) {
-            const int x = (k + kNB - 1) % kNB;
-            sc[x] = scal(jt + (kNB - 1) * G);
-            issue_tile<W>(a, a.F, tid_of(jt + (kNB - 1) * G), sc[x], recs_on, bufp(x), smem_u32(&bars[x]));
-        }
-        const TileScalars cur = sc[b];
-        const int64_t a0 = tile * kNodeTile;
-        const int nn = (int)min(kNodeTile, a.n - a0);
-        const int64_t l0 = cur.l0, l1 = cur.l1;
-        const int64_t r0 = recs_on ? cur.r0 : 0, r1 = recs_on ? cur.r1 : 0;
-        const int64_t sb0 = (l0 * 2) & ~int64_t(15), sb1 = (l1 * 2 + 15) & ~int64_t(15);
-        const int64_t wb0 = (l0 * kWB) & ~int64_t(15), wb1 = (l1 * kWB + 15) & ~int64_t(15);
-        const bool staged = (sb1 - sb0) + (kW ? (wb1 - wb0) : 0) <= a.edge_cap;
-        const double *Fs = reinterpret_cast<const double *>(buf);
-        const double *Hs = Fs + kNodeTile;
-        const double *Is = Hs + kNodeTile;
-        const int32_t *Ds = reinterpret_cast<const int32_t *>(Is + kNodeTile);
-        const float *Ws = reinterpret_cast<const float *>(Ds + kNodeTile);
-        const uint32_t *Rs = reinterpret_cast<const uint32_t *>(Ws + kNodeTile);
-        const int32_t *Xs = reinterpret_cast<const int32_t *>(Rs + kNodeTile);
-        const uint32_t *vofs_s = reinterpret_cast<const uint32_t *>(buf + kNodeBytes);
-        const uint16_t *vf_s = reinterpret_cast<const uint16_t *>(vofs_s + kVofsStride);
-        const uint16_t *pl_s = vf_s + kVfStride;
-        unsigned char *ebuf = buf + tile_buf_fixed<W>();
-        long long c0 = a.dbg ? clock64() : 0;
-        mbar_wait(smem_u32(&bars[b]), (uint32_t)((k / kNB) & 1));
-        const bool valid = i < nn;
-        const int64_t j = a0 + i;
-        const int R = (int)(r1 - r0);
-        RemRec<W> *recs = recs_of(b, cur);
-        // 1. remote pushes still pending: from the previous sweep, and from this sweep's
-        //    earlier waves (R15): heavy sums and the light records' gathered outflow
-        double hs = 0.0;
-        if (valid && recs_on) {
-            const int32_t hx = Xs[i];
-            if (hx >= 0) hs = a.hsum[hx];
-        }
-#pragma unroll 4
-        for (int q = i; q < R; q += kTileBlock) {
-            const RemRec<W> r = recs[q];
-            const bool early = tile_wave(r.src, a.waves) < a.wave;
-            const double v = early ? Anext[r.src] : (gather ? Aprev[r.src] : 0.0);
-            *reinterpret_cast<double *>(&recs[q]) = v * rec_w(r);
-        }
-        long long c1 = a.dbg ? clock64() : 0;
-        __syncthreads();
-        double f = 0.0, ivi = 0.0;
-        int dgi = 0;
-        if (valid) {
-            ivi = Is[i];
-            dgi = Ds[i];
-            double s = 0.0;
-            if (recs_on) {
-                const int rb = (int)Rs[i];
-                const int re = i + 1 < nn ? (int)Rs[i + 1] : R;
-                for (int q = rb; q < re; ++q) s += *reinterpret_cast<const double *>(&recs[q]);
+    uint32_t nodes = 0;                              // per thread: <= tiles x rounds
+    unsigned long long edges = 0;
+    unsigned long long *dbg = kProf ? a.dbg + blockIdx.x * kDbg : nullptr;
+    if (is_rw) {
+        // ------------------------------------------------ round warps
+        const int i = tid, wp = tid >> 5;
+        auto escal = [&](int64_t jt) {
+            const int64_t t = tid_of(jt);
+            return TileScalars{a.ltile[t], a.ltile[t + 1], a.lstage[t], 0};
+        };
+        if (i == 0)
+            for (int x = 0; x < 2; ++x)
+                if (blockIdx.x + x * G < a.ntw) {
+                    sc[x] = escal(blockIdx.x + x * G);
+                    issue_edges<W>(a, tid_of(blockIdx.x + x * G), sc[x], ebuf(x), E_full(x));
+                }
+        long long ls_cyc = 0, b2_cyc = 0, ns_cyc = 0, b1_cyc = 0, rows_w = 0;           // DIT_TILE_TIMING: local sums, wait after them
+        int k = 0;
+        for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
+            const int x = k & 1;
+            const uint32_t ph = (uint32_t)((k >> 1) & 1);
+            const int64_t tile = tid_of(jt);
+            const int64_t a0 = tile * kNodeTile;
+            const int nn = (int)min(kNodeTile, a.n - a0);
+            const bool valid = i < nn;
+            const int64_t j = a0 + i;
+            // scalars of the tile two ahead (loaded now, used after the rounds)
+            TileScalars nx{0, 0, 0, 0};
+            const bool has_nx = jt + 2 * G < a.ntw;
+            if (i == 0 && has_nx) nx = escal(jt + 2 * G);
+            long long c0 = kProf ? clock64() : 0;
+            bar_sync_n(kBarPFull + x, kTileBlock);
+            // f, 1/sum w and the out-degree now; H and wr from P[x] again at the state out
+            const PrepRow *prow = Pbuf + x * kNodeTile + i;
+            double f = 0.0, pivi = 0.0;
+            int32_t pdeg = 0;
+            if (valid) {
+                f = prow->f;
+                pivi = prow->ivi;
+                pdeg = prow->deg;
             }
-            f = Fs[i] + s + hs;
-        }
-        long long c2 = a.dbg ? clock64() : 0;
-        // 2. local diffusion rounds in shared memory
-        const uint16_t *es;
-        const StoreW<W> *ew = nullptr;
-        if (staged) {
-            es = reinterpret_cast<const uint16_t *>(ebuf + (l0 * 2 - sb0));
-            if constexpr (kW) ew = reinterpret_cast<const StoreW<W> *>(ebuf + (sb1 - sb0) + (l0 * kWB - wb0));
-        } else {
-            es = a.lsrc + l0;
-            if constexpr (kW) ew = a.lw + l0;
-        }
-        double D = 0.0;
-        for (int r = 0; r < a.rounds; ++r) {
-            double q = 0.0;
-            if (valid && f != 0.0) {
-                D += f;                              // Eq. (10)
-                nodes += 1;
-                edges += (unsigned long long)dgi;
-                q = d * f * ivi;                     // d F(i) / sum_k w_{i,k}
-            }
-            if (i < kTileThreads) gq[i] = q;
-            __syncthreads();
-            if constexpr (kTileBlockWarps == kVWarps) {
-                // Eq. (8) local pushes: warp w runs virtual warp w of pieces
-                const uint32_t o0 = vofs_s[wp];
-                const int K = (int)((vofs_s[wp + 1] - o0) >> 5);
-                if (K) psum[wp * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
-            } else {
+            long long c1 = kProf ? clock64() : 0;
+            mbar_wait(E_full(x), ph);
+            long long c2 = kProf ? clock64() : 0;
+            const TileScalars cur = sc[x];
+            unsigned char *E = ebuf(x);
+            const uint32_t *vofs_s = reinterpret_cast<const uint32_t *>(E);
+            const uint16_t *vf_s = reinterpret_cast<const uint16_t *>(vofs_s + kVofsStride);
+            const uint16_t *pl_s = vf_s + kVfStride;
+            const int st = cur.st;
+            const int64_t cnt = cur.l1 - cur.l0 - st;
+            // slot k of the tile: shared memory for k >= st, global below
+            const uint16_t *es_sm = reinterpret_cast<const uint16_t *>(E + kMetaBytes) - st;
+            const StoreW<W> *ew_sm = reinterpret_cast<const StoreW<W> *>(E + kMetaBytes + cnt * 2) - st;
+            const uint16_t *es_gl = a.lsrc + cur.l0;
+            const StoreW<W> *ew_gl = kW ? a.lw + cur.l0 : nullptr;
+            // the node's pieces (ranks into psum, in edge order): the first four in registers
+            const int p0 = valid ? (int)vf_s[i] : 0, np = valid ? (int)vf_s[i + 1] - p0 : 0;
+            const int pr0 = np > 0 ? pl_s[p0] : 0, pr1 = np > 1 ? pl_s[p0 + 1] : 0;
+            const int pr2 = np > 2 ? pl_s[p0 + 2] : 0, pr3 = np > 3 ? pl_s[p0 + 3] : 0;
+            double D = 0.0;
+            for (int r = 0; r < a.rounds; ++r) {
+                double q = 0.0;
+                if (f != 0.0) {                      // invalid threads hold f = 0
+                    D += f;                          // Eq. (10)
+                    nodes += 1;
+                    edges += (unsigned long long)pdeg;
+                    q = d * f * pivi;                // d F(i) / sum_k w_{i,k}
+                }
+                const long long t9 = kProf ? clock64() : 0;
+                gq[i] = q;
+                bar_sync_n(kBarRW, kRW);
+                const long long ta = kProf ? clock64() : 0;
+                if (kProf) b1_cyc += ta - t9;
                 // Eq. (8) local pushes: this warp's two virtual warps of pieces (longest with shortest)
+                const int vA = wp, vB = kVWarps - 1 - wp;
+                const uint32_t oA = vofs_s[vA], oB = vofs_s[vB];
+                const int KA = (int)((vofs_s[vA + 1] - oA) >> 5), KB = (int)((vofs_s[vB + 1] - oB) >> 5);
+                if (DIT_PAIR && (int)oA >= st) {      // both staged (oB > oA)
+                    if (kProf) rows_w += KA + KB;
+                    double rA, rB;
+                    local_sum_pair<W>(es_sm, ew_sm, gq, (int)oA, KA, (int)oB, KB, lane, rA, rB);
+                    if (KA) psum[vA * 32 + lane] = rA;
+                    if (KB) psum[vB * 32 + lane] = rB;
+                } else
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     const int vw = h2 ? kVWarps - 1 - wp : wp;
                     const uint32_t o0 = vofs_s[vw];
                     const int K = (int)((vofs_s[vw + 1] - o0) >> 5);
-                    if (K) psum[vw * 32 + lane] = local_sum<W>(es, ew, gq, (int)o0 + lane, K);
+                    if (kProf) rows_w += K;
+                    if (K) {
+                        double acc;
+                        if ((int)o0 >= st) acc = local_sum<W>(es_sm, ew_sm, gq, (int)o0 + lane, K);
+                        else acc = (a.diag & 1) ? 0.0 : local_sum<W>(es_gl, ew_gl, gq, (int)o0 + lane, K);
+                        psum[vw * 32 + lane] = acc;
+                    }
+                }
+                const long long tb = kProf ? clock64() : 0;
+                bar_sync_n(kBarRW, kRW);
+                const long long tc = kProf ? clock64() : 0;
+                if (kProf) {
+                    ls_cyc += tb - ta;
+                    b2_cyc += tc - tb;
+                }
+                if (np > 0) {                         // the node's pieces, in edge order
+                    const double x0 = psum[pr0], x1 = np > 1 ? psum[pr1] : 0.0;
+                    const double x2 = np > 2 ? psum[pr2] : 0.0, x3 = np > 3 ? psum[pr3] : 0.0;
+                    double acc = 0.0 + x0;
+                    if (np > 1) acc += x1;
+                    if (np > 2) acc += x2;
+                    if (np > 3) acc += x3;
+                    for (int p = p0 + 4; p < p0 + np; ++p) acc += psum[pl_s[p]];
+                    f = acc;
+                } else {
+                    f = 0.0;
+                }
+                if (kProf) {
+                    __syncwarp();
+                    ns_cyc += clock64() - tc;
                 }
             }
-            __syncthreads();
-            if (valid) {                              // the node's pieces, in edge order
-                const int p0 = vf_s[i], p1 = vf_s[i + 1];
-                double acc = 0.0;
-                for (int p = p0; p < p1; ++p) acc += psum[pl_s[p]];
-                f = acc;
+            long long c3 = kProf ? clock64() : 0;
+            // state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
+            if (valid) {
+                a.F[j] = f;
+                if (D != 0.0) a.H[j] = prow->H + D;
+                Anext[j] = d * D * pivi;
+                // R13: the pushes still pending carry d D(i) P_{t,i} over the pending
+                // out-edges t, i.e. |d D(i)| wr(i) with wr(i) = inv(i) sum_pending w
+                resid += fabs(f) + fabs(d * D) * (double)prow->wr;
+                if (pdeg == 0) leak += D;             // dangling: the fluid left the system (§3.3)
+            }
+            if (jt + 2 * G < a.ntw) bar_arrive_n(kBarPEmpty + x, kTileBlock);   // prep syncs it before tile k + 2
+            bar_sync_n(kBarRW, kRW);                       // E[x] read by every round warp
+            if (i == 0 && has_nx) {
+                sc[x] = nx;
+                issue_edges<W>(a, tid_of(jt + 2 * G), nx, E, E_full(x));
+            }
+            if (kProf && i == 0) {
+                dbg[st == 0 ? 10 : 12] += c3 - c2;    // rounds of fully / partly staged tiles
+                dbg[st == 0 ? 11 : 13] += 1;
+                dbg[0] += c1 - c0;                    // waiting for the prepared rows
+                dbg[1] += c2 - c1;                    // waiting for the edge bundle
+                dbg[2] += c3 - c2;                    // local rounds
+                dbg[3] += clock64() - c3;             // state out
+                dbg[7] += 1;
             }
         }
-        long long c3 = a.dbg ? clock64() : 0;
-        // 3. state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
-        if (valid) {
-            const double An = d * D * ivi;
-            a.F[j] = f;
-            if (D != 0.0) a.H[j] = Hs[i] + D;
-            Anext[j] = An;
-            // R13: the pushes still pending carry d D(i) P_{t,i} over the pending
-            // out-edges t, i.e. |d D(i)| wr(i) with wr(i) = inv(i) sum_pending w
-            resid += fabs(f) + fabs(d * D) * (double)Ws[i];
-            if (dgi == 0) leak += D;                 // dangling: the fluid left the system (§3.3)
+        if (kProf && lane == 0) {
+            atomicAdd(&dbg[8], (unsigned long long)ls_cyc);
+            atomicAdd(&dbg[9], (unsigned long long)b2_cyc);
+            atomicAdd(&dbg[14], (unsigned long long)ns_cyc);
+            atomicAdd(&dbg[16 + wp], (unsigned long long)ls_cyc);
+            atomicAdd(&dbg[32 + wp], (unsigned long long)rows_w);
+            atomicAdd(&dbg[15], (unsigned long long)b1_cyc);
         }
-        __syncthreads();                             // buffer b free for the bundle kNB-1 ahead
-        if (a.dbg && i == 0) {
-            const long long c4 = clock64();
-            unsigned long long *qd = a.dbg + blockIdx.x * 5;
-            qd[0] += c1 - c0;                        // waiting for the bundle
-            qd[1] += c2 - c1;                        // remote inflow (gathers)
-            qd[2] += c3 - c2;                        // local rounds
-            qd[3] += c4 - c3;                        // state out
-            qd[4] += 1;
+    } else {
+        // ------------------------------------------------ prep warps
+        const int p = tid - kRW;
+        auto rscal = [&](int64_t jt, int64_t &r0, int64_t &r1) {
+            const int64_t t = tid_of(jt);
+            r0 = recs_on ? a.rtile[t] : 0;
+            r1 = recs_on ? a.rtile[t + 1] : 0;
+        };
+        if (p == 0)
+            for (int x = 0; x < 2; ++x)
+                if (blockIdx.x + x * G < a.ntw) {
+                    int64_t r0, r1;
+                    rscal(blockIdx.x + x * G, r0, r1);
+                    issue_records<W>(a, r0, r1, rbuf(x), R_full(x));
+                }
+        int k = 0;
+        for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
+            const int x = k & 1;
+            const uint32_t ph = (uint32_t)((k >> 1) & 1);
+            const int64_t tile = tid_of(jt);
+            const int64_t a0 = tile * kNodeTile;
+            const int nn = (int)min(kNodeTile, a.n - a0);
+            long long c0 = kProf ? clock64() : 0;
+            // per-node state (independent loads, in flight together): nodes p, p + kPWt
+            int64_t r0 = 0, r1 = 0;
+            rscal(jt, r0, r1);
+            int64_t n0 = 0, n1 = 0;
+            const bool has_nx = jt + 2 * G < a.ntw;
+            if (p == 0 && has_nx) rscal(jt + 2 * G, n0, n1);
+            double Fj[kPN], ivi[kPN], Hj[kPN];
+            float wrj[kPN];
+            int32_t dg[kPN], hx[kPN];
+            int rb[kPN], re[kPN];
+#pragma unroll
+            for (int u = 0; u < kPN; ++u) {
+                const int q = p + u * kPWt;
+                const int64_t j = a0 + q;
+                Fj[u] = ivi[u] = Hj[u] = 0.0;
+                wrj[u] = 0.f;
+                dg[u] = 0;
+                hx[u] = -1;
+                rb[u] = re[u] = 0;
+                if (q < nn) {
+                    Fj[u] = a.F[j];
+                    ivi[u] = a.inv[j];
+                    Hj[u] = a.H[j];
+                    wrj[u] = a.wr[j];
+                    dg[u] = a.deg[j];
+                    if (recs_on) {
+                        hx[u] = a.hidx[j];
+                        rb[u] = (int)a.rrel[j];
+                        re[u] = q + 1 < nn ? (int)a.rrel[j + 1] : (int)(r1 - r0);
+                    }
+                }
+            }
+            mbar_wait(R_full(x), ph);
+            long long c1 = kProf ? clock64() : 0;
+            RemRec<W> *recs = reinterpret_cast<RemRec<W> *>(rbuf(x) + (r0 * kRS - ((r0 * kRS) & ~int64_t(15))));
+            const int R = (int)(r1 - r0);
+            // remote pushes still pending: from the previous sweep, and from this
+            // sweep's earlier waves (R15): light records' gathered outflow, in place
+#pragma unroll 4
+            for (int q = p; q < R; q += kPWt) {
+                const RemRec<W> rc = recs[q];
+                const bool early = tile_wave(rc.src, a.waves) < a.wave;
+                const double v = early ? Anext[rc.src] : (gather ? Aprev[rc.src] : 0.0);
+                *reinterpret_cast<double *>(&recs[q]) = v * rec_w(rc);
+            }
+            double hs[kPN];
+#pragma unroll
+            for (int u = 0; u < kPN; ++u) hs[u] = hx[u] >= 0 ? a.hsum[hx[u]] : 0.0;
+            bar_sync_n(kBarPW, kPWt);
+            double sm[kPN];
+#pragma unroll
+            for (int u = 0; u < kPN; ++u) {
+                double acc = 0.0;
+                for (int q = rb[u]; q < re[u]; ++q) acc += *reinterpret_cast<const double *>(&recs[q]);
+                sm[u] = acc;
+            }
+            long long c2 = kProf ? clock64() : 0;
+            if (k >= 2) bar_sync_n(kBarPEmpty + x, kTileBlock);   // the round warps read P[x] of tile k - 2
+            long long c3 = kProf ? clock64() : 0;
+#pragma unroll
+            for (int u = 0; u < kPN; ++u)
+                if (p + u * kPWt < nn)
+                    Pbuf[x * kNodeTile + p + u * kPWt] = PrepRow{Fj[u] + sm[u] + hs[u], ivi[u], Hj[u], wrj[u], dg[u]};
+            bar_arrive_n(kBarPFull + x, kTileBlock);
+            bar_sync_n(kBarPW, kPWt);                      // R[x] read by every prep warp
+            if (p == 0 && has_nx) issue_records<W>(a, n0, n1, rbuf(x), R_full(x));
+            if (kProf && p == 0) {
+                dbg[4] += c1 - c0;                    // node loads + waiting for the records
+                dbg[5] += c2 - c1;                    // gathers + sums
+                dbg[6] += c3 - c2;                    // waiting for the round warps
+            }
         }
     }
     // CTA partials (fixed order) and the last-block end of the sweep
     resid = warp_sum(resid);
     leak = warp_sum(leak);
-    nodes = warp_sum(nodes);
-    edges = warp_sum(edges);
+    const unsigned long long nodes64 = warp_sum((unsigned long long)nodes);
+    const unsigned long long edges64 = warp_sum(edges);
     const unsigned w = threadIdx.x >> 5;
     if (lane_id() == 0) {
         s_r[w] = resid;
         s_l[w] = leak;
-        s_c[w][0] = nodes;
-        s_c[w][1] = edges;
+        s_c[w][0] = nodes64;
+        s_c[w][1] = edges64;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double rr = 0.0, ll = 0.0;
-        unsigned long long x = 0, y = 0;
-        for (int q = 0; q < kTileBlockWarps; ++q) {
+        unsigned long long xx = 0, yy = 0;
+        for (int q = 0; q < kTileBlock / 32; ++q) {
             rr += s_r[q];
             ll += s_l[q];
-            x += s_c[q][0];
-            y += s_c[q][1];
+            xx += s_c[q][0];
+            yy += s_c[q][1];
         }
         a.part[a.wave * 4096 + blockIdx.x] = rr;
         a.part[(a.waves + a.wave) * 4096 + blockIdx.x] = ll;
-        if (x) {
-            atomicAdd(&ctrl->diffused_nodes, x);
-            atomicAdd(&ctrl->sel_edges, y);
+        if (xx) {
+            atomicAdd(&ctrl->diffused_nodes, xx);
+            atomicAdd(&ctrl->sel_edges, yy);
         }
         __threadfence();
         const unsigned v = atomicAdd(&ctrl->red_blocks, 1u);
@@ -1361,8 +1680,9 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     a.n = g.n;
     a.ntile = tp.ntile;
     a.m = g.m;
+    a.lstage = tp.lstage;
+    a.diag = getenv("DIT_TILE_DIAG") ? atoi(getenv("DIT_TILE_DIAG")) : 0;
     a.rounds = rounds;
-    a.edge_cap = 0;
     a.dbg = nullptr;
     a.wave = 0;
     a.waves = tp.waves;
@@ -1406,45 +1726,28 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
     DevGraph &g = h->g;
     State &s = h->s;
     TilePlan &tp = g.tl;
-    if (!tp.tile_smem) {
-        // kTileBlocksPerSM CTAs per SM, each with the shared head (gq, psum) and two
-        // bundle buffers; computed (and the attribute set) once per plan, off the sweep path
-        int per_sm = 0;
-        DI_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
-        cudaFuncAttributes fa;
-        DI_CUDA(cudaFuncGetAttributes(&fa, k_tile<W>));
-        constexpr bool kW = !std::is_same<W, NoW>::value;
-        const int64_t fixed = tile_buf_fixed<W>();
-        int optin = 0;
-        DI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-        const int64_t per_cta = std::min<int64_t>(optin, (int64_t)per_sm / kTileBlocksPerSM - 1024);
-        const int64_t budget = (per_cta - (int64_t)fa.sharedSizeBytes - kSharedHead) / kNB;
-        const int64_t wsz = kW ? (int64_t)sizeof(StoreW<W>) : 0;
-        int64_t cap = std::max<int64_t>(0, (budget - fixed) & ~int64_t(15));
-        cap = std::min<int64_t>(cap, (std::max<int64_t>(tp.max_tile_edges, 1) * (2 + wsz) + 47) & ~int64_t(15));
-        // with two CTAs per SM the edge buffers do not fit: the rounds read the
-        // edges from L1/L2 (prefetched to L2 with the bundle)
-        if (kTileBlocksPerSM > 1 || getenv("DIT_NO_EDGE_STAGING")) cap = 0;
-        tp.edge_cap = cap;
-        tp.tile_smem = (size_t)(kSharedHead + kNB * (fixed + cap));
-        DI_CUDA(cudaFuncSetAttribute(k_tile<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.tile_smem));
+    static bool attr_set = false;                    // once per weight kind, off the sweep path
+    if (!attr_set) {
+        DI_CUDA(cudaFuncSetAttribute(k_tile<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tile_smem_bytes<W>()));
+        DI_CUDA(cudaFuncSetAttribute(k_tile<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tile_smem_bytes<W>()));
+        attr_set = true;
     }
-    const int64_t cap = tp.edge_cap;
-    const size_t smem = tp.tile_smem;
     TileArgs<W> a = tile_args<W>(h, rounds);
-    a.edge_cap = cap;
     if (getenv("DIT_TILE_TIMING")) {
         if (!g_tile_dbg) {
-            DI_CUDA(cudaMalloc(&g_tile_dbg, 4096 * 5 * sizeof(unsigned long long)));
-            DI_CUDA(cudaMemset(g_tile_dbg, 0, 4096 * 5 * sizeof(unsigned long long)));
+            DI_CUDA(cudaMalloc(&g_tile_dbg, 4096 * kDbg * sizeof(unsigned long long)));
+            DI_CUDA(cudaMemset(g_tile_dbg, 0, 4096 * kDbg * sizeof(unsigned long long)));
         }
         a.dbg = g_tile_dbg;
     }
     a.wave = wave;
     a.ntw = tp.ntile > wave ? (tp.ntile - wave + tp.waves - 1) / tp.waves : 0;
     if (a.ntw == 0) return;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntw, (int64_t)h->num_sms * kTileBlocksPerSM));
-    k_tile<W><<<grid, kTileBlock, smem, h->stream>>>(a, s.ctrl);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntw, (int64_t)h->num_sms));
+    if (a.dbg) k_tile<W, true><<<grid, kTileBlock, tile_smem_bytes<W>(), h->stream>>>(a, s.ctrl);
+    else k_tile<W, false><<<grid, kTileBlock, tile_smem_bytes<W>(), h->stream>>>(a, s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());
 }
@@ -1529,13 +1832,13 @@ void launch_tile_flush(di_graph *h) {
 
 // Debug (not part of include/dit.h): k_tile phase cycles {wait, inflow, rounds,
 // state out} summed over CTAs, and the number of (CTA, tile) iterations.
-extern "C" int di_debug_tile_timing(double *out5) {
-    if (!dit::g_tile_dbg || !out5) return 1;
-    std::vector<unsigned long long> v(4096 * 5);
+extern "C" int di_debug_tile_timing(double *out8) {
+    if (!dit::g_tile_dbg || !out8) return 1;
+    std::vector<unsigned long long> v(4096 * dit::kDbg);
     if (cudaMemcpy(v.data(), dit::g_tile_dbg, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost))
         return 2;
-    for (int q = 0; q < 5; ++q) out5[q] = 0;
+    for (int q = 0; q < dit::kDbg; ++q) out8[q] = 0;
     for (int bb = 0; bb < 4096; ++bb)
-        for (int q = 0; q < 5; ++q) out5[q] += (double)v[bb * 5 + q];
+        for (int q = 0; q < dit::kDbg; ++q) out8[q] += (double)v[bb * dit::kDbg + q];
     return 0;
 }
