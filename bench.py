@@ -219,17 +219,137 @@ def roofline_from(prof_tot, workload, variant):
             "sweep_bytes_per_s_all_kernels": sum(prof_tot.get(f"{k}_bytes", 0) for k in kinds) / (tot_ms / 1e3) / 1e9}
 
 
+def cpu_baseline(args, gpu_edges_per_solve=None, g=None):
+    """The CPU oracle (oracle/, test infrastructure) timed as it stands on this
+    host: a bounded sample of the bench workload (configs[args.config] at its
+    single-GPU size), the same schedule as the GPU arm, one core."""
+    spec = spec_for(args)
+    if g is None:
+        g = synth.generate(spec)
+    sw = 1 if g.m > 50_000_000 else 5
+    ce, cdt = oracle_run(args, spec, oracle_cols(g), g.n, sw)
+    out = {"value": ce / cdt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+           "sample": oracle_desc(args, sw) + f" ({ce} diffused edges, {cdt:.1f} s)"}
+    if gpu_edges_per_solve:
+        # the oracle runs the GPU's schedule: a solve diffuses the same edges at its measured rate
+        out["time_to_tol_s"] = gpu_edges_per_solve / out["value"]
+        out["time_to_tol_kind"] = "estimate: the GPU solve's diffused edges / the oracle's measured edges/s"
+    return out
+
+
+def relaunch_distributed(args):
+    """`bench.py --gpus N` started without torchrun: re-execute under
+    torch.distributed.run, one rank per GPU (RANK / LOCAL_RANK / WORLD_SIZE from
+    the launcher, rendezvous on 127.0.0.1); rank 0's JSON line passes through."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but {have} visible CUDA device(s)",
+                          "n_gpus": args.gpus}), flush=True)
+        return 1
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator's rank count shows in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_update(args):
+    """--config 4: BASELINE configs[4], the dynamic update.  A step = di_update_edges
+    (1% of the configs[2] graph rewired: Theorem 4 corrective fluid + CSR rebuild on
+    the device) + the warm di_resume to tol, on a graph solved to tol beforehand
+    (untimed).  Beside it, the cold alternative: plan build (transpose + tile
+    plan) + cold solve of the modified graph (its CSR made by the same
+    di_update_edges on a fresh handle, untimed)."""
+    import torch
+    import paper_1501_06350_b200 as eng
+    from paper_1501_06350_b200 import _lib
+    torch.cuda.set_device(0)
+    spec = synth.CONFIGS[4]
+    tol = args.tol if args.tol is not None else spec.tol
+    g = synth.generate(spec)
+    delta = synth.rewire(spec, g, fraction=0.01, seed=4)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    rp, cl, wv = t(g.row_ptr), t(g.col), t(g.w)
+    dd = {k: (t(v) if v is not None else None) for k, v in delta.items()}
+    kw = dict(d=spec.d, tol=tol, variant=args.variant, local_rounds=args.rounds)
+    stream = torch.cuda.current_stream()
+    out = torch.empty(g.n, dtype=torch.float64, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    upd_ms, res_ms, cold_ms, edges, sweeps, cold_sweeps, prof_tot = [], [], [], 0, [], [], {}
+    with ClockSampler(0) as clk:
+        for it in range(args.warmup + args.steps):
+            G = eng.DIGraph(g.n, rp, cl, wv, stream=stream)
+            G.solve(out=out, **kw)
+            torch.cuda.synchronize()
+            a, b, c = ev(), ev(), ev()
+            a.record(stream)
+            G.update_edges(**dd)
+            b.record(stream)
+            if it >= args.warmup:
+                _lib.di_profile_enable(G.handle, True)
+            _, r = G.resume(out=out, tol=tol, variant=args.variant, local_rounds=args.rounds)
+            c.record(stream)
+            torch.cuda.synchronize()
+            assert r["converged"], r
+            if it >= args.warmup:
+                for k, v in _lib.di_profile_get(G.handle).items():
+                    prof_tot[k] = prof_tot.get(k, 0) + v
+                upd_ms.append(a.elapsed_time(b))
+                res_ms.append(b.elapsed_time(c))
+                edges += r["diffused_edges"]
+                sweeps.append(r["sweeps"])
+            G.close()
+            # the cold alternative: plan build + cold solve of the modified graph from F_0
+            G2 = eng.DIGraph(g.n, rp, cl, wv, stream=stream)
+            G2.update_edges(**dd)
+            a, b = ev(), ev()
+            torch.cuda.synchronize()
+            a.record(stream)
+            _, rc = G2.solve(out=out, **kw)
+            b.record(stream)
+            torch.cuda.synchronize()
+            G2.close()
+            if it >= args.warmup:
+                cold_ms.append(a.elapsed_time(b))
+                cold_sweeps.append(rc["sweeps"])
+    total = sum(upd_ms) + sum(res_ms)
+    line = {"metric": METRIC, "value": edges / (total / 1e3), "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / args.steps, "time_to_tol_s": total / args.steps / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{spec.name} (BASELINE configs[4]): update 1% of the edges + warm resume",
+                       "n": g.n, "m": g.m, "edges_added": int(len(delta["add_src"])),
+                       "edge_pairs_removed": int(len(delta["rem_src"])), "tol": tol, "variant": args.variant,
+                       "local_rounds": args.rounds, "update_ms": statistics.mean(upd_ms),
+                       "resume_ms": statistics.mean(res_ms), "resume_sweeps": sweeps[-1],
+                       "cold_build_and_solve_ms": statistics.mean(cold_ms), "cold_sweeps": cold_sweeps[-1],
+                       "l2": "inputs larger than L2; no flush"},
+            "roofline": roofline_from(prof_tot, spec.name, args.variant) if prof_tot else None,
+            "cpu_baseline": None, "e2e": None, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args):
     import torch
     import paper_1501_06350_b200 as eng
     from paper_1501_06350_b200 import _lib
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.config == 4:
+        return run_update(args)
+    if args.gpus > 1 and world == 0:
+        return relaunch_distributed(args)
     if world > 1 or args.gpus > 1:
         from paper_1501_06350_b200 import dist
         return dist.bench_sharded(args, METRIC, {"clock": ClockSampler, "roofline": roofline_from,
-                                                 "pinned": pinned_alloc})
+                                                 "pinned": pinned_alloc, "cpu_baseline": cpu_baseline})
     torch.cuda.set_device(0)
     spec = spec_for(args)
     tol = args.tol if args.tol is not None else spec.tol
@@ -303,10 +423,7 @@ def run_ours(args):
     # CPU oracle baseline (bounded sample)
     cpu = None
     if not args.no_cpu:
-        sw = 1 if g.m > 50_000_000 else 5
-        ce, cdt = oracle_run(args, spec, oracle_cols(g), g.n, sw)
-        cpu = {"value": ce / cdt, "unit": "edges/s", "cores": 1, "kind": "oracle",
-               "sample": oracle_desc(args, sw) + f" ({ce} diffused edges, {cdt:.1f} s)"}
+        cpu = cpu_baseline(args, results[-1]["diffused_edges"], g)
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "time_to_tol_s": total_ms / args.steps / 1e3,

@@ -250,8 +250,12 @@ int di_shard_set_recv(di_graph *g, int64_t total, const int32_t *local_idx, int3
  * retained until di_shard_finish) */
 int di_shard_begin(di_graph *g, double d, const double *Z, int32_t Z_mem, double tol,
                    const di_solve_opts *opts, double *stats);
-/* next threshold / done flag from the all-reduced gstats = {sum |F|_1, max |F|} (device) */
-int di_shard_control(di_graph *g, const double *gstats);
+/* next threshold / done flag from every rank's stats, gathered in rank order:
+ * gathered = device double[4 * nranks] (an all-gather of the stats buffers).
+ * The device sums |F|_1 and the leak and takes max |F| over ranks in rank order
+ * (deterministic, one collective per sweep); the global leak l (PAPER §3.3)
+ * sets di_shard_finish's completion factor and bound. */
+int di_shard_control(di_graph *g, const double *gathered, int32_t nranks);
 /* one sweep (select + diffusion); ghost fluid moved to ghost_out (device double[n_ghost]) */
 int di_shard_sweep(di_graph *g, double *ghost_out);
 /* F[local_idx[q]] += recv[q] (device double[total]), segment by segment */

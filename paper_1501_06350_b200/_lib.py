@@ -30,8 +30,6 @@ DI_DANGLING_DROP, DI_DANGLING_COMPLETE = 0, 1
 DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL, DI_VARIANT_TILED = 0, 1, 2, 3
 DI_TILE_NODES = 512   # include/dit.h
 DI_TILE_WAVES = 2     # include/dit.h (shards too: cross-rank pushes wait a sweep, R16)
-SHARD_TILED = True    # DI_VARIANT_TILED on shards (di_shard_* with di_shard_flush / _flush_apply)
-SHARD_TILED_FALLBACK = "pull"
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",
@@ -284,7 +282,7 @@ _lib.di_shard_info.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), c
 _lib.di_shard_ghost_ids.argtypes = [_P, _P, _I32]
 _lib.di_shard_set_recv.argtypes = [_P, _I64, _P, _I32, _P, _I32]
 _lib.di_shard_begin.argtypes = [_P, _D, _P, _I32, _D, ctypes.POINTER(di_solve_opts), _P]
-_lib.di_shard_control.argtypes = [_P, _P]
+_lib.di_shard_control.argtypes = [_P, _P, _I32]
 _lib.di_shard_sweep.argtypes = [_P, _P]
 _lib.di_shard_apply.argtypes = [_P, _P]
 _lib.di_shard_flush.argtypes = [_P, _P]
@@ -334,8 +332,8 @@ def di_shard_begin(h, d, Z=None, tol=1e-12, stats=None, **opts):
     _check(_lib.di_shard_begin(h, d, zp, zmem, tol, ctypes.byref(o), sp))
 
 
-def di_shard_control(h, gstats):
-    _check(_lib.di_shard_control(h, _ptr_mem(gstats)[0]))
+def di_shard_control(h, gathered, nranks):
+    _check(_lib.di_shard_control(h, _ptr_mem(gathered)[0], int(nranks)))
 
 
 def di_shard_sweep(h, ghost_out):

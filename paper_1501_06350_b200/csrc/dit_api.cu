@@ -59,11 +59,11 @@ static void keep_pool_memory(int device) {
 // per edge + 256 B per node, at most 60% of the free memory): the builders then
 // carve their temporaries out of one mapped chunk instead of growing the pool
 // piecemeal (which costs ~0.1 s of mapping whenever fragmentation forces it).
-static bool g_reserved[64] = {};   // reserve_pool done (reset by di_release_memory)
+static std::atomic<bool> g_reserved[64] = {};   // reserve_pool done (reset by di_release_memory)
 
 static void reserve_pool(int device, int64_t n, int64_t m, cudaStream_t st) {
-    bool *done = g_reserved;
-    if (device < 0 || device >= 64 || done[device] || getenv("DIT_NO_POOL_RESERVE")) return;
+    std::atomic<bool> *done = g_reserved;
+    if (device < 0 || device >= 64 || done[device].load() || getenv("DIT_NO_POOL_RESERVE")) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
     size_t fr = 0, tot = 0;
@@ -72,7 +72,7 @@ static void reserve_pool(int device, int64_t n, int64_t m, cudaStream_t st) {
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur);
     const uint64_t want = std::min<uint64_t>((uint64_t)(40 * (double)m + 256 * (double)n), (uint64_t)(0.6 * (double)fr));
     if (want < ((uint64_t)1 << 30)) return;         // small graphs: a later big one may still reserve
-    done[device] = true;
+    if (done[device].exchange(true)) return;        // another thread reserved it meanwhile
     if (want <= cur) return;
     void *p = nullptr;
     if (cudaMallocAsync(&p, want, st) != cudaSuccess) {
@@ -128,7 +128,7 @@ int di_release_memory(int32_t device) {
         DI_CUDA(cudaSetDevice(device));
         DI_CUDA(cudaDeviceSynchronize());
         release_cub_scratch(device);
-        if (device >= 0 && device < 64) g_reserved[device] = false;
+        if (device >= 0 && device < 64) g_reserved[device].store(false);
         cudaMemPool_t pool;
         DI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         DI_CUDA(cudaMemPoolTrimTo(pool, 0));
@@ -437,12 +437,12 @@ int di_shard_begin(di_graph *g, double d, const double *Z, int32_t Z_mem, double
     });
 }
 
-int di_shard_control(di_graph *g, const double *gstats) {
+int di_shard_control(di_graph *g, const double *gathered, int32_t nranks) {
     return guarded([&] {
         need_shard(g);
-        if (!gstats) fail(DI_ERR_INVALID, "gstats is NULL");
+        if (!gathered || nranks < 1) fail(DI_ERR_INVALID, "gathered stats: NULL or nranks < 1");
         use_device(g);
-        shard_control(g, gstats, g->s.flushing ? 1 : 0);
+        shard_control(g, gathered, nranks, g->s.flushing ? 1 : 0);
         g->s.flushing = false;
     });
 }

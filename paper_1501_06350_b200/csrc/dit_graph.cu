@@ -14,6 +14,7 @@
 // (F(t) += d H(j) P'_{t,j}).
 #include "dit_internal.cuh"
 
+#include <algorithm>
 #include <vector>
 
 namespace dit {
@@ -420,15 +421,18 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             g.w = w64;
             g.w_kind = DI_W_F64;
         }
-        // Theorem 4, first half: withdraw d P H over the old changed columns
-        if (state && n > 0) apply_column_fluid(h, chg, -d);
-        // rebuild the CSR
+        // the transpose and tile plan are derived from the old CSR: free them first
+        // (rebuilt by the next call that needs them), then allocate every buffer of
+        // the new CSR before the state is touched, so that a failure (OOM) leaves
+        // graph and fluid as they were
+        free_transpose(g);
         int64_t *deg = nullptr, *nrp = nullptr, *cursor = nullptr;
         DI_CUDA(cudaMallocAsync(&deg, (n > 0 ? n : 1) * sizeof(int64_t), st));
         track(deg);
         DI_CUDA(cudaMallocAsync(&cursor, (n > 0 ? n : 1) * sizeof(int64_t), st));
         track(cursor);
         DI_CUDA(cudaMallocAsync(&nrp, (n + 1) * sizeof(int64_t), st));
+        track(nrp);
         if (n > 0) {
             k_new_deg<<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, del, chg, addcnt, n, deg);
             count_launch();
@@ -440,8 +444,14 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         int32_t *ncol = nullptr;
         void *nwt = nullptr;
         DI_CUDA(cudaMallocAsync(&ncol, (m2 > 0 ? m2 : 1) * sizeof(int32_t), st));
+        track(ncol);
         const size_t es = g.w_kind == DI_W_F64 ? 8 : (g.w_kind == DI_W_F32 ? 4 : 0);
-        if (es) DI_CUDA(cudaMallocAsync(&nwt, (m2 > 0 ? m2 : 1) * es, st));
+        if (es) {
+            DI_CUDA(cudaMallocAsync(&nwt, (m2 > 0 ? m2 : 1) * es, st));
+            track(nwt);
+        }
+        // every allocation done.  Theorem 4, first half: withdraw d P H over the old changed columns
+        if (state && n > 0) apply_column_fluid(h, chg, -d);
         if (n > 0) {
             if (g.w_kind == DI_W_F64)
                 k_copy_kept<double><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, del, chg,
@@ -460,8 +470,9 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         }
         DI_CUDA(cudaGetLastError());
         DI_CUDA(cudaStreamSynchronize(st));
-        // swap in the new CSR, recompute the scales of changed rows
-        free_transpose(g);
+        // swap in the new CSR (no longer temporaries), recompute the scales of changed rows
+        tmp.erase(std::remove_if(tmp.begin(), tmp.end(), [&](void *p) { return p == nrp || p == ncol || p == nwt; }),
+                  tmp.end());
         cudaFree(g.row_ptr);
         cudaFree(g.col);
         cudaFree(g.w);

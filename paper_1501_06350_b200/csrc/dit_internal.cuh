@@ -49,6 +49,7 @@ struct Ctrl {
     SweepRec *hist;                     // per-sweep records (device), kHistCap entries
     double n_global;                    // n of the whole graph (threshold denominator)
     double *stats_out;                  // shard mode: local {r, fmax, leak, sel_edges} go here
+    double gleak;                       // shard mode: leak summed over ranks (k_control), -1 before
     unsigned long long last_sel_edges;  // frontier out-edges of the last sweep
     int stats_is_init;
     unsigned int done;
@@ -138,9 +139,16 @@ struct TilePlan {
     int64_t *chunk_start = nullptr;  // [nchunk+1] first heavy edge of each chunk
     int64_t *seg_start = nullptr;  // [nseg+1] first heavy edge of each segment
     int64_t *cfirst = nullptr;     // [nchunk+1] first segment of each chunk
-    int32_t *run_h = nullptr;      // [nrun] heavy index of each run (high bit: first run of the target)
+    int32_t *run_h = nullptr;      // [nrun] heavy index of each run
     int64_t *run_seg = nullptr;    // [nrun+1] first segment of each run
-    std::vector<int64_t> s_chunk, s_run;   // per (wave, stripe) group [W S + 1]: first chunk, first run
+    // fold order: heavy targets grouped by wave (wave_slot), each with its runs in
+    // stripe order: runs fold_run[fold_ptr[i] .. fold_ptr[i+1]) of target fold_h[i]
+    int64_t *fold_ptr = nullptr;   // [nh+1]
+    int32_t *fold_h = nullptr;     // [nh]
+    uint32_t *fold_run = nullptr;  // [nrun]
+    std::vector<int64_t> wave_slot;   // [waves+1]
+    int *hticket = nullptr;        // chunk tickets of k_heavy (one per wave)
+    std::vector<int64_t> s_chunk;  // per (wave, stripe) group [W S + 1]: first chunk
     int waves = 1;                 // tile waves per sweep (R15): wave of tile t = t % waves
     int64_t nstripe = 0;           // source stripes S
     double *tpart = nullptr;       // k_tile partials [2][waves][grid]
@@ -260,7 +268,7 @@ void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int ns
                     int mem);
 void shard_sweep(di_graph *h, double *ghost_out);
 void shard_apply(di_graph *h, const double *recv, int force);
-void shard_control(di_graph *h, const double *gstats, int force);
+void shard_control(di_graph *h, const double *gathered, int nranks, int force);
 void shard_reduce(di_graph *h);
 void shard_flush(di_graph *h, double *ghost_out);
 void shard_flush_apply(di_graph *h, const double *recv);

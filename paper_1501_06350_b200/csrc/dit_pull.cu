@@ -298,6 +298,7 @@ static size_t g_cub_cap[2][64] = {};
 
 void release_cub_scratch(int device) {
     if (device < 0 || device >= 64) return;
+    std::lock_guard<std::mutex> lock(scratch_mutex(device));   // no build on this device uses it meanwhile
     for (int sl = 0; sl < 2; ++sl) {
         if (g_cub_buf[sl][device]) cudaFree(g_cub_buf[sl][device]);
         g_cub_buf[sl][device] = nullptr;

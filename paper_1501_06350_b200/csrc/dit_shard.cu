@@ -126,7 +126,8 @@ __global__ void k_apply_seg(double *__restrict__ F, const int32_t *__restrict__ 
         F[idx[q]] += v[q];
 }
 
-__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m, int force);
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gathered, int nranks, int64_t m,
+                          int force);
 
 // Tiled shards: the ghost slots are heavy targets of the tile
 // plan's first wave.  di_shard_sweep runs wave 0's heavy gather (the previous
@@ -199,8 +200,8 @@ void shard_flush_apply(di_graph *h, const double *recv) {
     h->s.flushing = true;
 }
 
-void shard_control(di_graph *h, const double *gstats, int force) {
-    k_control<<<1, 32, 0, h->stream>>>(h->s.ctrl, gstats, h->g.m, force);
+void shard_control(di_graph *h, const double *gathered, int nranks, int force) {
+    k_control<<<1, 32, 0, h->stream>>>(h->s.ctrl, gathered, nranks, h->g.m, force);
     count_launch();
     DI_CUDA(cudaGetLastError());
 }

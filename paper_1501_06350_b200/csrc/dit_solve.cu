@@ -252,10 +252,19 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double *__restrict__ 
     finalize_control(ctrl, r, fm, is_init, m);
 }
 
-// shard mode: control from the all-reduced {sum r, max fm} (gstats[0], gstats[1])
-__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gstats, int64_t m, int force) {
+// shard mode: control from every rank's {r, fmax, leak, sel_edges}, gathered in
+// rank order: sum r, max fmax, sum leak (fixed order: every rank gets the same bits)
+__global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gathered, int nranks, int64_t m,
+                          int force) {
     if (threadIdx.x != 0 || (ctrl->done && !force)) return;
-    finalize_control(ctrl, gstats[0], gstats[1], ctrl->stats_is_init, m);
+    double r = 0.0, fm = 0.0, lk = 0.0;
+    for (int q = 0; q < nranks; ++q) {
+        r += gathered[4 * q];
+        fm = fmax(fm, gathered[4 * q + 1]);
+        lk += gathered[4 * q + 2];
+    }
+    ctrl->gleak = lk;
+    finalize_control(ctrl, r, fm, ctrl->stats_is_init, m);
 }
 
 // ---------------------------------------------------------------- output helpers
@@ -474,6 +483,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     c.hist = s.hist;
     c.n_global = (double)(g.n_global > 0 ? g.n_global : 1);
     c.stats_out = stats_out;
+    c.gleak = -1.0;
     *s.ctrl_host = c;
     DI_CUDA(cudaMemcpyAsync(s.ctrl, s.ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     s.launched = 0;
@@ -533,9 +543,11 @@ void fill_result(di_graph *h, const di_solve_opts &o, double tol, di_result *res
     if (res) {
         std::memset(res, 0, sizeof(*res));
         res->residual_l1 = g.n > 0 ? r.resid : 0.0;
-        res->leak = r.leak;
+        // a shard's bound and completion factor use the leak of the whole graph (§3.3)
+        const double leak = (g.shard && r.gleak >= 0.0) ? r.gleak : r.leak;
+        res->leak = leak;
         const bool comp = o.dangling == DI_DANGLING_COMPLETE;
-        const double den = comp ? (1.0 - s.d - s.d * r.leak) : (1.0 - s.d);
+        const double den = comp ? (1.0 - s.d - s.d * leak) : (1.0 - s.d);
         res->bound = res->residual_l1 / den;
         res->norm_factor = comp ? (1.0 - s.d) / den : 1.0;
         res->sweeps = (int64_t)r.sweeps;

@@ -425,10 +425,11 @@ __global__ void k_heavy_flags(const uint32_t *__restrict__ st, const uint32_t *_
 __global__ void k_heavy_index(const int64_t *__restrict__ runf, const int64_t *__restrict__ segf,
                               const int64_t *__restrict__ chkf, const int64_t *__restrict__ runid,
                               const int64_t *__restrict__ segid, const int64_t *__restrict__ chkid,
-                              const uint32_t *__restrict__ hh, int64_t mh, int64_t *__restrict__ seg_start,
+                              const uint32_t *__restrict__ hh, const uint32_t *__restrict__ st, int64_t mh,
+                              int64_t nstripe, int64_t nh, int64_t *__restrict__ seg_start,
                               int64_t *__restrict__ chunk_start, int64_t *__restrict__ cfirst,
                               int32_t *__restrict__ run_h, int64_t *__restrict__ run_seg,
-                              unsigned long long *__restrict__ frun) {
+                              uint32_t *__restrict__ rkey, uint32_t *__restrict__ rval) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
         if (segf[p]) seg_start[segid[p]] = p;
         if (chkf[p]) {
@@ -436,16 +437,31 @@ __global__ void k_heavy_index(const int64_t *__restrict__ runf, const int64_t *_
             cfirst[chkid[p]] = segid[p];
         }
         if (runf[p]) {
-            run_h[runid[p]] = (int32_t)hh[p];
-            run_seg[runid[p]] = segid[p];
-            atomicMin(&frun[hh[p]], (unsigned long long)runid[p]);   // the target's first (lowest-stripe) run
+            const int64_t r = runid[p];
+            run_h[r] = (int32_t)hh[p];
+            run_seg[r] = segid[p];
+            // fold order: by (wave of the target, heavy index); a stable sort keeps stripe order
+            rkey[r] = (uint32_t)((int64_t)(st[p] / nstripe) * nh + hh[p]);
+            rval[r] = (uint32_t)r;
         }
     }
 }
 
-__global__ void k_mark_first_run(const unsigned long long *__restrict__ frun, int64_t nh, int32_t *__restrict__ run_h) {
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += (int64_t)gridDim.x * blockDim.x)
-        run_h[frun[h]] |= (int32_t)0x80000000;
+// fold index: target slot of every sorted run position (flags on key changes)
+__global__ void k_fold_flags(const uint32_t *__restrict__ skey, int64_t nrun, int64_t *__restrict__ flag) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nrun; p += (int64_t)gridDim.x * blockDim.x)
+        flag[p] = (p == 0 || skey[p - 1] != skey[p]) ? 1 : 0;
+}
+
+__global__ void k_fold_index(const uint32_t *__restrict__ skey, const int64_t *__restrict__ flag,
+                             const int64_t *__restrict__ slot, int64_t nrun, int64_t nh, int64_t *__restrict__ fold_ptr,
+                             int32_t *__restrict__ fold_h, unsigned long long *__restrict__ wave_first) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nrun; p += (int64_t)gridDim.x * blockDim.x)
+        if (flag[p]) {
+            fold_ptr[slot[p]] = p;
+            fold_h[slot[p]] = (int32_t)(skey[p] % (uint32_t)nh);
+            atomicMin(&wave_first[skey[p] / (uint32_t)nh], (unsigned long long)slot[p]);
+        }
 }
 
 __global__ void k_fill_u64(unsigned long long *__restrict__ p, int64_t cnt, unsigned long long v) {
@@ -622,7 +638,8 @@ void free_tiles(TilePlan &t) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
                     (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
-                    (void *)t.hsum, (void *)t.tpart})
+                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run,
+                    (void *)t.hticket})
         cudaFree(p);
     t = TilePlan();
 }
@@ -665,11 +682,13 @@ static void build_tiles_t(di_graph *h) {
     phase_mark(st, "tiles: start");
     tp.ntile = (n + kNodeTile - 1) / kNodeTile;
     tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
+    if (const char *e = getenv("DIT_STRIPE_NODES")) tp.stripe_nodes = std::max<int64_t>(kNodeTile, atoll(e));   // tests
     const int64_t nS = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
     tp.nstripe = nS;
     tp.waves = kTileWaves;                           // shards too (R16: cross-rank pushes wait a sweep)
     if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = std::max(1, atoi(e));
-    tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(tp.waves, tp.ntile));   // empty waves dropped
+    // empty waves dropped; at most 32 (the per-wave totals of k_tile's partials array)
+    tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(tp.waves, 32), tp.ntile));
     const int64_t S = tp.waves * nS;                 // heavy groups (wave, stripe)
     // ---- classes of the in-edges
     int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
@@ -685,7 +704,7 @@ static void build_tiles_t(di_graph *h) {
     }
     // local rank of every CSC position among its target's local in-edges: a scan of
     // local flags (32-bit through CUB when m < 2^31, else 64-bit)
-    const bool l32 = m < (int64_t)0x7fffffff;
+    const bool l32 = m < (int64_t)0x7fffffff && !getenv("DIT_FORCE_L64");   // DIT_FORCE_L64: tests of the 64-bit path
     void *L = nullptr;
     {
         const size_t ls = l32 ? sizeof(uint32_t) : sizeof(int64_t);
@@ -794,7 +813,6 @@ static void build_tiles_t(di_graph *h) {
     phase_mark(st, "tiles: split edges");
     // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
     tp.s_chunk.assign(S + 1, 0);
-    tp.s_run.assign(S + 1, 0);
     if (tp.mh > 0) {
         auto sorted = radix_sort_u32(k0, v0, k1, v1, tp.mh, bits_for(S + 1), st);
         uint32_t *skey = sorted.first, *sval = sorted.second;
@@ -844,28 +862,57 @@ static void build_tiles_t(di_graph *h) {
         DI_CUDA(cudaMallocAsync(&tp.run_h, tp.nrun * sizeof(int32_t), st));
         DI_CUDA(cudaMallocAsync(&tp.run_seg, (tp.nrun + 1) * sizeof(int64_t), st));
         DI_CUDA(cudaMallocAsync(&tp.part, tp.nseg * sizeof(double), st));
-        unsigned long long *frun;
-        DI_CUDA(cudaMallocAsync(&frun, tp.nh * sizeof(unsigned long long), st));
-        k_fill_u64<<<grid_for(h, tp.nh), 256, 0, st>>>(frun, tp.nh, ~0ull);
-        k_heavy_index<<<grid_for(h, tp.mh), 256, 0, st>>>(runf, segf, chkf, runid, segid, chkid, hh, tp.mh,
-                                                          tp.seg_start, tp.chunk_start, tp.cfirst, tp.run_h,
-                                                          tp.run_seg, frun);
-        k_mark_first_run<<<grid_for(h, tp.nh), 256, 0, st>>>(frun, tp.nh, tp.run_h);
-        count_launch(3);
+        uint32_t *rk0, *rv0, *rk1, *rv1;
+        for (uint32_t **p : {&rk0, &rv0, &rk1, &rv1}) DI_CUDA(cudaMallocAsync(p, tp.nrun * sizeof(uint32_t), st));
+        k_heavy_index<<<grid_for(h, tp.mh), 256, 0, st>>>(runf, segf, chkf, runid, segid, chkid, hh, skey, tp.mh, nS,
+                                                          tp.nh, tp.seg_start, tp.chunk_start, tp.cfirst, tp.run_h,
+                                                          tp.run_seg, rk0, rv0);
+        count_launch();
+        if ((int64_t)tp.waves * tp.nh >= (int64_t)0xffffffffLL) {
+            set_error("tiled plan: too many heavy targets for one graph handle");
+            throw Fail{DI_ERR_INVALID};
+        }
+        // the heavy targets of each wave, each with its runs in stripe order (k_heavy_fold)
+        {
+            auto fs = radix_sort_u32(rk0, rv0, rk1, rv1, tp.nrun, bits_for((int64_t)tp.waves * tp.nh + 1), st);
+            int64_t *ff, *fslot;
+            DI_CUDA(cudaMallocAsync(&ff, (tp.nrun + 1) * sizeof(int64_t), st));
+            DI_CUDA(cudaMallocAsync(&fslot, (tp.nrun + 1) * sizeof(int64_t), st));
+            k_fold_flags<<<grid_for(h, tp.nrun), 256, 0, st>>>(fs.first, tp.nrun, ff);
+            exclusive_scan_i64(ff, fslot, tp.nrun, st);
+            const int64_t nslot = read_i64(fslot + tp.nrun, st);
+            DI_CUDA(cudaMallocAsync(&tp.fold_ptr, (nslot + 1) * sizeof(int64_t), st));
+            DI_CUDA(cudaMallocAsync(&tp.fold_h, (nslot + 1) * sizeof(int32_t), st));
+            DI_CUDA(cudaMallocAsync(&tp.fold_run, tp.nrun * sizeof(uint32_t), st));
+            unsigned long long *wf;
+            DI_CUDA(cudaMallocAsync(&wf, (tp.waves + 1) * sizeof(unsigned long long), st));
+            k_fill_u64<<<1, 64, 0, st>>>(wf, tp.waves + 1, (unsigned long long)nslot);
+            k_fold_index<<<grid_for(h, tp.nrun), 256, 0, st>>>(fs.first, ff, fslot, tp.nrun, tp.nh, tp.fold_ptr,
+                                                               tp.fold_h, wf);
+            count_launch(3);
+            DI_CUDA(cudaMemcpyAsync(tp.fold_run, fs.second, tp.nrun * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+            DI_CUDA(cudaMemcpyAsync(tp.fold_ptr + nslot, &tp.nrun, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            std::vector<unsigned long long> w(tp.waves + 1);
+            DI_CUDA(cudaMemcpyAsync(w.data(), wf, (tp.waves + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                    st));
+            DI_CUDA(cudaStreamSynchronize(st));
+            tp.wave_slot.assign(tp.waves + 1, nslot);
+            for (int c = tp.waves - 1; c >= 0; --c) tp.wave_slot[c] = std::min<int64_t>((int64_t)w[c], tp.wave_slot[c + 1]);
+            for (void *p : {(void *)ff, (void *)fslot, (void *)wf, (void *)rk0, (void *)rv0, (void *)rk1, (void *)rv1})
+                DI_CUDA(cudaFreeAsync(p, st));
+        }
         DI_CUDA(cudaMemcpyAsync(tp.seg_start + tp.nseg, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         DI_CUDA(cudaMemcpyAsync(tp.chunk_start + tp.nchunk, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         DI_CUDA(cudaMemcpyAsync(tp.cfirst + tp.nchunk, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         DI_CUDA(cudaMemcpyAsync(tp.run_seg + tp.nrun, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
         phase_mark(st, "heavy: index");
-        // first run of every stripe
-        for (int64_t s = 0; s < S; ++s) tp.s_run[s] = sbeg[s] < tp.mh ? read_i64(runid + sbeg[s], st) : tp.nrun;
-        tp.s_run[S] = tp.nrun;
         for (int64_t *p : {runf, segf, chkf, runid, segid, chkid, sbeg_d}) DI_CUDA(cudaFreeAsync(p, st));
-        DI_CUDA(cudaFreeAsync(frun, st));
         DI_CUDA(cudaFreeAsync(scnt, st));
     }
     phase_mark(st, "tiles: heavy sort + index");
     DI_CUDA(cudaMallocAsync(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double), st));
+    DI_CUDA(cudaMallocAsync(&tp.hticket, 64 * sizeof(int), st));
+    DI_CUDA(cudaMemsetAsync(tp.hticket, 0, 64 * sizeof(int), st));
     DI_CUDA(cudaMallocAsync(&tp.tpart, (2 * (size_t)tp.waves * 4096 + 64) * sizeof(double), st));
     unsigned long long *mx;
     DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
@@ -900,64 +947,41 @@ void build_tiles(di_graph *h) {
 }
 
 // ---------------------------------------------------------------- heavy remote sums
-// One launch per stripe s (and one more after the last): first the previous
-// stripe's runs are folded into hsum (run order = target order within the
-// stripe; a target's first run sets, later stripes add: fixed order), then
-// the chunks of stripe s: CTA per chunk stages A(src) w of its edges in
-// shared memory, warp per segment sums (lane-strided + fixed butterfly).
-// fold the runs [q0, q1) of a finished stripe into hsum (lane per run; long runs
-// by the whole warp): a target's first run sets, later stripes add (fixed order)
-__device__ __forceinline__ void heavy_fold(int64_t q0, int64_t q1, const int32_t *__restrict__ run_h,
-                                           const int64_t *__restrict__ run_seg, const double *__restrict__ part,
-                                           double *__restrict__ hsum) {
-    const unsigned lane = lane_id();
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = q0 + gw * 32; base < q1; base += nw * 32) {
-        const int64_t q = base + lane;
-        int64_t sb = 0, se = 0;
-        int32_t hv = 0;
-        if (q < q1) {
-            sb = run_seg[q];
-            se = run_seg[q + 1];
-            hv = run_h[q];
-        }
-        const int cnt = (int)(se - sb);
-        if (cnt > 0 && cnt < 32) {
-            double acc = 0.0;
-            for (int64_t s = sb; s < se; ++s) acc += part[s];
-            const int32_t hx = hv & 0x7fffffff;
-            hsum[hx] = (hv < 0) ? acc : hsum[hx] + acc;
-        }
-        unsigned big = __ballot_sync(0xffffffffu, cnt >= 32);
-        while (big) {
-            const int b = __ffs(big) - 1;
-            big &= big - 1;
-            const int64_t bb = __shfl_sync(0xffffffffu, sb, b), be = __shfl_sync(0xffffffffu, se, b);
-            const int32_t bh = __shfl_sync(0xffffffffu, hv, b);
-            double acc = 0.0;
-            for (int64_t s = bb + lane; s < be; s += 32) acc += part[s];
-            acc = warp_sum(acc);
-            if (lane == 0) {
-                const int32_t hx = bh & 0x7fffffff;
-                hsum[hx] = (bh < 0) ? acc : hsum[hx] + acc;
-            }
-        }
-    }
-}
+// Heavy targets' remote inflow, per wave, in two launches:
+//   k_heavy_chunks -- persistent CTAs take 2048-edge chunks of the wave's heavy
+//     edges by ticket, in (stripe, target, source) order, so that at any time the
+//     gathered slice of the outflow A is about one stripe (L2-resident); a CTA
+//     stages A(src) w of its chunk in shared memory, then one thread per short
+//     segment (target within chunk) / one warp per long one sums it into part;
+//   k_heavy_fold -- per heavy target of the wave, its runs (one per source
+//     stripe) and their segments summed in stripe / edge order into hsum.
+// Every sum has a fixed order whatever CTA takes which chunk: bitwise reproducible.
 
-// the chunks [c0, c1) of one stripe: CTA per chunk stages A(src) w of its edges in
-// shared memory, then one thread per short segment / one warp per long one sums it
+// the chunks [c0, c1) by ticket; CTA per chunk at a time
 template <typename W>
-__device__ __forceinline__ void heavy_chunks(const RemRec<W> *__restrict__ hrec,
-                                             const int64_t *__restrict__ chunk_start,
-                                             const int64_t *__restrict__ seg_start,
-                                             const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
-                                             const double *__restrict__ Aprev, const double *__restrict__ Afresh,
-                                             bool gather, int wave, int waves, int force, double *__restrict__ part,
-                                             double *vals, int *sbnd) {
+__global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__restrict__ hrec,
+                                                           const int64_t *__restrict__ chunk_start,
+                                                           const int64_t *__restrict__ seg_start,
+                                                           const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
+                                                           const double *__restrict__ A0, const double *__restrict__ A1,
+                                                           double *__restrict__ part, int wave, int waves,
+                                                           const Ctrl *__restrict__ ctrl, int force,
+                                                           int *__restrict__ ticket) {
+    __shared__ double vals[kHeavyChunk];
+    __shared__ int sbnd[kHeavyChunk + 1];
+    __shared__ int s_c;
+    if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
+    const bool gather = ctrl->gather != 0;
+    if (force ? !gather : (!gather && wave == 0)) return;
+    // the previous sweep wrote A[(sweeps - 1) & 1], this sweep's earlier waves A[sweeps & 1]
+    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
+    const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
     const unsigned w = threadIdx.x >> 5, lane = lane_id();
-    for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
+    for (;;) {
+        if (threadIdx.x == 0) s_c = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int64_t c = c0 + s_c;
+        if (c >= c1) break;
         const int64_t e0 = chunk_start[c];
         const int cnt = (int)(chunk_start[c + 1] - e0);
         const int64_t sg0 = cfirst[c];
@@ -1002,29 +1026,55 @@ __device__ __forceinline__ void heavy_chunks(const RemRec<W> *__restrict__ hrec,
     }
 }
 
-// One launch per stripe s (and one more after the last): first the previous
-// stripe's runs are folded into hsum, then the chunks of stripe s.
-template <typename W>
-__global__ void __launch_bounds__(kThreads) k_heavy_s(const RemRec<W> *__restrict__ hrec,
-                                                      const int64_t *__restrict__ chunk_start,
-                                                      const int64_t *__restrict__ seg_start,
-                                                      const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
-                                                      const int32_t *__restrict__ run_h,
-                                                      const int64_t *__restrict__ run_seg, int64_t q0, int64_t q1,
-                                                      const double *__restrict__ A0, const double *__restrict__ A1,
-                                                      double *__restrict__ part, double *__restrict__ hsum,
-                                                      int wave, int waves, const Ctrl *__restrict__ ctrl, int force) {
-    __shared__ double vals[kHeavyChunk];
-    __shared__ int sbnd[kHeavyChunk + 1];
+// hsum of the wave's heavy targets [t0, t1) (fold slots): lane per target, a
+// warp per target of more than 64 segments; resets the wave's ticket
+__global__ void __launch_bounds__(kThreads) k_heavy_fold(const int64_t *__restrict__ fold_ptr,
+                                                         const int32_t *__restrict__ fold_h,
+                                                         const uint32_t *__restrict__ fold_run,
+                                                         const int64_t *__restrict__ run_seg,
+                                                         const double *__restrict__ part, double *__restrict__ hsum,
+                                                         int64_t t0, int64_t t1, int wave, const Ctrl *__restrict__ ctrl,
+                                                         int force, int *__restrict__ ticket) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;   // k_heavy_chunks of this wave is done (stream order)
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
     const bool gather = ctrl->gather != 0;
     if (force ? !gather : (!gather && wave == 0)) return;
-    // the previous sweep wrote A[(sweeps - 1) & 1], this sweep's earlier waves A[sweeps & 1]
-    const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
-    const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
-    heavy_fold(q0, q1, run_h, run_seg, part, hsum);
-    heavy_chunks<W>(hrec, chunk_start, seg_start, cfirst, c0, c1, Aprev, Afresh, gather, wave, waves, force, part,
-                    vals, sbnd);
+    const unsigned lane = lane_id();
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = t0 + gw * 32; base < t1; base += nw * 32) {
+        const int64_t i = base + lane;
+        int64_t r0 = 0, r1 = 0, nseg = 0;
+        if (i < t1) {
+            r0 = fold_ptr[i];
+            r1 = fold_ptr[i + 1];
+            for (int64_t r = r0; r < r1; ++r) nseg += run_seg[fold_run[r] + 1] - run_seg[fold_run[r]];
+        }
+        if (i < t1 && nseg <= 64) {
+            double acc = 0.0;
+            for (int64_t r = r0; r < r1; ++r) {
+                const uint32_t q = fold_run[r];
+                double rs = 0.0;
+                for (int64_t s = run_seg[q]; s < run_seg[q + 1]; ++s) rs += part[s];
+                acc += rs;
+            }
+            hsum[fold_h[i]] = acc;
+        }
+        unsigned big = __ballot_sync(0xffffffffu, i < t1 && nseg > 64);
+        while (big) {
+            const int l = __ffs(big) - 1;
+            big &= big - 1;
+            const int64_t b0 = __shfl_sync(0xffffffffu, r0, l), b1 = __shfl_sync(0xffffffffu, r1, l);
+            double acc = 0.0;
+            for (int64_t r = b0; r < b1; ++r) {
+                const uint32_t q = fold_run[r];
+                double rs = 0.0;
+                for (int64_t s = run_seg[q] + lane; s < run_seg[q + 1]; s += 32) rs += part[s];
+                acc += warp_sum(rs);
+            }
+            if (lane == 0) hsum[fold_h[base + l]] = acc;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- tile kernel
@@ -1690,35 +1740,38 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     return a;
 }
 
-// resident CTAs of k_heavy_s per SM: its grids are exactly one wave
+// resident CTAs of k_heavy_chunks per SM (its grid is exactly one wave of CTAs)
 template <typename W>
 static int heavy_ctas_per_sm() {
     static int v = 0;
     if (!v) {
-        DI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_heavy_s<W>, kThreads, 0));
+        DI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_heavy_chunks<W>, kThreads, 0));
         if (v < 1) v = 1;
     }
     return v;
 }
 
-// the heavy targets' remote inflow hsum of one wave: one launch per stripe + the last fold
+// the heavy targets' remote inflow hsum of one wave: chunks by ticket, then the fold
 template <typename W>
 static void launch_heavy_t(di_graph *h, int wave, int force) {
     TilePlan &tp = h->g.tl;
     State &s = h->s;
     if (tp.nh == 0) return;
     const int64_t S = tp.nstripe, g0 = (int64_t)wave * S;
-    for (int64_t st = 0; st <= S; ++st) {
-        const int64_t c0 = st < S ? tp.s_chunk[g0 + st] : 0, c1 = st < S ? tp.s_chunk[g0 + st + 1] : 0;
-        const int64_t q0 = st > 0 ? tp.s_run[g0 + st - 1] : 0, q1 = st > 0 ? tp.s_run[g0 + st] : 0;
-        const int64_t work = std::max<int64_t>(c1 - c0, (q1 - q0 + 255) / 256);
-        if (work == 0) continue;
-        const int grid = (int)std::min<int64_t>(work, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
-        k_heavy_s<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
-                                                       tp.cfirst, c0, c1, tp.run_h, tp.run_seg, q0, q1, s.A, s.A2,
-                                                       tp.part, tp.hsum, wave, tp.waves, s.ctrl, force);
+    const int64_t c0 = tp.s_chunk[g0], c1 = tp.s_chunk[g0 + S];
+    const int64_t t0 = tp.wave_slot[wave], t1 = tp.wave_slot[wave + 1];
+    if (c1 > c0) {
+        const int grid = (int)std::min<int64_t>(c1 - c0, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
+        k_heavy_chunks<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
+                                                            tp.cfirst, c0, c1, s.A, s.A2, tp.part, wave, tp.waves,
+                                                            s.ctrl, force, tp.hticket + wave);
         count_launch();
     }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((t1 - t0 + kThreads - 1) / kThreads,
+                                                                 (int64_t)h->num_sms * 8));
+    k_heavy_fold<<<grid, kThreads, 0, h->stream>>>(tp.fold_ptr, tp.fold_h, tp.fold_run, tp.run_seg, tp.part, tp.hsum,
+                                                   t0, t1, wave, s.ctrl, force, tp.hticket + wave);
+    count_launch();
 }
 
 template <typename W>

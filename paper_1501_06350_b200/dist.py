@@ -40,13 +40,16 @@ class CudaShard:
             _lib.di_shard_ghost_ids(self.h, self.ghost_ids)
         self.send = torch.zeros(max(self.n_ghost, 1), dtype=torch.float64, device=self.dev)
         self.stats = torch.zeros(4, dtype=torch.float64, device=self.dev)
-        self.gstats = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        self.gathered = torch.zeros(4, dtype=torch.float64, device=self.dev)   # [world][4], sized by the plan
+        self.world = 1
         self.recv = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.send_counts = None
         self.recv_counts = None
 
     # --- exchange plan
     def set_recv(self, local_idx, seg_counts):
+        self.world = len(seg_counts)
+        self.gathered = torch.zeros(4 * self.world, dtype=torch.float64, device=self.dev)
         _lib.di_shard_set_recv(self.h, local_idx, seg_counts)
         self.recv = torch.zeros(max(int(sum(seg_counts)), 1), dtype=torch.float64, device=self.dev)
         self.recv_counts = [int(c) for c in seg_counts]
@@ -56,7 +59,11 @@ class CudaShard:
         _lib.di_shard_begin(self.h, d, None, tol, self.stats, **opts)
 
     def control(self):
-        _lib.di_shard_control(self.h, self.gstats)
+        _lib.di_shard_control(self.h, self.gathered, self.world)
+
+    def global_residual(self):
+        """sum over ranks of |F|_1 from the last gathered stats (host read, for chunk sizing)"""
+        return float(self.gathered.view(self.world, 4)[:, 0].sum().item())
 
     def sweep(self):
         _lib.di_shard_sweep(self.h, self.send)
@@ -115,10 +122,10 @@ class TorchCollectives:
         s.set_recv((recv_ids - s.lo).to(torch.int32), recv_counts.tolist())
 
     def allreduce_stats(self, shards):
+        # one collective per sweep: every rank's {|F|_1, max|F|, leak, edges}, reduced on
+        # the device in rank order by di_shard_control (deterministic, identical on all ranks)
         (s,) = shards
-        s.gstats.copy_(s.stats[:2])
-        self.dist.all_reduce(s.gstats[0:1], op=self.dist.ReduceOp.SUM, group=self.group)
-        self.dist.all_reduce(s.gstats[1:2], op=self.dist.ReduceOp.MAX, group=self.group)
+        self.dist.all_gather_into_tensor(s.gathered, s.stats, group=self.group)
 
     def alltoall(self, shards):
         (s,) = shards
@@ -142,8 +149,8 @@ class TorchCollectives:
 def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
     """Cold sharded solve; returns (list of local H tensors, list of local result dicts).
 
-    Per sweep: sweep -> all-to-all(ghost fluid) -> apply -> reduce -> all-reduce
-    (sum |F|_1, max |F|) -> control.  The host polls `done` once per chunk.
+    Per sweep: sweep -> all-to-all(ghost fluid) -> apply -> reduce -> all-gather
+    of the ranks' {|F|_1, max |F|, leak} -> control (reduced on the device).  The host polls `done` once per chunk.
     The tiled schedule (variant 3) leaves the last sweep's remote pushes
     pending (R13): once done, they are exchanged and applied like a
     sweep (flush -> all-to-all -> flush_apply -> all-reduce -> control), and
@@ -184,7 +191,7 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
             raise RuntimeError("ranks disagree on convergence")
         # next chunk from the decay of the global residual (identical on every rank,
         # so the ranks stay in lock step): the sweeps still needed to reach tol
-        r = float(shards[0].gstats[0].item())
+        r = shards[0].global_residual()
         nxt = min(chunk * 2, max_chunk)
         if r_prev is not None and 0.0 < r < r_prev and tol > 0.0:
             rate = (r / r_prev) ** (1.0 / (swept - s_prev))
@@ -197,14 +204,28 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
 
 
 # ------------------------------------------------------------------ bench (torchrun)
+def bench_spec(world, config, scale_n=None):
+    """The sharded bench's workload: BASELINE configs[3] (400M nodes, ~8B weighted
+    edges, int64 row offsets) over 8 GPUs; at 2 / 4 GPUs the same generator on
+    world x 50M nodes (weak-scaling slices: 50M nodes, ~1B edges per GPU, the
+    shape of one configs[3] rank).  Returns (spec, workload name)."""
+    import synth
+    base = synth.CONFIGS[3] if config in (2, 3) else synth.CONFIGS[config]
+    per = scale_n or synth.CONFIGS[2].n
+    if config in (2, 3) and scale_n is None and world * per == base.n:
+        return base, f"{base.name} (BASELINE configs[3]) over {world} GPUs"
+    spec = base.scaled(per * world)
+    return spec, f"{base.name} generator, {world} x {per} nodes (weak-scaling slice of configs[3])"
+
+
 def bench_sharded(args, metric, tools):
-    """bench.py --gpus N under torchrun: weak scaling, each rank owns the rows of
-    a configs[2]-shaped slice (50M nodes, ~1B edges per GPU).  `tools` carries
-    bench.py's clock sampler, roofline arithmetic and pinned allocator
-    (measurement plumbing only)."""
+    """bench.py --gpus N under torchrun (bench.py re-executes itself under
+    torch.distributed.run when started without it): weak scaling, each rank owns
+    a contiguous 50M-node range with its ~1B out-edges (bench_spec).  `tools`
+    carries bench.py's clock sampler, roofline arithmetic, pinned allocator and
+    CPU-oracle timer (measurement plumbing only)."""
     import json
     import os
-    import time
 
     import torch.distributed as dist
 
@@ -214,9 +235,7 @@ def bench_sharded(args, metric, tools):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    base = synth.CONFIGS[args.config]
-    per = args.scale_n or base.n
-    spec = base.scaled(per * world)
+    spec, workload = bench_spec(world, args.config, args.scale_n)
     tol = args.tol if args.tol is not None else spec.tol
     bounds = node_ranges(spec.n, world)
     lo, hi = bounds[rank], bounds[rank + 1]
@@ -226,12 +245,8 @@ def bench_sharded(args, metric, tools):
     coll = TorchCollectives()
     coll.plan([sh], bounds)
     variant = args.variant
-    theta = args.theta
-    if variant == "tiled":
-        variant = _lib.SHARD_TILED_FALLBACK if not getattr(_lib, "SHARD_TILED", False) else "tiled"
-        if variant == "pull":
-            theta = 0.0
-    kw = dict(theta=theta, variant={"auto": 0, "push": 1, "pull": 2, "tiled": 3}[variant], local_rounds=args.rounds)
+    kw = dict(theta=args.theta, variant={"auto": 0, "push": 1, "pull": 2, "tiled": 3}[variant],
+              local_rounds=args.rounds)
     for _ in range(args.warmup):
         solve([sh], coll, d=spec.d, tol=tol, **kw)
     torch.cuda.synchronize()
@@ -258,6 +273,7 @@ def bench_sharded(args, metric, tools):
     ms_max = coll.allreduce_max([ms], stream.device)[0]
     edges = coll.allreduce_sum([float(sum(r["diffused_edges"] for r in res))], stream.device)[0]
     cross = coll.allreduce_sum([float(sh.n_ghost), float(g.m)], stream.device)
+    plan = _lib.di_plan_stats(sh.h) if variant == "tiled" else None
     sh.close()                                 # the e2e shards below reuse its pooled memory
     torch.cuda.synchronize()
     # e2e: every rank builds its shard from pinned host buffers, solves and reads H back
@@ -296,19 +312,22 @@ def bench_sharded(args, metric, tools):
                                  stream.device)[0]
         e2e = {"value": e_edges / (e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(spec.n * 8), "ms_per_step": e_ms / args.e2e_steps}
+    dist.barrier()
     if rank == 0:
+        cpu = None if args.no_cpu else tools["cpu_baseline"](args)
         line = {"metric": metric, "value": edges / (ms_max / 1e3), "unit": "edges/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "time_to_tol_s": ms_max / args.steps / 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{spec.name} sharded, {per} nodes per GPU (weak scaling)", "n": spec.n,
-                           "m": int(cross[1]), "tol": tol, "theta": theta, "variant": variant,
-                           "local_rounds": args.rounds, "ghost_slots_total": int(cross[0]),
-                           "sweeps_per_solve": res[-1]["sweeps"],
+                "config": {"workload": workload, "n": spec.n, "m": int(cross[1]), "tol": tol, "theta": args.theta,
+                           "variant": variant, "local_rounds": args.rounds, "ghost_slots_total": int(cross[0]),
+                           "exchange_bytes_per_sweep": int(cross[0]) * 8,
+                           "sweeps_per_solve": res[-1]["sweeps"], "rank0_plan": plan,
                            "l2": "inputs larger than L2 (F 8n B, CSR ~8m B >> 126 MB); no flush",
-                           "parallelism": f"node-range partition x{world}, NCCL all-to-all + all-reduce"},
-                "roofline": tools["roofline"](prof_tot, spec.name, variant), "cpu_baseline": None, "e2e": e2e,
+                           "parallelism": f"node-range partition x{world}, NCCL all-to-all + all-gather"},
+                "roofline": tools["roofline"](prof_tot, spec.name, variant), "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
+    dist.barrier()
     dist.destroy_process_group()
     return 0

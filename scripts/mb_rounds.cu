@@ -85,10 +85,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_rounds(const uint16_t *__res
 
 template <int kWarps, bool kIntConv>
 void run(const char *name, const uint16_t *dsrc, const float *dw, int K, int tiles, int rounds, double *dout,
-         unsigned long long *dcyc, int nsm) {
+         unsigned long long *dcyc, int nsm, int ctas_per_sm = 1) {
     const int S = kVW * 32 * K;
     const size_t smem = ((S * 2 + 15) & ~15) + (size_t)S * 4 + (kNode + 2) * 8 + 1024 * 8;
     cudaFuncSetAttribute(k_rounds<kWarps, kIntConv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    nsm *= ctas_per_sm;
     k_rounds<kWarps, kIntConv><<<nsm, kWarps * 32, smem>>>(dsrc, dw, K, 2, rounds, dout, dcyc);   // warm
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -110,7 +111,7 @@ void run(const char *name, const uint16_t *dsrc, const float *dw, int K, int til
     cm /= nsm;
     const double edges = (double)S * rounds * tiles;
     printf("%-40s K=%2d smem=%6zu  %8.1f cycles/tile (%6.1f /round)  %.3f edges/cycle/SM  %.3f ms\n", name, K, smem,
-           cm / tiles, cm / tiles / rounds, edges / cm, ms);
+           cm / tiles / ctas_per_sm, cm / tiles / rounds / ctas_per_sm, edges * ctas_per_sm / cm, ms);
 }
 
 int main() {
@@ -151,8 +152,8 @@ int main() {
     cudaMalloc(&dr, S * 2);
     cudaMalloc(&dc, S * 2);
     cudaMalloc(&dw, S * 4);
-    cudaMalloc(&dout, (size_t)nsm * 1024 * 8);
-    cudaMalloc(&dcyc, nsm * 8);
+    cudaMalloc(&dout, (size_t)nsm * 2 * 1024 * 8);
+    cudaMalloc(&dcyc, nsm * 2 * 8);
     cudaMemcpy(dr, src_r.data(), S * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dc, src_c.data(), S * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dw, w.data(), S * 4, cudaMemcpyHostToDevice);
@@ -160,17 +161,12 @@ int main() {
     cudaMalloc(&dh, S * 2);
     cudaMalloc(&db, S * 2);
     cudaMemcpy(db, src_b.data(), S * 2, cudaMemcpyHostToDevice);
-    for (int K : {8, 12}) {
-        heur(K);
-        cudaMemcpy(dh, src_h.data(), S * 2, cudaMemcpyHostToDevice);
-        run<16, false>("16 warps, random src, F2F", dr, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<16, true>("16 warps, random src, int conv", dr, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<16, true>("16 warps, half-warp distinct, int conv", dc, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<16, true>("16 warps, pairs per bank, int conv", db, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<16, true>("16 warps, heuristic order, int conv", dh, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<32, true>("32 warps, random src, int conv", dr, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<32, true>("32 warps, half-warp distinct, int conv", dc, dw, K, tiles, rounds, dout, dcyc, nsm);
-        run<32, true>("32 warps, heuristic order, int conv", dh, dw, K, tiles, rounds, dout, dcyc, nsm);
+    for (int K : {8}) {
+        run<16, false>("1 CTA x 16 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
+        run<16, false>("2 CTAs x 16 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
+        run<16, false>("1 CTA x 16 warps, half-warp distinct", dc, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
+        run<16, false>("2 CTAs x 16 warps, half-warp distinct", dc, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
+        run<32, false>("1 CTA x 32 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
     }
     return 0;
 }

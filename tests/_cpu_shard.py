@@ -30,13 +30,16 @@ class CpuShard:
         self.deg = deg
         self.send = torch.zeros(max(self.n_ghost, 1), dtype=torch.float64)
         self.stats = torch.zeros(4, dtype=torch.float64)
-        self.gstats = torch.zeros(2, dtype=torch.float64)
+        self.gathered = torch.zeros(4, dtype=torch.float64)
+        self.world = 1
         self.recv = torch.zeros(1, dtype=torch.float64)
         self.send_counts = self.recv_counts = None
 
     def set_recv(self, local_idx, seg_counts):
         self.recv_idx = np.asarray(local_idx, dtype=np.int64)
         self.recv_counts = [int(c) for c in seg_counts]
+        self.world = len(self.recv_counts)
+        self.gathered = torch.zeros(4 * self.world, dtype=torch.float64)
         self.recv = torch.zeros(max(sum(self.recv_counts), 1), dtype=torch.float64)
 
     def begin(self, d, tol, theta=1.0, max_sweeps=0, **_):
@@ -55,13 +58,15 @@ class CpuShard:
         a = np.abs(self.F[: self.n_local])
         self.stats[0] = float(a.sum())
         self.stats[1] = float(a.max()) if len(a) else 0.0
+        self.stats[2] = self.leak
         if count:
             self.sweeps += 1
 
     def control(self):
         if self.done:
             return
-        r, fm = float(self.gstats[0]), float(self.gstats[1])
+        g = self.gathered.view(self.world, 4).numpy()
+        r, fm = float(g[:, 0].sum()), float(g[:, 1].max())
         self.resid = r
         self.T = min(self.theta * r / self.n_global, fm)
         self.done = r <= self.tol or self.sweeps >= self.max_sweeps
@@ -92,6 +97,9 @@ class CpuShard:
 
     def poll(self):
         return self.done
+
+    def global_residual(self):
+        return float(self.gathered.view(self.world, 4)[:, 0].sum())
 
     def finish(self, tol, **_):
         return torch.from_numpy(self.H.copy()), {"residual_l1": self.resid, "sweeps": self.sweeps,

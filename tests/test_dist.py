@@ -88,3 +88,35 @@ def test_node_ranges_partition():
         b = node_ranges(n, w)
         assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(w))
         assert max(b[i + 1] - b[i] for i in range(w)) - min(b[i + 1] - b[i] for i in range(w)) <= 1
+
+
+def test_bench_spec_weak_scaling_and_config3():
+    # bench.py --gpus N: 8 ranks run BASELINE configs[3] itself (400M nodes, 50M per
+    # rank); 2 / 4 ranks the same generator on N x 50M nodes (weak-scaling slices)
+    from paper_1501_06350_b200.dist import bench_spec, node_ranges
+    s8, name8 = bench_spec(8, 2)
+    assert s8 == synth.CONFIGS[3] and "configs[3]" in name8 and "8 GPUs" in name8
+    b = node_ranges(s8.n, 8)
+    assert all(b[r + 1] - b[r] == 50_000_000 for r in range(8))
+    for w in (2, 4):
+        s, name = bench_spec(w, 2)
+        assert s.n == w * 50_000_000 and s.seed == synth.CONFIGS[3].seed and s.deg_cap == 5000
+        assert "weak-scaling slice" in name
+    s1, _ = bench_spec(2, 2, scale_n=1000)
+    assert s1.n == 2000
+
+
+def test_bench_relaunch_without_enough_gpus():
+    # without torchrun, bench.py --gpus N re-executes itself under torch.distributed.run;
+    # with fewer visible GPUs than N it says so on one JSON line and exits non-zero
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert p.returncode == 1
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert "error" in line and line["n_gpus"] == 2

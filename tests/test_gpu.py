@@ -370,3 +370,29 @@ def test_release_memory_then_rebuild(eng):
     H2, r2 = G.solve(d=D, tol=spec.tol, variant="tiled")
     assert np.array_equal(H1, H2.cpu().numpy()) and r1["sweeps"] == r2["sweeps"]
     G.close()
+
+
+@pytest.mark.parametrize("variant", ["pull", "tiled"])
+def test_completed_bound_and_norm_factor_exact(eng, variant):
+    # PAPER §3.3 (final display): with dangling completion the engine returns the
+    # normalised history (1-d)/(1-d-d l) H_k, and |x_completed - that|_1 is EXACTLY
+    # the returned bound |F_k|/(1-d-d l_k) (pinned on the oracle in test_oracle.py);
+    # a wrong leak, factor or denominator on the device breaks the equality
+    rng = np.random.default_rng(17)
+    n = 900
+    deg = rng.integers(0, 6, size=n)
+    deg[rng.random(n) < 0.15] = 0
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    col = rng.integers(0, n, size=rp[-1]).astype(np.int32)
+    cp, ri, pv = graph.column_entries(n, rp, col, None)
+    xc = dense.dense_solve(graph.dense_P(n, cp, ri, pv), D, synth.uniform_Z(n), completed=True)
+    G = eng.DIGraph(n, rp, col)
+    for k in (1, 3, 8):
+        H, res = G.solve(d=D, tol=0.0, variant=variant, theta=0.0, max_sweeps=k, dangling="complete")
+        F, Hraw, _, leak = G.state()
+        assert res["leak"] == pytest.approx(leak, rel=1e-15) and leak > 0
+        assert res["norm_factor"] == pytest.approx((1 - D) / (1 - D - D * leak), rel=1e-14)
+        assert np.allclose(H.cpu().numpy(), res["norm_factor"] * Hraw.cpu().numpy(), rtol=1e-15, atol=0)
+        assert res["bound"] == pytest.approx(np.abs(F.cpu().numpy()).sum() / (1 - D - D * leak), rel=1e-13)
+        assert np.abs(xc - H.cpu().numpy()).sum() == pytest.approx(res["bound"], rel=1e-9)

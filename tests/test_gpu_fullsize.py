@@ -1,0 +1,184 @@
+"""Full-size parity of the bench's workload (BASELINE configs[2]) and of the
+dynamic update (configs[4]) against the CPU oracle, plus the tiled plan's
+rarely taken build paths (several heavy source stripes, the 64-bit local-rank
+scan, our own LSD radix transpose) element by element.
+
+north_star: ||H_gpu - H_oracle||_1 <= 1e-9 with both solved to |F|_1 <= 1e-12
+(float64 fluid), top-1000 ranking identical (R9, R11).  The oracle
+is the single-threaded C frontier sweep (oracle/c/di_oracle.c, reading R1) on
+the full 1e9-edge graphs: a few minutes of host time per solve.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import di, graph
+
+pytestmark = pytest.mark.gpu
+D = 0.85
+L1_BAR = 1e-9
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1501_06350_b200 as eng
+    return eng
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return synth.generate(synth.CONFIGS[2])
+
+
+def assert_topk(h_gpu, h_ref, k, eps):
+    ia = np.argsort(-h_gpu, kind="stable")[:k]
+    ib = np.argsort(-h_ref, kind="stable")[:k]
+    for p in np.flatnonzero(ia != ib):
+        assert abs(h_ref[ia[p]] - h_ref[ib[p]]) <= eps, f"rank {p}: {ia[p]} vs {ib[p]}"
+
+
+def eq12_residual(n, row_ptr, col, w, H, d, chunk=1 << 27):
+    """Eq. (12) over EVERY node: r = F_0 + d P H - H with F_0 = (1-d)/n (uniform
+    Z), P from Eq. (1) (oracle arithmetic, float64, numpy, edge chunks).  For the
+    GPU's (F, H), r must be its F; Theorem 1 then bounds |x - H|_1 <= |r|_1/(1-d)."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    deg = np.diff(row_ptr)
+    m = int(row_ptr[-1])
+    wsum = np.zeros(n)
+    if w is None:
+        wsum[:] = deg
+    else:
+        for a in range(0, m, chunk):
+            b = min(m, a + chunk)
+            src = np.searchsorted(row_ptr, np.arange(a, b, dtype=np.int64), side="right") - 1
+            wsum += np.bincount(src, weights=w[a:b].astype(np.float64), minlength=n)
+    scale = np.where(wsum > 0, H / np.where(wsum > 0, wsum, 1.0), 0.0)
+    PH = np.zeros(n)
+    for a in range(0, m, chunk):
+        b = min(m, a + chunk)
+        src = np.searchsorted(row_ptr, np.arange(a, b, dtype=np.int64), side="right") - 1
+        c = scale[src]
+        if w is not None:
+            c = c * w[a:b].astype(np.float64)
+        PH += np.bincount(col[a:b], weights=c, minlength=n)
+    return (1.0 - d) / n + d * PH - H
+
+
+def test_config2_full_size_vs_oracle(eng, cfg2):
+    # the bench's workload and launch configuration (tiled, 4 local rounds, 2 waves)
+    g = cfg2
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    H, res = G.solve(d=D, tol=1e-12, variant="tiled", local_rounds=4)
+    assert res["converged"] and res["residual_l1"] <= 1e-12
+    F, Hs, _, _ = G.state()
+    H = H.cpu().numpy()
+    F = F.cpu().numpy()
+    G.close()
+    # the full-vector certificate: Eq. (12) holds at every node, so the returned
+    # residual is the true |F|_1 and Eq. (11) bounds the distance to x
+    # (float64 rounding of the products and sums: ~1e-16 of |H|_1 = 1 over all nodes)
+    r = eq12_residual(g.n, g.row_ptr, g.col, g.w, H, D)
+    assert np.abs(r - F).sum() <= 1e-13
+    assert np.abs(r).sum() <= 1e-12 + 1e-13
+    ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12, method="sweep")
+    assert ref.residual <= 1e-12
+    assert np.abs(H - ref.H).sum() <= L1_BAR
+    assert_topk(H, ref.H, 1000, 2 * (res["bound"] + ref.residual / (1 - D)))
+
+
+def test_config4_full_size_vs_cold_oracle(eng, cfg2):
+    # configs[4]: 1% of the configs[2] graph rewired; warm restart by Theorem 4
+    # (corrective fluid d (P' - P) H) against a cold oracle solve of the new graph
+    spec = synth.CONFIGS[4]
+    g = cfg2
+    delta = synth.rewire(spec, g, fraction=0.01, seed=4)
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    G.solve(d=D, tol=spec.tol, variant="tiled")
+    G.update_edges(**delta)
+    H, r = G.resume(tol=1e-12, variant="tiled")
+    assert r["converged"] and r["residual_l1"] <= 1e-12
+    F, _, _, _ = G.state()
+    H = H.cpu().numpy()
+    F = F.cpu().numpy()
+    G.close()
+    rp2, c2, w2, _ = graph.apply_delta(g.n, g.row_ptr, g.col, g.w, delta["add_src"], delta["add_dst"],
+                                       delta["add_w"], delta["rem_src"], delta["rem_dst"])
+    res12 = eq12_residual(g.n, rp2, c2, w2, H, D)
+    assert np.abs(res12 - F).sum() <= 1e-13
+    cold = di.di_solve(g.n, rp2, c2, w2, D, tol=1e-12, method="sweep")
+    assert np.abs(H - cold.H).sum() <= L1_BAR
+    assert_topk(H, cold.H, 1000, 2 * (r["bound"] + cold.residual / (1 - D)))
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _tiled_elementwise(eng, g, rounds, sweeps, stats_check=None):
+    cp, ri, pv = graph.column_entries(g.n, g.row_ptr, g.col, g.w)
+    st = di.di_init(g.n, D)
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    for k in sweeps:
+        _, res = G.solve(d=D, tol=0.0, variant="tiled", local_rounds=rounds, max_sweeps=k)
+        if stats_check:
+            stats_check(eng._lib.di_plan_stats(G.handle))
+            stats_check = None
+        F, H, _, leak = G.state()
+        r = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=eng._lib.DI_TILE_NODES, rounds=rounds, tol=0,
+                               max_sweeps=k, waves=eng._lib.DI_TILE_WAVES)
+        assert res["sweeps"] == k
+        assert np.allclose(H.cpu().numpy(), r.H, rtol=1e-12, atol=1e-22)
+        assert np.allclose(F.cpu().numpy(), r.F, rtol=1e-10, atol=1e-20)
+        assert leak == pytest.approx(r.leak, rel=1e-12, abs=1e-20)
+        assert res["diffused_edges"] == r.edges and res["diffused_nodes"] == r.nodes
+    G.close()
+
+
+def test_tiled_several_heavy_stripes_elementwise(eng):
+    # the heavy remote in-edges sorted by source stripe and folded stripe by stripe
+    # into hsum: at 1M nodes one default stripe (6.3M nodes) holds
+    # everything, so the stripe is shrunk to 200K nodes -> 5 stripes per wave
+    spec = synth.CONFIGS[1].scaled(1_000_000, seed=21, weighted=True)
+    g = synth.generate(spec)
+
+    def check(stats):
+        assert stats["stripes"] >= 3 and stats["heavy_edges"] > 0 and stats["heavy_runs"] > stats["heavy_targets"]
+
+    with _env(DIT_STRIPE_NODES=200_000):
+        _tiled_elementwise(eng, g, 4, (1, 2, 5), check)
+
+
+def test_tiled_64bit_scan_and_own_radix_elementwise(eng):
+    # the plan paths a 1e9-edge single graph never takes: the 64-bit local-rank scan
+    # (m >= 2^31 edges) and our own LSD radix transpose (DIT_OWN_RADIX)
+    spec = synth.CONFIGS[1].scaled(150_001, seed=22, weighted=True)
+    g = synth.generate(spec)
+    with _env(DIT_FORCE_L64=1, DIT_OWN_RADIX=1):
+        _tiled_elementwise(eng, g, 3, (1, 3))
+
+
+def test_tiled_edge_order_without_bank_balance(eng):
+    # the bank-aware slot order (k_ell_balance) only permutes summation order
+    # within pieces: both layouts match the oracle element-wise
+    spec = synth.CONFIGS[1].scaled(60_013, seed=23, weighted=True)
+    g = synth.generate(spec)
+    with _env(DIT_NO_BANK_ORDER=1):
+        _tiled_elementwise(eng, g, 4, (2,))
+    _tiled_elementwise(eng, g, 4, (2,))

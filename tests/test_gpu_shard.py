@@ -38,11 +38,9 @@ class LockstepCollectives:
         self.roff = [np.concatenate([[0], np.cumsum(s.recv_counts)]) for s in shards]
 
     def allreduce_stats(self, shards):
-        tot = sum(s.stats[0] for s in shards)
-        mx = torch.stack([s.stats[1] for s in shards]).max()
+        allst = torch.cat([s.stats for s in shards])        # the all-gather, rank order
         for s in shards:
-            s.gstats[0] = tot
-            s.gstats[1] = mx
+            s.gathered.copy_(allst)
 
     def alltoall(self, shards):
         for r, s in enumerate(shards):
@@ -86,6 +84,30 @@ def test_lockstep_shards_match_oracle(gpu, world, variant):
     assert np.abs(H - ref.H).sum() <= 1e-9
     assert len({r["sweeps"] for r in res}) == 1 and all(r["residual_l1"] <= 1e-12 for r in res)
     assert sum(s.n_ghost for s in shards) > 0
+    for s in shards:
+        s.close()
+
+
+@pytest.mark.parametrize("world,variant", [(2, 2), (3, 3)])
+def test_lockstep_shards_completion_uses_global_leak(gpu, world, variant):
+    # PAPER §3.3 on shards: every rank's completion factor (1-d)/(1-d-d l) and
+    # bound |F|/(1-d-d l) take the leak l of the WHOLE graph (all-gathered with
+    # the residual), so the concatenated H is the completed solution
+    from paper_1501_06350_b200 import DANGLING, dist
+    spec = synth.CONFIGS[1].scaled(60_000, seed=18, weighted=True)
+    shards, bounds = _shards(spec, world)
+    coll = LockstepCollectives()
+    coll.plan(shards, bounds)
+    Hs, res = dist.solve(shards, coll, d=D, tol=1e-12, variant=variant, dangling=DANGLING["complete"])
+    H = torch.cat(Hs).cpu().numpy()
+    g = synth.generate(spec)
+    ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12)
+    xc = di.normalized_history(ref.H, D, ref.leak)
+    assert abs(H.sum() - 1.0) <= 1e-9
+    assert np.abs(H - xc).sum() <= 1e-9
+    assert len({r["leak"] for r in res}) == 1 and res[0]["leak"] == pytest.approx(ref.leak, rel=1e-9)
+    assert len({r["norm_factor"] for r in res}) == 1
+    assert all(r["bound"] == pytest.approx(r["residual_l1"] / (1 - D - D * r["leak"]), rel=1e-15) for r in res)
     for s in shards:
         s.close()
 

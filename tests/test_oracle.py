@@ -446,3 +446,37 @@ def test_tiled_conservation_and_convergence(tile, rounds, waves, bounds):
     # more local rounds never need more sweeps than one round
     r1 = di.tiled_sweep_run(g.n, cp, ri, pv, D, st.F, st.H, tile=tile, rounds=1, tol=1e-13, waves=waves, bounds=bounds)
     assert r.steps <= r1.steps
+
+
+# ----------------------------------------------- §3.3 completed bound, pinned
+def test_bound_completed_hand_value():
+    # PAPER §3.3 final display |x - (1-d)/(1-d-d l) H| = |F|/(1-d-d l) with
+    # |F|_1 = 0.1, l = 0.05, d = 0.85: 0.1 / (0.15 - 0.0425) = 0.1 / 0.1075
+    assert di.bound_completed(np.array([0.04, -0.06]), 0.85, 0.05) == pytest.approx(0.9302325581395349, rel=1e-15)
+    # no leak: factor 1
+    assert di.normalized_history(np.array([1.0]), 0.85, 0.0)[0] == 1.0
+    # single dangling node after one step: H = 0.15, l = 0.15 -> factor 0.15 / 0.0225 = 20/3,
+    # normalised H = 1 = the completed solution (P completed = (1): x = 0.85 x + 0.15)
+    assert di.normalized_history(np.array([0.15]), 0.85, 0.15)[0] == pytest.approx(1.0, rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_bound_completed_is_the_exact_distance(seed):
+    # §3.3: "the exact L1 distance between x and the normalized H is equal to
+    # |F_k| / (1-d-d l_k)": against the dense completed solve (a wrong denominator
+    # or normalisation factor breaks the equality), at several intermediate steps
+    rng = np.random.default_rng(seed)
+    n = 40
+    deg = rng.integers(0, 4, size=n)
+    deg[rng.random(n) < 0.2] = 0
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    col = rng.integers(0, n, size=rp[-1]).astype(np.int32)
+    cp, ri, pv = graph.column_entries(n, rp, col, None)
+    xc = dense.dense_solve(graph.dense_P(n, cp, ri, pv), D, synth.uniform_Z(n), completed=True)
+    st = di.di_init(n, D)
+    for k in (1, 5, 17, 60):
+        r = di.seq_run(n, cp, ri, pv, D, st.F, st.H, sched="cyc", tol=0, max_steps=k)
+        dist = np.abs(xc - di.normalized_history(r.H, D, r.leak)).sum()
+        assert dist == pytest.approx(di.bound_completed(r.F, D, r.leak), rel=1e-12)
+        assert r.leak > 0 or k < 3
