@@ -147,7 +147,6 @@ struct TilePlan {
     int32_t *fold_h = nullptr;     // [nh]
     uint32_t *fold_run = nullptr;  // [nrun]
     std::vector<int64_t> wave_slot;   // [waves+1]
-    int *hticket = nullptr;        // chunk tickets of k_heavy (one per wave)
     std::vector<int64_t> s_chunk;  // per (wave, stripe) group [W S + 1]: first chunk
     int waves = 1;                 // tile waves per sweep (R15): wave of tile t = t % waves
     int64_t nstripe = 0;           // source stripes S

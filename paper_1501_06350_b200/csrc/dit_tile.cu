@@ -67,13 +67,9 @@ static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per round warp");
 template <typename W>
 using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
 
-// sliced-ELL slot groups: the first K - K % kSlotGroup slots of a lane sit in runs
-// of kSlotGroup (one vector load each), the rest one per row of 32
-#ifndef DIT_SLOT_GROUP
-#define DIT_SLOT_GROUP 4
-#endif
-constexpr int kSlotGroup = DIT_SLOT_GROUP;
-static_assert(kSlotGroup == 1 || kSlotGroup == 2 || kSlotGroup == 4, "slot group 1, 2 or 4");
+// sliced-ELL slot groups: the first K - K % 4 slots of a lane sit in runs of four
+// (one 8-byte source load, one 16-byte weight load), the rest one per row of 32
+constexpr int kSlotGroup = 4;
 // offset of slot s of lane `lane` in a virtual warp of K slots per lane
 __host__ __device__ __forceinline__ int64_t ell_slot(int64_t s, int lane, int64_t K) {
     const int64_t Kg = K - K % kSlotGroup;
@@ -638,8 +634,7 @@ void free_tiles(TilePlan &t) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
                     (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
-                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run,
-                    (void *)t.hticket})
+                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run})
         cudaFree(p);
     t = TilePlan();
 }
@@ -804,7 +799,7 @@ static void build_tiles_t(di_graph *h) {
     DI_CUDA(cudaFreeAsync(tkey, st));
     DI_CUDA(cudaFreeAsync(L, st));
     count_launch();
-    if (tp.mpad > 0 && !getenv("DIT_NO_BANK_ORDER")) {
+    if (tp.mpad > 0 && getenv("DIT_BANK_ORDER")) {   // opt-in: ~1% faster rounds for ~55 ms of build (configs[2])
         k_ell_balance<W><<<(int)std::min<int64_t>(tp.ntile * kVWarps / kBalWarps + 1, (int64_t)h->num_sms * 16),
                            kBalWarps * 32, 0, st>>>(
             tp.ltile, tp.vofs, tp.ntile, tp.lsrc, (SW *)tp.lw);
@@ -911,8 +906,6 @@ static void build_tiles_t(di_graph *h) {
     }
     phase_mark(st, "tiles: heavy sort + index");
     DI_CUDA(cudaMallocAsync(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double), st));
-    DI_CUDA(cudaMallocAsync(&tp.hticket, 64 * sizeof(int), st));
-    DI_CUDA(cudaMemsetAsync(tp.hticket, 0, 64 * sizeof(int), st));
     DI_CUDA(cudaMallocAsync(&tp.tpart, (2 * (size_t)tp.waves * 4096 + 64) * sizeof(double), st));
     unsigned long long *mx;
     DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
@@ -948,16 +941,17 @@ void build_tiles(di_graph *h) {
 
 // ---------------------------------------------------------------- heavy remote sums
 // Heavy targets' remote inflow, per wave, in two launches:
-//   k_heavy_chunks -- persistent CTAs take 2048-edge chunks of the wave's heavy
-//     edges by ticket, in (stripe, target, source) order, so that at any time the
-//     gathered slice of the outflow A is about one stripe (L2-resident); a CTA
-//     stages A(src) w of its chunk in shared memory, then one thread per short
-//     segment (target within chunk) / one warp per long one sums it into part;
+//   k_heavy_chunks -- one launch per source stripe (the gathered slice of the
+//     outflow A stays L2-resident), CTAs stride over the stripe's 2048-edge
+//     chunks (a shared ticket counter was measured 2x slower: 40K same-address
+//     atomics per wave serialise at one L2 slice); a CTA stages A(src) w of its
+//     chunk in shared memory, then one thread per short segment (target within
+//     chunk) / one warp per long one sums it into part;
 //   k_heavy_fold -- per heavy target of the wave, its runs (one per source
 //     stripe) and their segments summed in stripe / edge order into hsum.
 // Every sum has a fixed order whatever CTA takes which chunk: bitwise reproducible.
 
-// the chunks [c0, c1) by ticket; CTA per chunk at a time
+// the chunks [c0, c1) of one stripe; CTA per chunk at a time
 template <typename W>
 __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__restrict__ hrec,
                                                            const int64_t *__restrict__ chunk_start,
@@ -965,11 +959,9 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
                                                            const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
                                                            const double *__restrict__ A0, const double *__restrict__ A1,
                                                            double *__restrict__ part, int wave, int waves,
-                                                           const Ctrl *__restrict__ ctrl, int force,
-                                                           int *__restrict__ ticket) {
+                                                           const Ctrl *__restrict__ ctrl, int force) {
     __shared__ double vals[kHeavyChunk];
     __shared__ int sbnd[kHeavyChunk + 1];
-    __shared__ int s_c;
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
     const bool gather = ctrl->gather != 0;
     if (force ? !gather : (!gather && wave == 0)) return;
@@ -977,26 +969,37 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
     const double *__restrict__ Aprev = (ctrl->sweeps & 1) ? A0 : A1;
     const double *__restrict__ Afresh = (ctrl->sweeps & 1) ? A1 : A0;
     const unsigned w = threadIdx.x >> 5, lane = lane_id();
-    for (;;) {
-        if (threadIdx.x == 0) s_c = atomicAdd(ticket, 1);
-        __syncthreads();
-        const int64_t c = c0 + s_c;
-        if (c >= c1) break;
+    for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
         const int64_t e0 = chunk_start[c];
         const int cnt = (int)(chunk_start[c + 1] - e0);
         const int64_t sg0 = cfirst[c];
         const int ns = (int)(cfirst[c + 1] - sg0);
         for (int q = threadIdx.x; q < ns; q += kThreads) sbnd[q] = (int)(seg_start[sg0 + q] - e0);
         if (threadIdx.x == 0) sbnd[ns] = cnt;
-#pragma unroll 8
-        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+        // all of this thread's records first, then all their gathers (kPer loads in flight each)
+        constexpr int kPer = (int)kHeavyChunk / kThreads;
+        RemRec<W> rr[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int k = threadIdx.x + u * kThreads;
+            if (k < cnt) rr[u] = hrec[e0 + k];
+        }
+        double vv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
             // a source of an earlier wave pushed this sweep; the others in the previous
             // one (still pending); in the flush only the pending pushes are left (R15)
-            const RemRec<W> r = hrec[e0 + k];
-            const bool early = tile_wave(r.src, waves) < wave;
-            double v = 0.0;
-            if (force ? !early : (early || gather)) v = (early && !force ? Afresh : Aprev)[r.src] * rec_w(r);
-            vals[k] = v;
+            const int k = threadIdx.x + u * kThreads;
+            vv[u] = 0.0;
+            if (k < cnt) {
+                const bool early = tile_wave(rr[u].src, waves) < wave;
+                if (force ? !early : (early || gather)) vv[u] = (early && !force ? Afresh : Aprev)[rr[u].src];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int k = threadIdx.x + u * kThreads;
+            if (k < cnt) vals[k] = vv[u] * rec_w(rr[u]);
         }
         __syncthreads();
         for (int q0 = (int)(w * 32); q0 < ns; q0 += kThreads) {
@@ -1027,15 +1030,15 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
 }
 
 // hsum of the wave's heavy targets [t0, t1) (fold slots): lane per target, a
-// warp per target of more than 64 segments; resets the wave's ticket
+// warp per target of more than 64 segments
 __global__ void __launch_bounds__(kThreads) k_heavy_fold(const int64_t *__restrict__ fold_ptr,
                                                          const int32_t *__restrict__ fold_h,
                                                          const uint32_t *__restrict__ fold_run,
                                                          const int64_t *__restrict__ run_seg,
                                                          const double *__restrict__ part, double *__restrict__ hsum,
                                                          int64_t t0, int64_t t1, int wave, const Ctrl *__restrict__ ctrl,
-                                                         int force, int *__restrict__ ticket) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;   // k_heavy_chunks of this wave is done (stream order)
+                                                         int force) {
+
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
     const bool gather = ctrl->gather != 0;
     if (force ? !gather : (!gather && wave == 0)) return;
@@ -1102,7 +1105,6 @@ struct TileArgs {
     int rounds;
     int wave, waves;         // this launch runs tiles wave, wave + waves, ... (R15)
     int64_t ntw;             // tiles of the wave
-    int diag;                // DIT_TILE_DIAG (debug): bit 0 = skip the unstaged local sums (wrong results)
 };
 
 // one target's local pushes in its sliced-ELL column: slots base, base+32, ...
@@ -1161,91 +1163,6 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
         }
     }
     return (a0 + a1) + (a2 + a3);
-}
-
-// A round warp's two virtual warps (A = the longer, B) from shared memory as one
-// software-pipelined walk over steps of four slots per lane: the sources and
-// weights of step j + 1 are loaded while step j's outflow gathers are in flight.
-// Four partial sums per virtual warp (slot mod 4), combined in a fixed order (R14).
-#ifndef DIT_PAIR
-#define DIT_PAIR 0
-#endif
-template <typename W>
-__device__ __forceinline__ void local_sum_pair(const uint16_t *es, const StoreW<W> *ew, const double *gq, int oA,
-                                               int KA, int oB, int KB, int lane, double &rA, double &rB) {
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    using SW = StoreW<W>;
-    const int SA = (KA + 3) >> 2, S = SA + ((KB + 3) >> 2);
-    auto load = [&](int j, int (&sv)[4], SW (&wv)[4]) {
-        const bool inA = j < SA;
-        const int o = inA ? oA : oB, K = inA ? KA : KB, g = inA ? j : j - SA;
-        const int Kg = K & ~3;
-        if (4 * g < Kg) {                              // runs of four slots per lane
-            const int k = o + 128 * g + 4 * lane;
-            const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
-            sv[0] = (int)(e.x & 0xffffu);
-            sv[1] = (int)(e.x >> 16);
-            sv[2] = (int)(e.y & 0xffffu);
-            sv[3] = (int)(e.y >> 16);
-            if constexpr (kW) {
-                if constexpr (sizeof(SW) == 4) {
-                    const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
-                    wv[0] = w4.x;
-                    wv[1] = w4.y;
-                    wv[2] = w4.z;
-                    wv[3] = w4.w;
-                } else {
-                    for (int u = 0; u < 4; ++u) wv[u] = ew[k + u];
-                }
-            }
-        } else {                                       // the last K % 4 slots, one per row of 32
-            const int t = K - Kg, k = o + 32 * Kg + lane;
-            sv[0] = es[k];
-            sv[1] = t > 1 ? (int)es[k + 32] : (int)kNodeTile;
-            sv[2] = t > 2 ? (int)es[k + 64] : (int)kNodeTile;
-            sv[3] = (int)kNodeTile;                     // zero outflow
-            if constexpr (kW) {
-                wv[0] = ew[k];
-                wv[1] = t > 1 ? ew[k + 32] : SW(0);
-                wv[2] = t > 2 ? ew[k + 64] : SW(0);
-                wv[3] = SW(0);
-            }
-        }
-    };
-    int sv[4];
-    SW wv[4] = {SW(1), SW(1), SW(1), SW(1)};
-    rA = 0.0;
-    rB = 0.0;
-    if (S == 0) return;
-    load(0, sv, wv);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int j = 0; j < S; ++j) {
-        int sn[4] = {0, 0, 0, 0};
-        SW wn[4] = {SW(1), SW(1), SW(1), SW(1)};
-        if (j + 1 < S) load(j + 1, sn, wn);
-        const double v0 = gq[sv[0]], v1 = gq[sv[1]], v2 = gq[sv[2]], v3 = gq[sv[3]];
-        if constexpr (kW) {
-            a0 = fma(v0, (double)wv[0], a0);
-            a1 = fma(v1, (double)wv[1], a1);
-            a2 = fma(v2, (double)wv[2], a2);
-            a3 = fma(v3, (double)wv[3], a3);
-        } else {
-            a0 += v0;
-            a1 += v1;
-            a2 += v2;
-            a3 += v3;
-        }
-        if (j == SA - 1) {
-            rA = (a0 + a1) + (a2 + a3);
-            a0 = a1 = a2 = a3 = 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            sv[u] = sn[u];
-            wv[u] = wn[u];
-        }
-    }
-    if (S > SA) rB = (a0 + a1) + (a2 + a3);
 }
 
 struct TileScalars {
@@ -1431,16 +1348,6 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 const long long ta = kProf ? clock64() : 0;
                 if (kProf) b1_cyc += ta - t9;
                 // Eq. (8) local pushes: this warp's two virtual warps of pieces (longest with shortest)
-                const int vA = wp, vB = kVWarps - 1 - wp;
-                const uint32_t oA = vofs_s[vA], oB = vofs_s[vB];
-                const int KA = (int)((vofs_s[vA + 1] - oA) >> 5), KB = (int)((vofs_s[vB + 1] - oB) >> 5);
-                if (DIT_PAIR && (int)oA >= st) {      // both staged (oB > oA)
-                    if (kProf) rows_w += KA + KB;
-                    double rA, rB;
-                    local_sum_pair<W>(es_sm, ew_sm, gq, (int)oA, KA, (int)oB, KB, lane, rA, rB);
-                    if (KA) psum[vA * 32 + lane] = rA;
-                    if (KB) psum[vB * 32 + lane] = rB;
-                } else
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     const int vw = h2 ? kVWarps - 1 - wp : wp;
@@ -1450,7 +1357,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     if (K) {
                         double acc;
                         if ((int)o0 >= st) acc = local_sum<W>(es_sm, ew_sm, gq, (int)o0 + lane, K);
-                        else acc = (a.diag & 1) ? 0.0 : local_sum<W>(es_gl, ew_gl, gq, (int)o0 + lane, K);
+                        else acc = local_sum<W>(es_gl, ew_gl, gq, (int)o0 + lane, K);
                         psum[vw * 32 + lane] = acc;
                     }
                 }
@@ -1731,7 +1638,6 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     a.ntile = tp.ntile;
     a.m = g.m;
     a.lstage = tp.lstage;
-    a.diag = getenv("DIT_TILE_DIAG") ? atoi(getenv("DIT_TILE_DIAG")) : 0;
     a.rounds = rounds;
     a.dbg = nullptr;
     a.wave = 0;
@@ -1758,19 +1664,22 @@ static void launch_heavy_t(di_graph *h, int wave, int force) {
     State &s = h->s;
     if (tp.nh == 0) return;
     const int64_t S = tp.nstripe, g0 = (int64_t)wave * S;
-    const int64_t c0 = tp.s_chunk[g0], c1 = tp.s_chunk[g0 + S];
     const int64_t t0 = tp.wave_slot[wave], t1 = tp.wave_slot[wave + 1];
-    if (c1 > c0) {
-        const int grid = (int)std::min<int64_t>(c1 - c0, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
+    // one launch per source stripe: the gathered slice of A (kStripeBytes) stays in L2
+    for (int64_t sg = 0; sg < S; ++sg) {
+        const int64_t a0 = tp.s_chunk[g0 + sg], a1 = tp.s_chunk[g0 + sg + 1];
+        if (a1 <= a0) continue;
+        const int grid = (int)std::min<int64_t>(a1 - a0, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
         k_heavy_chunks<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
-                                                            tp.cfirst, c0, c1, s.A, s.A2, tp.part, wave, tp.waves,
-                                                            s.ctrl, force, tp.hticket + wave);
+                                                            tp.cfirst, a0, a1, s.A, s.A2, tp.part, wave, tp.waves,
+                                                            s.ctrl, force);
         count_launch();
     }
+
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((t1 - t0 + kThreads - 1) / kThreads,
                                                                  (int64_t)h->num_sms * 8));
     k_heavy_fold<<<grid, kThreads, 0, h->stream>>>(tp.fold_ptr, tp.fold_h, tp.fold_run, tp.run_seg, tp.part, tp.hsum,
-                                                   t0, t1, wave, s.ctrl, force, tp.hticket + wave);
+                                                   t0, t1, wave, s.ctrl, force);
     count_launch();
 }
 

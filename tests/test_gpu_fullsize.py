@@ -174,11 +174,11 @@ def test_tiled_64bit_scan_and_own_radix_elementwise(eng):
         _tiled_elementwise(eng, g, 3, (1, 3))
 
 
-def test_tiled_edge_order_without_bank_balance(eng):
-    # the bank-aware slot order (k_ell_balance) only permutes summation order
-    # within pieces: both layouts match the oracle element-wise
+def test_tiled_edge_order_with_bank_balance(eng):
+    # the bank-aware slot order (k_ell_balance, opt-in DIT_BANK_ORDER) only permutes
+    # the summation order within pieces: both layouts match the oracle element-wise
     spec = synth.CONFIGS[1].scaled(60_013, seed=23, weighted=True)
     g = synth.generate(spec)
-    with _env(DIT_NO_BANK_ORDER=1):
+    with _env(DIT_BANK_ORDER=1):
         _tiled_elementwise(eng, g, 4, (2,))
     _tiled_elementwise(eng, g, 4, (2,))
