@@ -98,11 +98,171 @@ static int read_flag(int *dflag, cudaStream_t st) {
     return v;
 }
 
+// scales of the rows [i0, i1) (pipelined create)
+template <typename Wt>
+__global__ void k_scales_rows(const int64_t *__restrict__ row_ptr, const Wt *__restrict__ w, int64_t i0, int64_t i1,
+                              double *__restrict__ inv) {
+    for (int64_t j = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < i1; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = row_ptr[j], e = row_ptr[j + 1];
+        if (b == e) {
+            inv[j] = 0.0;
+            continue;
+        }
+        if (!w) {
+            inv[j] = 1.0 / (double)(e - b);
+            continue;
+        }
+        double s = 0.0;                       // sum_k w_{j,k}, in edge order (as k_scales)
+        for (int64_t k = b; k < e; ++k) s += (double)w[k];
+        inv[j] = 1.0 / s;
+    }
+}
+
+static bool pinned_host(const void *p) {
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Create from pinned host buffers with the tile plan built while the edges
+// upload: row_ptr first, then the targets chunk by chunk (plan
+// phase 1 of each chunk as it lands), then the weights chunk by chunk (phase
+// 2: validation, scales, ELL); the remote part of the plan after the last chunk.
+static void create_graph_pipelined(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
+                                   const void *weights, int w_dtype) {
+    DevGraph &g = h->g;
+    cudaStream_t st = h->stream;
+    g.n = n;
+    g.m = m;
+    g.nt = n;
+    g.n_global = n;
+    phase_mark(st, "create: start");
+    DI_CUDA(cudaMallocAsync(&g.row_ptr, (n + 1) * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&g.col, m * sizeof(int32_t), st));
+    if (w_dtype == DI_W_F32) DI_CUDA(cudaMallocAsync(&g.w, m * sizeof(float), st));
+    DI_CUDA(cudaMallocAsync(&g.inv, n * sizeof(double) + 16, st));
+    g.w_kind = w_dtype == DI_W_F32 ? DI_W_F32 : DI_W_NONE;
+    int *flags = nullptr;
+    DI_CUDA(cudaMallocAsync(&flags, 2 * sizeof(int), st));
+    DI_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+    // chunks of whole tiles, ~kPlanChunkEdges edges each (host row_ptr)
+    PlanFeed feed;
+    const int64_t ntile = (n + kNodeTile - 1) / kNodeTile;
+    feed.tile_lo.push_back(0);
+    feed.edge_lo.push_back(0);
+    for (int64_t t = 1; t <= ntile; ++t) {
+        // (clamped: a malformed row_ptr is rejected below, after the copies are issued)
+        const int64_t e = std::min(m, std::max(feed.edge_lo.back(), row_ptr[std::min(n, t * kNodeTile)]));
+        if (t == ntile || e - feed.edge_lo.back() >= kPlanChunkEdges) {
+            feed.tile_lo.push_back(t);
+            feed.edge_lo.push_back(e);
+        }
+    }
+    const int nch = (int)feed.tile_lo.size() - 1;
+    cudaStream_t cs = nullptr;
+    DI_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t go = nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto cleanup = [&]() {
+        if (cs) cudaStreamSynchronize(cs);
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+        if (go) cudaEventDestroy(go);
+        if (cs) cudaStreamDestroy(cs);
+        cs = nullptr;
+        go = nullptr;
+        evs.clear();
+    };
+    try {
+        DI_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+        DI_CUDA(cudaEventRecord(go, st));                // the buffers exist before the copies land
+        DI_CUDA(cudaStreamWaitEvent(cs, go, 0));
+        // row_ptr first on the copy stream (copies on one engine run in issue order)
+        DI_CUDA(cudaMemcpyAsync(g.row_ptr, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+        cudaEvent_t rows_ready;
+        DI_CUDA(cudaEventCreateWithFlags(&rows_ready, cudaEventDisableTiming));
+        evs.push_back(rows_ready);
+        DI_CUDA(cudaEventRecord(rows_ready, cs));
+        for (int pass = 0; pass < (w_dtype == DI_W_F32 ? 2 : 1); ++pass)
+            for (int c = 0; c < nch; ++c) {
+                const int64_t e0 = feed.edge_lo[c], e1 = feed.edge_lo[c + 1];
+                if (e1 > e0) {
+                    if (pass == 0)
+                        DI_CUDA(cudaMemcpyAsync(g.col + e0, col + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, cs));
+                    else
+                        DI_CUDA(cudaMemcpyAsync((float *)g.w + e0, (const float *)weights + e0, (e1 - e0) * 4,
+                                                cudaMemcpyHostToDevice, cs));
+                }
+                cudaEvent_t ev;
+                DI_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                evs.push_back(ev);
+                DI_CUDA(cudaEventRecord(ev, cs));
+                (pass == 0 ? feed.col_ready : feed.w_ready).push_back(ev);
+            }
+        if (w_dtype != DI_W_F32) feed.w_ready = feed.col_ready;   // unweighted: phase 2 needs the targets only
+        // row_ptr validated before the plan uses it
+        DI_CUDA(cudaStreamWaitEvent(st, rows_ready, 0));
+        k_check_rows<<<grid_for(h, n + 1), 256, 0, st>>>(g.row_ptr, n, m, flags);
+        count_launch();
+        if (read_flag(flags, st)) {
+            set_error("row_ptr must be non-decreasing with row_ptr[0]=0 and row_ptr[n]=m");
+            throw Fail{DI_ERR_INVALID};
+        }
+        feed.on_col = [&](int c) {                       // target ids of the chunk in [0, n)
+            const int64_t e0 = feed.edge_lo[c], e1 = feed.edge_lo[c + 1];
+            if (e1 > e0) {
+                k_check_edges<float><<<grid_for(h, e1 - e0), 256, 0, st>>>(g.col + e0, nullptr, e1 - e0, n, flags,
+                                                                          flags + 1);
+                count_launch();
+            }
+        };
+        feed.on_w = [&](int c) {                         // weights of the chunk, then the scales of its rows
+            const int64_t e0 = feed.edge_lo[c], e1 = feed.edge_lo[c + 1];
+            const int64_t i0 = std::min(n, feed.tile_lo[c] * kNodeTile), i1 = std::min(n, feed.tile_lo[c + 1] * kNodeTile);
+            if (w_dtype == DI_W_F32 && e1 > e0) {
+                k_check_edges<float><<<grid_for(h, e1 - e0), 256, 0, st>>>(g.col + e0, (const float *)g.w + e0, e1 - e0,
+                                                                          n, flags, flags + 1);
+                count_launch();
+            }
+            if (i1 > i0) {
+                k_scales_rows<float><<<grid_for(h, i1 - i0), 256, 0, st>>>(
+                    g.row_ptr, w_dtype == DI_W_F32 ? (const float *)g.w : nullptr, i0, i1, g.inv);
+                count_launch();
+            }
+        };
+        phase_mark(st, "create: row_ptr + launch the upload");
+        build_tiles(h, &feed, flags);
+        cleanup();
+    } catch (...) {
+        cleanup();
+        cudaFree(flags);
+        throw;
+    }
+    int fl[2] = {0, 0};
+    DI_CUDA(cudaMemcpyAsync(fl, flags, sizeof(fl), cudaMemcpyDeviceToHost, st));
+    DI_CUDA(cudaFreeAsync(flags, st));
+    DI_CUDA(cudaStreamSynchronize(st));
+    if (fl[0]) {
+        set_error(fl[0] & 1 ? "row_ptr must be non-decreasing with row_ptr[0]=0 and row_ptr[n]=m"
+                            : (fl[0] & 2 ? "col ids must be in [0, n) (n_global for a shard)" : "weights must be finite and > 0"));
+        throw Fail{DI_ERR_INVALID};
+    }
+}
+
 // Copy + validate the caller's CSR into the handle.
 void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
                   const void *weights, int w_dtype, int mem, int64_t col_bound) {
     DevGraph &g = h->g;
     cudaStream_t st = h->stream;
+    // host graphs of 16M+ edges from pinned memory: the tile plan is built during the upload
+    if (mem == DI_MEM_HOST && col_bound == n && m >= ((int64_t)1 << 24) && w_dtype != DI_W_F64 && n > 0 &&
+        !getenv("DIT_NO_EAGER_PLAN") && pinned_host(col) && pinned_host(row_ptr) &&
+        (w_dtype == DI_W_NONE || pinned_host(weights))) {
+        create_graph_pipelined(h, n, m, row_ptr, col, weights, w_dtype);
+        return;
+    }
     g.n = n;
     phase_mark(st, "create: start");
     g.m = m;

@@ -2,6 +2,7 @@
 // The C ABI is include/dit.h; DESIGN.md describes the data layout and kernels.
 #pragma once
 
+#include <functional>
 #include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -76,8 +77,6 @@ struct PullPlan {
     double *pbuf = nullptr;        // [npieces] partial sums of split targets
     int64_t *tile_start = nullptr; // [ntiles+1] first piece of each 2048-edge tile
     int64_t ntiles = 0;
-    uint32_t *tkey = nullptr;      // [m] target of each in-edge (the sort's keys), kept for the
-                                   // tile plan's build and freed by it
 };
 
 // Tile-local schedule (R12, §5): node tiles of kNodeTile ids.  An
@@ -156,6 +155,18 @@ struct TilePlan {
     int64_t max_tile_edges = 0;    // most local in-edges of one tile
     int32_t *lstage = nullptr;     // [ntile] first slot (relative to ltile) that k_tile stages in shared memory
 };
+
+// Chunks of whole tiles for the plan builder (dit_plan.cu): chunk c is tiles
+// [tile_lo[c], tile_lo[c+1]), edges [edge_lo[c], edge_lo[c+1]); with a feed
+// (graph create overlapping the upload) its targets / weights are resident once
+// col_ready[c] / w_ready[c] fired, and on_col / on_w run right after the waits
+// (validation and scales of the chunk, on the build's stream).
+struct PlanFeed {
+    std::vector<int64_t> tile_lo, edge_lo;
+    std::vector<cudaEvent_t> col_ready, w_ready;
+    std::function<void(int)> on_col, on_w;
+};
+constexpr int64_t kPlanChunkEdges = (int64_t)1 << 26;   // plan chunk size without a feed
 
 // Per-node weight-scale storage and raw weights.
 struct DevGraph {
@@ -240,7 +251,9 @@ void launch_pull(di_graph *h);
 void launch_pull_plan(di_graph *h, const PullPlan &p, const double *A, int want);
 void build_plan_pieces(di_graph *h, PullPlan &p);
 void free_plan(PullPlan &p);
-void build_tiles(di_graph *h);
+// feed: chunks arriving during create (then `bad` = the create's validation flags:
+// nonzero after the chunks stops the build before its remote part)
+void build_tiles(di_graph *h, const PlanFeed *feed = nullptr, const int *bad = nullptr);
 void free_tiles(TilePlan &t);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
@@ -277,6 +290,8 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
 void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t count, cudaStream_t st);
 std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1,
                                                  int64_t count, int bits, cudaStream_t st);
+std::pair<uint32_t *, uint64_t *> radix_sort_u32_u64(uint32_t *k0, uint64_t *v0, uint32_t *k1, uint64_t *v1,
+                                                     int64_t count, int bits, cudaStream_t st);
 
 // ---- DIT_BUILD_TIMING (debug): host-side phase timer, stream-synchronised ----
 void phase_mark(cudaStream_t st, const char *name);

@@ -213,13 +213,27 @@ std::pair<uint32_t *, uint32_t *> radix_sort_u32(uint32_t *k0, uint32_t *v0, uin
     return {k0, v0};
 }
 
+// the same with u64 values (the tile plan's packed {source, weight} payloads)
+std::pair<uint32_t *, uint64_t *> radix_sort_u32_u64(uint32_t *k0, uint64_t *v0, uint32_t *k1, uint64_t *v1,
+                                                     int64_t count, int bits, cudaStream_t st) {
+    if (count <= 0) return {k0, v0};
+    const int64_t ntiles = (count + kSortTile - 1) / kSortTile;
+    int64_t *hc, *ho;
+    DI_CUDA(cudaMallocAsync(&hc, (int64_t)kRadix * ntiles * sizeof(int64_t), st));
+    DI_CUDA(cudaMallocAsync(&ho, ((int64_t)kRadix * ntiles + 1) * sizeof(int64_t), st));
+    for (int shift = 0; shift < bits; shift += kRadixBits) {
+        radix_sort_pass_launch(k0, v0, k1, v1, count, shift, ntiles, hc, ho, true, st);
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+    }
+    DI_CUDA(cudaFreeAsync(hc, st));
+    DI_CUDA(cudaFreeAsync(ho, st));
+    return {k0, v0};
+}
+
 // Work plan of a CSC (pieces, tiles, split-target fixups) for k_pull.
 void build_plan_pieces(di_graph *h, PullPlan &pd) {
     cudaStream_t st = h->stream;
-    if (pd.tkey && h->g.tl.built) {                  // the tile plan is built: nobody needs the keys
-        DI_CUDA(cudaFreeAsync(pd.tkey, st));
-        pd.tkey = nullptr;
-    }
     const int64_t nt = pd.nt, m = pd.m;
     int64_t *pc, *po;
     DI_CUDA(cudaMallocAsync(&pc, (nt + 1) * sizeof(int64_t), st));
@@ -265,7 +279,6 @@ void free_plan(PullPlan &p) {
     cudaFree(p.fix);
     cudaFree(p.pbuf);
     cudaFree(p.tile_start);
-    cudaFree(p.tkey);
     p = PullPlan();
 }
 
@@ -359,9 +372,6 @@ static void build_transpose_packed(di_graph *h, int64_t *cnt) {
     k_run_bounds<<<grid, kThreads, 0, st>>>(kb.Current(), m, cnt);
     k_unpack_t<<<grid, kThreads, 0, st>>>(vb.Current(), m, T.src, (float *)T.w);
     count_launch(2);
-    // the tile plan reads the sorted keys (and frees them): copy them out of the block
-    DI_CUDA(cudaMallocAsync(&T.tkey, (size_t)m * 4, st));
-    DI_CUDA(cudaMemcpyAsync(T.tkey, kb.Current(), (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
     DI_CUDA(cudaStreamSynchronize(st));              // the block is free for the next build
 }
 

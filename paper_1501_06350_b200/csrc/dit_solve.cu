@@ -456,13 +456,15 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     DevGraph &g = h->g;
     const bool want_pull = o.variant != DI_VARIANT_PUSH;
     if (want_pull && g.n > 0) {
-        build_transpose(h);
         if (o.variant == DI_VARIANT_TILED) {
-            build_tiles(h);
+            build_tiles(h);                          // straight from the CSR (dit_plan.cu): no transpose
             if (!s.A2) DI_CUDA(cudaMallocAsync(&s.A2, g.n * sizeof(double), h->stream));
-        } else if (!g.t.pieces_built) {
-            build_plan_pieces(h, g.t);
-            phase_mark(h->stream, "transpose: pull pieces");
+        } else {
+            build_transpose(h);
+            if (!g.t.pieces_built) {
+                build_plan_pieces(h, g.t);
+                phase_mark(h->stream, "transpose: pull pieces");
+            }
         }
         if (!s.A) DI_CUDA(cudaMallocAsync(&s.A, g.n * sizeof(double), h->stream));
     }
@@ -477,8 +479,8 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
     c.theta = o.theta;
     c.tol = tol;
     c.max_sweeps = (unsigned long long)(o.max_sweeps > 0 ? o.max_sweeps : 10000000LL);
-    c.variant = g.t.built && (o.variant == DI_VARIANT_TILED || g.t.pieces_built) ? o.variant : DI_VARIANT_PUSH;
-    if (o.variant == DI_VARIANT_TILED && !g.tl.built) c.variant = DI_VARIANT_PUSH;
+    c.variant = o.variant == DI_VARIANT_TILED ? (g.tl.built ? o.variant : DI_VARIANT_PUSH)
+                                              : (g.t.built && g.t.pieces_built ? o.variant : DI_VARIANT_PUSH);
     c.pull_edges = o.pull_frac * (double)g.m;
     c.hist = s.hist;
     c.n_global = (double)(g.n_global > 0 ? g.n_global : 1);

@@ -38,7 +38,7 @@
 // 2048-edge chunk, warp per segment; then the stripe's runs folded into
 // hsum in stripe order.  Every summation has a fixed order: bitwise
 // reproducible run to run.
-#include "dit_internal.cuh"
+#include "dit_tile.cuh"
 
 #include <cub/device/device_scan.cuh>
 #include <algorithm>
@@ -46,898 +46,6 @@
 #include <type_traits>
 
 namespace dit {
-
-constexpr int kTileThreads = (int)kNodeTile;     // build kernels: thread i owns node i of the tile
-// k_tile: one 1024-thread CTA per SM, 16 round warps (thread i owns node i) and
-// 16 prep warps (the next tile's inflow)
-constexpr int kRW = (int)kNodeTile;
-constexpr int kPWt = (int)kNodeTile / 2;           // two nodes per prep thread
-constexpr int kPN = (int)kNodeTile / kPWt;
-constexpr int kTileBlock = kRW + kPWt;
-constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kVRows = 2 * (int)kNodeTile;       // local-edge pieces per tile (at most)
-constexpr int kVWarps = kVRows / 32;             // virtual warps: round warp w runs w and kVWarps-1-w
-constexpr int kVofsStride = 36;                  // u32 per tile (kVWarps + 1, padded to 16 B)
-constexpr int kVfStride = 520;                   // u16 per tile (kNodeTile + 1, padded to 16 B)
-constexpr int kMetaBytes = kVofsStride * 4 + kVfStride * 2 + kVRows * 2;   // per-tile layout, TMA-staged
-constexpr int64_t kGqSlots = kNodeTile + 16;     // outflow per node + one zero slot per bank pair (ELL padding)
-constexpr int kTileSmemBudget = 227 * 1024 - 2048;   // dynamic shared memory of k_tile (static arrays aside)
-static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per round warp");
-
-template <typename W>
-using StoreW = typename std::conditional<std::is_same<W, NoW>::value, float, W>::type;
-
-// sliced-ELL slot groups: the first K - K % 4 slots of a lane sit in runs of four
-// (one 8-byte source load, one 16-byte weight load), the rest one per row of 32
-constexpr int kSlotGroup = 4;
-// offset of slot s of lane `lane` in a virtual warp of K slots per lane
-__host__ __device__ __forceinline__ int64_t ell_slot(int64_t s, int lane, int64_t K) {
-    const int64_t Kg = K - K % kSlotGroup;
-    return s < Kg ? 32 * kSlotGroup * (s / kSlotGroup) + kSlotGroup * lane + (s % kSlotGroup) : 32 * s + lane;
-}
-
-// remote record: source and raw weight of one remote in-edge
-template <typename W>
-struct RemRec {
-    int32_t src;
-    float w;
-};
-template <>
-struct RemRec<double> {
-    int32_t src;
-    int32_t pad;
-    double w;
-};
-template <typename W>
-__device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w; }
-
-// Shared memory of k_tile (one CTA per SM, everything double-buffered by tile
-// parity): gq / psum of the rounds, the prepared per-node rows P, the light
-// records R (prep warps) and the edge bundles E = {layout, staged slots} (round warps).
-struct PrepRow {
-    double f, ivi, H;        // inflow-completed fluid, 1/sum w, history
-    float wr;                // pending share of the out-weight (R13)
-    int32_t deg;             // out-degree
-};
-static_assert(sizeof(PrepRow) == 32, "32-byte prepared rows");
-constexpr int kOffPsum = ((int)kGqSlots * 8 + 127) & ~127;
-constexpr int kOffP = kOffPsum + kVRows * 8;
-constexpr int kOffR = kOffP + 2 * (int)kNodeTile * (int)sizeof(PrepRow);
-template <typename W>
-constexpr int tile_rec_buf() { return (((int)kLightCap * (int)sizeof(RemRec<W>) + 32) + 127) & ~127; }
-template <typename W>
-constexpr int tile_off_e() { return kOffR + 2 * tile_rec_buf<W>(); }
-template <typename W>
-constexpr int tile_e_buf() { return ((kTileSmemBudget - tile_off_e<W>()) / 2) & ~127; }
-template <typename W>
-constexpr int tile_smem_bytes() { return tile_off_e<W>() + 2 * tile_e_buf<W>(); }
-static_assert(kOffP % 16 == 0 && kOffR % 128 == 0 && kMetaBytes % 16 == 0, "aligned shared buffers");
-
-#ifndef DIT_STRIPE_MB
-#define DIT_STRIPE_MB 48
-#endif
-constexpr int64_t kStripeBytes = (int64_t)DIT_STRIPE_MB << 20;   // outflow slice per heavy stripe (L2-resident)
-#ifndef DIT_TILE_WAVES
-#define DIT_TILE_WAVES 2
-#endif
-constexpr int kTileWaves = DIT_TILE_WAVES;      // tile waves per sweep (R15), single GPU
-__device__ __forceinline__ int tile_wave(int64_t node, int waves) { return (int)((node / kNodeTile) % waves); }
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-// bounded wait: a byte-count mismatch becomes a trap (an error), never a hung GPU
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin) {
-        if (spin > 8) __nanosleep(64);               // long waits: leave the issue slots to others
-        if (spin > (1ll << 26)) __trap();
-    }
-}
-// bulk global -> shared copy (the TMA engine), completion counted on `bar`
-__device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-
-// bulk prefetch of a global range into L2 (the TMA engine; no completion tracking)
-__device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
-// ---------------------------------------------------------------- build
-// light / heavy split of the remote in-edges, one thread per tile
-__global__ void k_classify(const int64_t *__restrict__ rc, int64_t n, int64_t ntile, int64_t *__restrict__ lrc,
-                           int64_t *__restrict__ hc, int64_t *__restrict__ hflag) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntile; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a = t * kNodeTile, z = min(n, a + kNodeTile);
-        int64_t light = 0;
-        for (int64_t j = a; j < z; ++j)
-            if (rc[j] <= kHeavyTh) light += rc[j];
-        const int64_t th = light > kLightCap ? 0 : kHeavyTh;   // overflowing tile: every remote target heavy
-        for (int64_t j = a; j < z; ++j) {
-            const bool heavy = rc[j] > th;
-            lrc[j] = heavy ? 0 : rc[j];
-            hc[j] = heavy ? rc[j] : 0;
-            hflag[j] = heavy ? 1 : 0;
-        }
-    }
-}
-
-// shard ghost slots: heavy targets whose sums leave through the all-to-all
-__global__ void k_classify_ghosts(const int64_t *__restrict__ rc, int64_t n, int64_t nt, int64_t *__restrict__ lrc,
-                                  int64_t *__restrict__ hc, int64_t *__restrict__ hflag) {
-    for (int64_t t = n + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-        lrc[t] = 0;
-        hc[t] = rc[t];
-        hflag[t] = rc[t] > 0;
-    }
-}
-
-// balanced sliced-ELL layout of a tile's local in-edges: CTA per tile
-// 512-thread block reductions for the layout kernel (fixed order: deterministic)
-__device__ __forceinline__ int64_t block_sum_512(int64_t v, int64_t *red) {
-    v = warp_sum(v);
-    if (lane_id() == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    int64_t s = 0;
-    for (int w = 0; w < (int)kNodeTile / 32; ++w) s += red[w];
-    __syncthreads();
-    return s;
-}
-__device__ __forceinline__ int block_exscan_512(int v, int *sc) {
-    const int lane = (int)lane_id(), w = (int)(threadIdx.x >> 5);
-    int x = v;                                       // inclusive warp scan
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sc[w] = x;
-    __syncthreads();
-    int base = 0;
-    for (int q = 0; q < w; ++q) base += sc[q];
-    __syncthreads();
-    return base + x - v;
-}
-
-__global__ void __launch_bounds__(kTileThreads) k_tile_layout(const int64_t *__restrict__ lc, int64_t n,
-                                                               int64_t ntile, int eb, int64_t stage_cap,
-                                                               uint32_t *__restrict__ vofs,
-                                                               uint16_t *__restrict__ vfirst,
-                                                               uint16_t *__restrict__ plist, int32_t *__restrict__ vcap,
-                                                               int64_t *__restrict__ pcnt, int32_t *__restrict__ lstage) {
-    __shared__ int64_t d_s[kNodeTile];
-    __shared__ int32_t len_s[kVRows], lenr_s[kVRows];
-    __shared__ uint16_t vf_s[kNodeTile + 1], rank_s[kVRows];
-    __shared__ int s_V;
-    __shared__ int64_t s_red[kNodeTile / 32 + 1];
-    __shared__ int s_scan[kNodeTile / 32 + 1];
-    const int k = threadIdx.x;
-    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
-        const int64_t a0 = t * kNodeTile;
-        const int nn = (int)min(kNodeTile, n - a0);
-        const int64_t dk = k < nn ? lc[a0 + k] : 0;
-        d_s[k] = dk;
-        // cap: at most kVRows pieces (E / cap + nonzero rows <= kVRows); block sums
-        const int64_t E = block_sum_512(dk, s_red), nz = block_sum_512((int64_t)(dk > 0), s_red);
-        const int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
-        // node k's pieces: its slots in node order (exclusive scan of the piece counts)
-        const int np = (int)((dk + cap - 1) / cap);
-        const int first = block_exscan_512(np, s_scan);
-        vf_s[k] = (uint16_t)first;
-        for (int q = 0; q < np; ++q) len_s[first + q] = (int32_t)min(cap, dk - (int64_t)q * cap);
-        if (k == kNodeTile - 1) {
-            vf_s[kNodeTile] = (uint16_t)(first + np);
-            s_V = first + np;
-            vcap[t] = (int32_t)cap;
-        }
-        __syncthreads();
-        const int V = s_V;
-        for (int p = k; p < V; p += kTileThreads) {   // rank: longest first, ties by piece order
-            const int lp = len_s[p];
-            int r = 0;
-            for (int q = 0; q < V; ++q) {
-                const int lq = len_s[q];
-                r += (lq > lp) || (lq == lp && q < p);
-            }
-            rank_s[p] = (uint16_t)r;
-            lenr_s[r] = lp;
-        }
-        __syncthreads();
-        for (int p = k; p < kVRows; p += kTileThreads) plist[t * kVRows + p] = p < V ? rank_s[p] : 0;
-        for (int i = k; i < kVfStride; i += kTileThreads) vfirst[t * kVfStride + i] = vf_s[min(i, (int)kNodeTile)];
-        if (k == 0) {
-            uint32_t off = 0;
-            for (int vw = 0; vw < kVWarps; ++vw) {
-                vofs[t * kVofsStride + vw] = off;
-                off += 32u * (uint32_t)(32 * vw < V ? lenr_s[32 * vw] : 0);   // the virtual warp's longest piece
-            }
-            for (int vw = kVWarps; vw < kVofsStride; ++vw) vofs[t * kVofsStride + vw] = off;
-            pcnt[t] = off;
-            // shared-memory staging (k_tile): the longest suffix of virtual warps whose
-            // slots (eb bytes each) fit the edge buffer; the others are read from L2
-            int v = 0;
-            while (v < kVWarps && (int64_t)(off - vofs[t * kVofsStride + v]) * eb > stage_cap) ++v;
-            lstage[t] = (int32_t)(v < kVWarps ? vofs[t * kVofsStride + v] : off);
-        }
-        __syncthreads();
-    }
-}
-
-// light offsets relative to the tile, tile bases, heavy index, out-degree
-__global__ void k_tile_rel(const int64_t *__restrict__ rptr, const int64_t *__restrict__ hpos,
-                           const int64_t *__restrict__ hflag, const int64_t *__restrict__ row_ptr, int64_t n,
-                           int64_t nt, int64_t ntile, uint32_t *__restrict__ rrel, int32_t *__restrict__ hidx,
-                           int32_t *__restrict__ deg, int64_t *__restrict__ rtile) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= nt; j += (int64_t)gridDim.x * blockDim.x) {
-        if (j < nt) hidx[j] = hflag[j] ? (int32_t)hpos[j] : -1;
-        if (j < n) {
-            const int64_t b = (j / kNodeTile) * kNodeTile;
-            rrel[j] = (uint32_t)(rptr[j] - rptr[b]);
-            deg[j] = (int32_t)(row_ptr[j + 1] - row_ptr[j]);
-        }
-        if (j <= n && (j % kNodeTile == 0 || j == n)) {
-            const int64_t t = (j + kNodeTile - 1) / kNodeTile;   // j == n: the end of the last tile
-            if (t <= ntile) rtile[t] = rptr[j];
-        }
-    }
-}
-
-template <typename W>
-__global__ void k_fill_pad(uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ lw, int64_t cnt) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
-        lsrc[e] = (uint16_t)kNodeTile;     // the always-zero outflow slot
-        if (lw) lw[e] = StoreW<W>(0);
-    }
-}
-
-// ---- edge-parallel plan build (hub targets with millions of in-edges must not
-// serialise on one warp): target of every CSC position, local flags, their
-// exclusive scan L, so that a local in-edge's rank within its target is
-// L[k] - L[tptr[t]] and a remote one's (k - tptr[t]) minus that.
-__global__ void k_fill_tkey(const int64_t *__restrict__ tptr, int64_t nt, uint32_t *__restrict__ tkey) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = warp; t < nt; t += nw)
-        for (int64_t k = tptr[t] + lane_id(); k < tptr[t + 1]; k += 32) tkey[k] = (uint32_t)t;
-}
-
-template <typename LT>
-__global__ void k_local_flags(const uint32_t *__restrict__ tkey, const int32_t *__restrict__ tsrc, int64_t m,
-                              int64_t n, LT *__restrict__ flag) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= m; k += (int64_t)gridDim.x * blockDim.x) {
-        if (k == m) {
-            flag[k] = 0;
-            continue;
-        }
-        const int64_t t = tkey[k];
-        flag[k] = (t < n && tsrc[k] / kNodeTile == t / kNodeTile) ? 1 : 0;
-    }
-}
-
-template <typename LT>
-__global__ void k_counts_from_scan(const int64_t *__restrict__ tptr, const LT *__restrict__ L, int64_t nt,
-                                   int64_t *__restrict__ lc, int64_t *__restrict__ rc) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = tptr[t], e = tptr[t + 1];
-        lc[t] = L[e] - L[b];
-        rc[t] = (e - b) - lc[t];
-    }
-}
-
-// every in-edge to its class, one thread per CSC position (see k_split_edges)
-template <typename W, typename LT>
-__global__ void k_split_flat(const int64_t *__restrict__ tptr, const uint32_t *__restrict__ tkey,
-                             const int32_t *__restrict__ tsrc, const StoreW<W> *__restrict__ tw,
-                             const LT *__restrict__ L, int64_t m, int64_t n, const int64_t *__restrict__ ltile,
-                             const uint32_t *__restrict__ vofs, const uint16_t *__restrict__ vfirst,
-                             const uint16_t *__restrict__ plist, const int32_t *__restrict__ vcap,
-                             const int64_t *__restrict__ rptr, const int64_t *__restrict__ hptr,
-                             const int32_t *__restrict__ hidx, int64_t stripe_nodes, int64_t nstripe, int waves,
-                             uint16_t *__restrict__ lsrc, StoreW<W> *__restrict__ lw, RemRec<W> *__restrict__ rrec,
-                             RemRec<W> *__restrict__ htmp, uint32_t *__restrict__ hkey, uint32_t *__restrict__ hval,
-                             uint32_t *__restrict__ hof) {
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = tkey[k];
-        const int32_t s = tsrc[k];
-        const int64_t b = tptr[t];
-        const int64_t lrank = (int64_t)(L[k] - L[b]);
-        const bool owned = t < n;
-        const int64_t tile = owned ? t / kNodeTile : -1;
-        if (owned && s / kNodeTile == tile) {
-            // balanced sliced-ELL: local in-edge q of t is slot q % cap of its piece q / cap
-            const int64_t cap = vcap[tile];
-            const int pf = vfirst[tile * kVfStride + (t - tile * kNodeTile)];
-            const int r = plist[tile * kVRows + pf + (int)(lrank / cap)];
-            const uint32_t v0 = vofs[tile * kVofsStride + r / 32], v1 = vofs[tile * kVofsStride + r / 32 + 1];
-            const int64_t o = ltile[tile] + v0 + ell_slot(lrank % cap, r % 32, (v1 - v0) / 32);
-            lsrc[o] = (uint16_t)(s - tile * kNodeTile);
-            if constexpr (kW) lw[o] = tw[k];
-        } else {
-            const int32_t hx = hidx[t];
-            const int64_t o = (hx >= 0 ? hptr[t] : rptr[t]) + (k - b) - lrank;
-            RemRec<W> r{};
-            r.src = s;
-            if constexpr (kW) r.w = tw[k];
-            else r.w = 1.0f;
-            if (hx >= 0) {
-                htmp[o] = r;
-                // heavy edges grouped by (wave of the target, stripe of the source)
-                hkey[o] = (uint32_t)((owned ? tile_wave(t, waves) : 0) * nstripe + s / stripe_nodes);
-                hval[o] = (uint32_t)o;
-                hof[o] = (uint32_t)hx;
-            } else {
-                rrec[o] = r;
-            }
-        }
-    }
-}
-
-// heavy edges in (stripe, target, source) order: records, stripe and target of each
-template <typename W>
-__global__ void k_heavy_gather(const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sval, int64_t mh,
-                               const RemRec<W> *__restrict__ htmp, const uint32_t *__restrict__ hof,
-                               RemRec<W> *__restrict__ hrec, uint32_t *__restrict__ hh) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = sval[p];
-        hrec[p] = htmp[q];
-        hh[p] = hof[q];
-    }
-}
-
-// run / segment / chunk flags: run = (stripe, target); chunk = 2048 edges from
-// the stripe's start; segment = run cut at chunk starts
-__global__ void k_heavy_flags(const uint32_t *__restrict__ st, const uint32_t *__restrict__ hh, int64_t mh,
-                              const int64_t *__restrict__ sbeg, int64_t *__restrict__ runf, int64_t *__restrict__ segf,
-                              int64_t *__restrict__ chkf) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = st[p];
-        const bool run = p == 0 || st[p - 1] != s || hh[p - 1] != hh[p];
-        const bool chk = (p - sbeg[s]) % kHeavyChunk == 0;
-        runf[p] = run;
-        chkf[p] = chk;
-        segf[p] = run || chk;
-    }
-}
-
-__global__ void k_heavy_index(const int64_t *__restrict__ runf, const int64_t *__restrict__ segf,
-                              const int64_t *__restrict__ chkf, const int64_t *__restrict__ runid,
-                              const int64_t *__restrict__ segid, const int64_t *__restrict__ chkid,
-                              const uint32_t *__restrict__ hh, const uint32_t *__restrict__ st, int64_t mh,
-                              int64_t nstripe, int64_t nh, int64_t *__restrict__ seg_start,
-                              int64_t *__restrict__ chunk_start, int64_t *__restrict__ cfirst,
-                              int32_t *__restrict__ run_h, int64_t *__restrict__ run_seg,
-                              uint32_t *__restrict__ rkey, uint32_t *__restrict__ rval) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x) {
-        if (segf[p]) seg_start[segid[p]] = p;
-        if (chkf[p]) {
-            chunk_start[chkid[p]] = p;
-            cfirst[chkid[p]] = segid[p];
-        }
-        if (runf[p]) {
-            const int64_t r = runid[p];
-            run_h[r] = (int32_t)hh[p];
-            run_seg[r] = segid[p];
-            // fold order: by (wave of the target, heavy index); a stable sort keeps stripe order
-            rkey[r] = (uint32_t)((int64_t)(st[p] / nstripe) * nh + hh[p]);
-            rval[r] = (uint32_t)r;
-        }
-    }
-}
-
-// fold index: target slot of every sorted run position (flags on key changes)
-__global__ void k_fold_flags(const uint32_t *__restrict__ skey, int64_t nrun, int64_t *__restrict__ flag) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nrun; p += (int64_t)gridDim.x * blockDim.x)
-        flag[p] = (p == 0 || skey[p - 1] != skey[p]) ? 1 : 0;
-}
-
-__global__ void k_fold_index(const uint32_t *__restrict__ skey, const int64_t *__restrict__ flag,
-                             const int64_t *__restrict__ slot, int64_t nrun, int64_t nh, int64_t *__restrict__ fold_ptr,
-                             int32_t *__restrict__ fold_h, unsigned long long *__restrict__ wave_first) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nrun; p += (int64_t)gridDim.x * blockDim.x)
-        if (flag[p]) {
-            fold_ptr[slot[p]] = p;
-            fold_h[slot[p]] = (int32_t)(skey[p] % (uint32_t)nh);
-            atomicMin(&wave_first[skey[p] / (uint32_t)nh], (unsigned long long)slot[p]);
-        }
-}
-
-__global__ void k_fill_u64(unsigned long long *__restrict__ p, int64_t cnt, unsigned long long v) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = v;
-}
-
-// share of every source's out-weight that leaves its tile: a thread per source
-// (rows of more than 32 edges by the whole warp)
-template <typename W>
-__global__ void k_remote_share(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                               const StoreW<W> *__restrict__ w, const double *__restrict__ inv, int64_t n,
-                               int waves, float *__restrict__ wr) {
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    const int lane = lane_id();
-    // leaves the tile and is still pending after the sweep (a later wave takes its
-    // pushes in during the sweep, R15); ghost targets always pending
-    auto pending = [&](int64_t i, int64_t e) {
-        const int64_t t = col[e];
-        return t >= n || (t / kNodeTile != i / kNodeTile && tile_wave(t, waves) <= tile_wave(i, waves));
-    };
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int64_t i = base + threadIdx.x;
-        int64_t b = 0, e = 0;
-        if (i < n) {
-            b = row_ptr[i];
-            e = row_ptr[i + 1];
-        }
-        const bool big = e - b > 32;
-        if (i < n && !big) {
-            double s = 0.0;
-            for (int64_t q = b; q < e; ++q)
-                if (pending(i, q)) s += kW ? (double)w[q] : 1.0;
-            wr[i] = (float)(s * inv[i]);
-        }
-        unsigned m = __ballot_sync(0xffffffffu, big);
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            const int64_t il = __shfl_sync(0xffffffffu, i, l), bl = __shfl_sync(0xffffffffu, b, l),
-                          el = __shfl_sync(0xffffffffu, e, l);
-            double s = 0.0;
-            for (int64_t q = bl + lane; q < el; q += 32)
-                if (pending(il, q)) s += kW ? (double)w[q] : 1.0;
-            s = warp_sum(s);
-            if (lane == 0) wr[il] = (float)(s * inv[il]);
-        }
-    }
-}
-
-// Bank-aware slot order: the rounds gather gq[src] for 32
-// pieces at once, one slot row per load; a 64-bit shared load is served per
-// half-warp, one wavefront per distinct bank pair (src mod 16) hit twice.  The
-// order of a piece's slots is free (any fixed order is a valid summation
-// order, R14), so each virtual warp's rows are refilled greedily: per row, the
-// lanes of a half-warp claim distinct bank pairs, the most frequent remaining
-// ones first; padding slots (zero outflow) take a free pair.  One warp per
-// virtual warp of <= kBalMaxK slots per lane (longer ones keep edge order).
-constexpr int kBalMaxK = 32, kBalWarps = 4;
-template <typename W>
-__global__ void __launch_bounds__(kBalWarps * 32) k_ell_balance(const int64_t *__restrict__ ltile,
-                                                                const uint32_t *__restrict__ vofs, int64_t ntile,
-                                                                uint16_t *__restrict__ lsrc,
-                                                                StoreW<W> *__restrict__ lw) {
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    __shared__ uint16_t es[kBalWarps][kBalMaxK][32];
-    __shared__ StoreW<W> ew[kBalWarps][kW ? kBalMaxK : 1][32];
-    __shared__ uint8_t ord[kBalWarps][kBalMaxK][32];
-    __shared__ int cnt[kBalWarps][2][16];
-    const int wb = threadIdx.x >> 5, lane = lane_id(), half = lane >> 4;
-    const int64_t nitem = ntile * kVWarps;
-    for (int64_t item = (int64_t)blockIdx.x * kBalWarps + wb; item < nitem; item += (int64_t)gridDim.x * kBalWarps) {
-        const int64_t tile = item / kVWarps;
-        const int vw = (int)(item % kVWarps);
-        const uint32_t o0 = vofs[tile * kVofsStride + vw];
-        const int K = (int)((vofs[tile * kVofsStride + vw + 1] - o0) >> 5);
-        if (K < 2 || K > kBalMaxK) continue;           // warp-uniform
-        const int64_t base = ltile[tile] + o0;
-        if (lane < 16) cnt[wb][0][lane] = cnt[wb][1][lane] = 0;
-        __syncwarp();
-        for (int s = 0; s < K; ++s) {
-            const int64_t pos = base + ell_slot(s, lane, K);
-            const int src = lsrc[pos];
-            es[wb][s][lane] = (uint16_t)src;
-            if constexpr (kW) ew[wb][s][lane] = lw[pos];
-            if (src < (int)kNodeTile) atomicAdd(&cnt[wb][half][src & 15], 1);
-        }
-        __syncwarp();
-        uint32_t rem = K == 32 ? 0xffffffffu : ((1u << K) - 1u);
-        for (int r = 0; r < K; ++r) {
-            unsigned used = 0;
-            int choice = -1, cb = -1;
-            for (int it = 0; it < 4; ++it) {
-                int best = -1, bb = -1, bc = -1;
-                if (choice < 0)
-                    for (uint32_t m = rem; m; m &= m - 1) {
-                        const int e = __ffs(m) - 1;
-                        const int src = es[wb][e][lane];
-                        if (src >= (int)kNodeTile) continue;
-                        const int b = src & 15;
-                        if ((used >> b) & 1u) continue;
-                        const int c = cnt[wb][half][b];
-                        if (c > bc) {
-                            bc = c;
-                            best = e;
-                            bb = b;
-                        }
-                    }
-                const bool prop = choice < 0 && best >= 0;
-                const unsigned peers = __match_any_sync(0xffffffffu, prop ? half * 16 + bb : 64 + lane);
-                const bool win = prop && lane == __ffs(peers) - 1;
-                if (win) {
-                    choice = best;
-                    cb = bb;
-                }
-                unsigned bits = win ? (1u << bb) : 0u;
-                for (int o = 8; o; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
-                used |= bits;
-            }
-            // left over: a padding slot takes a free bank pair, else the most frequent remaining entry
-            int pad = -1;
-            if (choice < 0)
-                for (uint32_t m = rem; m; m &= m - 1) {
-                    const int e = __ffs(m) - 1;
-                    if (es[wb][e][lane] >= (int)kNodeTile) {
-                        pad = e;
-                        break;
-                    }
-                }
-            const unsigned padl = __ballot_sync(0xffffffffu, pad >= 0) & (half ? 0xffff0000u : 0x0000ffffu);
-            if (pad >= 0) {
-                int k = __popc(padl & ((1u << lane) - 1u));
-                unsigned fr = ~used & 0xffffu;
-                int b = 0;
-                for (; fr && k > 0; --k) fr &= fr - 1;
-                if (fr) b = __ffs(fr) - 1;
-                choice = pad;
-                es[wb][pad][lane] = (uint16_t)(kNodeTile + b);
-            } else if (choice < 0) {
-                int bc = -1;
-                for (uint32_t m = rem; m; m &= m - 1) {
-                    const int e = __ffs(m) - 1;
-                    const int b = es[wb][e][lane] & 15;
-                    if (cnt[wb][half][b] > bc) {
-                        bc = cnt[wb][half][b];
-                        choice = e;
-                        cb = b;
-                    }
-                }
-            }
-            __syncwarp();
-            if (pad < 0) atomicSub(&cnt[wb][half][cb], 1);
-            ord[wb][r][lane] = (uint8_t)choice;
-            rem &= ~(1u << choice);
-            __syncwarp();
-        }
-        for (int r = 0; r < K; ++r) {
-            const int e = ord[wb][r][lane];
-            const int64_t pos = base + ell_slot(r, lane, K);
-            lsrc[pos] = es[wb][e][lane];
-            if constexpr (kW) lw[pos] = ew[wb][e][lane];
-        }
-        __syncwarp();
-    }
-}
-
-__global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntile, unsigned long long *__restrict__ mx) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntile; t += (int64_t)gridDim.x * blockDim.x)
-        atomicMax(mx, (unsigned long long)(ltile[t + 1] - ltile[t]));
-}
-
-void free_tiles(TilePlan &t) {
-    for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
-                    (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
-                    (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
-                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run})
-        cudaFree(p);
-    t = TilePlan();
-}
-
-static int64_t read_i64(const int64_t *p, cudaStream_t st) {
-    int64_t v = 0;
-    DI_CUDA(cudaMemcpyAsync(&v, p, sizeof(v), cudaMemcpyDeviceToHost, st));
-    DI_CUDA(cudaStreamSynchronize(st));
-    return v;
-}
-
-static int bits_for(int64_t x) {
-    int b = 1;
-    while (b < 32 && ((int64_t)1 << b) < x) ++b;
-    return b;
-}
-
-__global__ void k_u32_to_i64(const uint32_t *__restrict__ a, int64_t *__restrict__ b, int64_t cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
-        b[i] = a[i];
-}
-
-// per-stripe edge counts of the sorted stripe keys
-__global__ void k_stripe_count(const uint32_t *__restrict__ st, int64_t mh, unsigned long long *__restrict__ cnt) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < mh; p += (int64_t)gridDim.x * blockDim.x)
-        if (p == mh - 1 || st[p + 1] != st[p]) atomicAdd(&cnt[st[p]], (unsigned long long)(p + 1));
-}
-
-template <typename W>
-static void build_tiles_t(di_graph *h) {
-    DevGraph &g = h->g;
-    TilePlan &tp = g.tl;
-    cudaStream_t st = h->stream;
-    const int64_t n = g.n;
-    const int grid = h->num_sms * 8;
-    using SW = StoreW<W>;
-    constexpr bool kW = !std::is_same<W, NoW>::value;
-    const size_t rs = sizeof(RemRec<W>);
-    const int64_t nt = g.nt;                         // owned nodes + shard ghost slots
-    phase_mark(st, "tiles: start");
-    tp.ntile = (n + kNodeTile - 1) / kNodeTile;
-    tp.stripe_nodes = std::max<int64_t>(kNodeTile, kStripeBytes / (int64_t)sizeof(double));
-    if (const char *e = getenv("DIT_STRIPE_NODES")) tp.stripe_nodes = std::max<int64_t>(kNodeTile, atoll(e));   // tests
-    const int64_t nS = (n + tp.stripe_nodes - 1) / tp.stripe_nodes;
-    tp.nstripe = nS;
-    tp.waves = kTileWaves;                           // shards too (R16: cross-rank pushes wait a sweep)
-    if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = std::max(1, atoi(e));
-    // empty waves dropped; at most 32 (the per-wave totals of k_tile's partials array)
-    tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(tp.waves, 32), tp.ntile));
-    const int64_t S = tp.waves * nS;                 // heavy groups (wave, stripe)
-    // ---- classes of the in-edges
-    int64_t *lc, *rc, *lrc, *hc, *hflag, *rptr, *hptr, *hpos;
-    for (int64_t **p : {&lc, &rc, &lrc, &hc, &hflag, &rptr, &hptr, &hpos})
-        DI_CUDA(cudaMallocAsync(p, (nt + 1) * sizeof(int64_t), st));
-    const int64_t m = g.m;
-    uint32_t *tkey = g.t.tkey;                       // the transpose's sorted keys when it kept them
-    g.t.tkey = nullptr;
-    if (!tkey) {
-        DI_CUDA(cudaMallocAsync(&tkey, (m > 0 ? m : 1) * sizeof(uint32_t), st));
-        k_fill_tkey<<<grid, 256, 0, st>>>(g.t.ptr, nt, tkey);
-        count_launch();
-    }
-    // local rank of every CSC position among its target's local in-edges: a scan of
-    // local flags (32-bit through CUB when m < 2^31, else 64-bit)
-    const bool l32 = m < (int64_t)0x7fffffff && !getenv("DIT_FORCE_L64");   // DIT_FORCE_L64: tests of the 64-bit path
-    void *L = nullptr;
-    {
-        const size_t ls = l32 ? sizeof(uint32_t) : sizeof(int64_t);
-        void *lflag = nullptr;
-        DI_CUDA(cudaMallocAsync(&lflag, (m + 1) * ls, st));
-        DI_CUDA(cudaMallocAsync(&L, (m + 1) * ls, st));
-        if (l32) {
-            k_local_flags<uint32_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (uint32_t *)lflag);
-            size_t tb = 0;
-            DI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (uint32_t *)lflag, (uint32_t *)L, (int)(m + 1), st));
-            {
-                std::lock_guard<std::mutex> lock(scratch_mutex(h->device));
-                DI_CUDA(cub::DeviceScan::ExclusiveSum(cub_scratch(h->device, tb), tb, (uint32_t *)lflag, (uint32_t *)L,
-                                                      (int)(m + 1), st));
-                DI_CUDA(cudaStreamSynchronize(st));
-            }
-            k_counts_from_scan<uint32_t><<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, (const uint32_t *)L, nt, lc, rc);
-        } else {
-            k_local_flags<int64_t><<<grid_for(h, m + 1), 256, 0, st>>>(tkey, g.t.src, m, n, (int64_t *)lflag);
-            exclusive_scan_i64((const int64_t *)lflag, (int64_t *)L, m, st);
-            k_counts_from_scan<int64_t><<<grid_for(h, nt), 256, 0, st>>>(g.t.ptr, (const int64_t *)L, nt, lc, rc);
-        }
-        count_launch(2);
-        DI_CUDA(cudaFreeAsync(lflag, st));
-    }
-    k_classify<<<grid_for(h, tp.ntile), 256, 0, st>>>(rc, n, tp.ntile, lrc, hc, hflag);
-    count_launch(2);
-    if (nt > n) {
-        k_classify_ghosts<<<grid_for(h, nt - n), 256, 0, st>>>(rc, n, nt, lrc, hc, hflag);
-        count_launch();
-    }
-    exclusive_scan_i64(lrc, rptr, nt, st);
-    exclusive_scan_i64(hc, hptr, nt, st);
-    exclusive_scan_i64(hflag, hpos, nt, st);
-    tp.mlight = read_i64(rptr + nt, st);
-    tp.mh = read_i64(hptr + nt, st);
-    tp.nh = read_i64(hpos + nt, st);
-    if (tp.mh >= (int64_t)0xffffffffLL) {
-        set_error("tiled plan: too many heavy remote edges for one graph handle");
-        throw Fail{DI_ERR_INVALID};
-    }
-    phase_mark(st, "tiles: classify");
-    // ---- sliced-ELL layout of the local in-edges
-    int32_t *vcap;
-    int64_t *pcnt;
-    DI_CUDA(cudaMallocAsync(&vcap, (tp.ntile + 1) * sizeof(int32_t), st));
-    DI_CUDA(cudaMallocAsync(&pcnt, (tp.ntile + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMallocAsync(&tp.vofs, tp.ntile * kVofsStride * sizeof(uint32_t), st));
-    DI_CUDA(cudaMallocAsync(&tp.vfirst, tp.ntile * kVfStride * sizeof(uint16_t), st));
-    DI_CUDA(cudaMallocAsync(&tp.plist, tp.ntile * kVRows * sizeof(uint16_t), st));
-    DI_CUDA(cudaMallocAsync(&tp.ltile, (tp.ntile + 1) * sizeof(int64_t), st));
-    DI_CUDA(cudaMallocAsync(&tp.lstage, (tp.ntile + 1) * sizeof(int32_t), st));
-    k_tile_layout<<<(unsigned)std::min<int64_t>(tp.ntile, (int64_t)h->num_sms * 4), kTileThreads, 0, st>>>(
-        lc, n, tp.ntile, (int)(2 + (kW ? sizeof(SW) : 0)), (int64_t)(tile_e_buf<W>() - kMetaBytes), tp.vofs,
-        tp.vfirst, tp.plist, vcap, pcnt, tp.lstage);
-    count_launch();
-    exclusive_scan_i64(pcnt, tp.ltile, tp.ntile, st);
-    tp.mpad = read_i64(tp.ltile + tp.ntile, st);
-    tp.mloc = g.m - tp.mlight - tp.mh;
-    // +16 B: aligned TMA supersets may read up to 15 bytes past the end
-    DI_CUDA(cudaMallocAsync(&tp.lsrc, tp.mpad * sizeof(uint16_t) + 16, st));
-    if (kW) DI_CUDA(cudaMallocAsync(&tp.lw, tp.mpad * sizeof(SW) + 16, st));
-    if (tp.mpad > 0) {
-        k_fill_pad<W><<<grid_for(h, tp.mpad), 256, 0, st>>>(tp.lsrc, (SW *)tp.lw, tp.mpad);
-        count_launch();
-    }
-    phase_mark(st, "tiles: ELL layout");
-    // ---- per-node arrays, tile bases
-    DI_CUDA(cudaMallocAsync(&tp.rrel, n * sizeof(uint32_t) + 16, st));
-    DI_CUDA(cudaMallocAsync(&tp.hidx, nt * sizeof(int32_t) + 16, st));
-    DI_CUDA(cudaMallocAsync(&tp.wr, n * sizeof(float) + 16, st));
-    DI_CUDA(cudaMallocAsync(&tp.deg, n * sizeof(int32_t) + 16, st));
-    DI_CUDA(cudaMallocAsync(&tp.rtile, (tp.ntile + 1) * sizeof(int64_t), st));
-    k_tile_rel<<<grid_for(h, nt + 1), 256, 0, st>>>(rptr, hpos, hflag, g.row_ptr, n, nt, tp.ntile, tp.rrel, tp.hidx,
-                                                    tp.deg, tp.rtile);
-    k_remote_share<W><<<grid_for(h, n), 256, 0, st>>>(g.row_ptr, g.col, (const SW *)g.w, g.inv, n, tp.waves, tp.wr);
-    count_launch(2);
-    phase_mark(st, "tiles: node arrays");
-    // ---- edges to their classes
-    DI_CUDA(cudaMallocAsync(&tp.rrec, tp.mlight * rs + 16, st));
-    DI_CUDA(cudaMallocAsync(&tp.hrec, tp.mh * rs + 16, st));
-    const int64_t mh1 = tp.mh > 0 ? tp.mh : 1;
-    RemRec<W> *htmp;
-    uint32_t *k0, *v0, *k1, *v1, *hof, *hh;
-    DI_CUDA(cudaMallocAsync(&htmp, mh1 * rs, st));
-    for (uint32_t **p : {&k0, &v0, &k1, &v1, &hof, &hh}) DI_CUDA(cudaMallocAsync(p, mh1 * sizeof(uint32_t), st));
-    if (m > 0 && l32)
-        k_split_flat<W, uint32_t><<<grid_for(h, m), 256, 0, st>>>(
-            g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, (const uint32_t *)L, m, n, tp.ltile, tp.vofs, tp.vfirst,
-            tp.plist, vcap, rptr, hptr, tp.hidx, tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
-            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
-    else if (m > 0)
-        k_split_flat<W, int64_t><<<grid_for(h, m), 256, 0, st>>>(
-            g.t.ptr, tkey, g.t.src, (const SW *)g.t.w, (const int64_t *)L, m, n, tp.ltile, tp.vofs, tp.vfirst,
-            tp.plist, vcap, rptr, hptr, tp.hidx, tp.stripe_nodes, nS, tp.waves, tp.lsrc, (SW *)tp.lw,
-            (RemRec<W> *)tp.rrec, htmp, k0, v0, hof);
-    DI_CUDA(cudaFreeAsync(tkey, st));
-    DI_CUDA(cudaFreeAsync(L, st));
-    count_launch();
-    if (tp.mpad > 0 && getenv("DIT_BANK_ORDER")) {   // opt-in: ~1% faster rounds for ~55 ms of build (configs[2])
-        k_ell_balance<W><<<(int)std::min<int64_t>(tp.ntile * kVWarps / kBalWarps + 1, (int64_t)h->num_sms * 16),
-                           kBalWarps * 32, 0, st>>>(
-            tp.ltile, tp.vofs, tp.ntile, tp.lsrc, (SW *)tp.lw);
-        count_launch();
-    }
-    phase_mark(st, "tiles: split edges");
-    // ---- heavy edges by (stripe, target, source): a stable sort on the stripe
-    tp.s_chunk.assign(S + 1, 0);
-    if (tp.mh > 0) {
-        auto sorted = radix_sort_u32(k0, v0, k1, v1, tp.mh, bits_for(S + 1), st);
-        uint32_t *skey = sorted.first, *sval = sorted.second;
-        k_heavy_gather<W><<<grid_for(h, tp.mh), 256, 0, st>>>(skey, sval, tp.mh, htmp, hof, (RemRec<W> *)tp.hrec, hh);
-        count_launch();
-        phase_mark(st, "heavy: stripe sort");
-        // stripe starts
-        unsigned long long *scnt;
-        DI_CUDA(cudaMallocAsync(&scnt, (S + 1) * sizeof(unsigned long long), st));
-        DI_CUDA(cudaMemsetAsync(scnt, 0, (S + 1) * sizeof(unsigned long long), st));
-        k_stripe_count<<<grid_for(h, tp.mh), 256, 0, st>>>(skey, tp.mh, scnt);
-        count_launch();
-        std::vector<unsigned long long> ends(S + 1);
-        DI_CUDA(cudaMemcpyAsync(ends.data(), scnt, (S + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        DI_CUDA(cudaStreamSynchronize(st));
-        std::vector<int64_t> sbeg(S + 1, 0);
-        for (int64_t s = 0, last = 0; s < S; ++s) {   // ends[s] = one past the stripe's last edge (0 if empty)
-            sbeg[s] = last;
-            if (ends[s]) last = (int64_t)ends[s];
-            sbeg[s + 1] = last;
-        }
-        for (int64_t s = 0; s < S; ++s)
-            tp.s_chunk[s + 1] = tp.s_chunk[s] + (sbeg[s + 1] - sbeg[s] + kHeavyChunk - 1) / kHeavyChunk;
-        tp.nchunk = tp.s_chunk[S];
-        int64_t *sbeg_d;
-        DI_CUDA(cudaMallocAsync(&sbeg_d, (S + 1) * sizeof(int64_t), st));
-        DI_CUDA(cudaMemcpyAsync(sbeg_d, sbeg.data(), (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        // flags -> ids
-        int64_t *runf, *segf, *chkf, *runid, *segid, *chkid;
-        for (int64_t **p : {&runf, &segf, &chkf, &runid, &segid, &chkid})
-            DI_CUDA(cudaMallocAsync(p, (tp.mh + 1) * sizeof(int64_t), st));
-        k_heavy_flags<<<grid_for(h, tp.mh), 256, 0, st>>>(skey, hh, tp.mh, sbeg_d, runf, segf, chkf);
-        count_launch();
-        exclusive_scan_i64(runf, runid, tp.mh, st);
-        exclusive_scan_i64(segf, segid, tp.mh, st);
-        exclusive_scan_i64(chkf, chkid, tp.mh, st);
-        phase_mark(st, "heavy: flags + scans");
-        tp.nrun = read_i64(runid + tp.mh, st);
-        tp.nseg = read_i64(segid + tp.mh, st);
-        if (read_i64(chkid + tp.mh, st) != tp.nchunk) {
-            set_error("tiled plan: heavy chunk count mismatch");
-            throw Fail{DI_ERR_CUDA};
-        }
-        DI_CUDA(cudaMallocAsync(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t), st));
-        DI_CUDA(cudaMallocAsync(&tp.chunk_start, (tp.nchunk + 1) * sizeof(int64_t), st));
-        DI_CUDA(cudaMallocAsync(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t), st));
-        DI_CUDA(cudaMallocAsync(&tp.run_h, tp.nrun * sizeof(int32_t), st));
-        DI_CUDA(cudaMallocAsync(&tp.run_seg, (tp.nrun + 1) * sizeof(int64_t), st));
-        DI_CUDA(cudaMallocAsync(&tp.part, tp.nseg * sizeof(double), st));
-        uint32_t *rk0, *rv0, *rk1, *rv1;
-        for (uint32_t **p : {&rk0, &rv0, &rk1, &rv1}) DI_CUDA(cudaMallocAsync(p, tp.nrun * sizeof(uint32_t), st));
-        k_heavy_index<<<grid_for(h, tp.mh), 256, 0, st>>>(runf, segf, chkf, runid, segid, chkid, hh, skey, tp.mh, nS,
-                                                          tp.nh, tp.seg_start, tp.chunk_start, tp.cfirst, tp.run_h,
-                                                          tp.run_seg, rk0, rv0);
-        count_launch();
-        if ((int64_t)tp.waves * tp.nh >= (int64_t)0xffffffffLL) {
-            set_error("tiled plan: too many heavy targets for one graph handle");
-            throw Fail{DI_ERR_INVALID};
-        }
-        // the heavy targets of each wave, each with its runs in stripe order (k_heavy_fold)
-        {
-            auto fs = radix_sort_u32(rk0, rv0, rk1, rv1, tp.nrun, bits_for((int64_t)tp.waves * tp.nh + 1), st);
-            int64_t *ff, *fslot;
-            DI_CUDA(cudaMallocAsync(&ff, (tp.nrun + 1) * sizeof(int64_t), st));
-            DI_CUDA(cudaMallocAsync(&fslot, (tp.nrun + 1) * sizeof(int64_t), st));
-            k_fold_flags<<<grid_for(h, tp.nrun), 256, 0, st>>>(fs.first, tp.nrun, ff);
-            exclusive_scan_i64(ff, fslot, tp.nrun, st);
-            const int64_t nslot = read_i64(fslot + tp.nrun, st);
-            DI_CUDA(cudaMallocAsync(&tp.fold_ptr, (nslot + 1) * sizeof(int64_t), st));
-            DI_CUDA(cudaMallocAsync(&tp.fold_h, (nslot + 1) * sizeof(int32_t), st));
-            DI_CUDA(cudaMallocAsync(&tp.fold_run, tp.nrun * sizeof(uint32_t), st));
-            unsigned long long *wf;
-            DI_CUDA(cudaMallocAsync(&wf, (tp.waves + 1) * sizeof(unsigned long long), st));
-            k_fill_u64<<<1, 64, 0, st>>>(wf, tp.waves + 1, (unsigned long long)nslot);
-            k_fold_index<<<grid_for(h, tp.nrun), 256, 0, st>>>(fs.first, ff, fslot, tp.nrun, tp.nh, tp.fold_ptr,
-                                                               tp.fold_h, wf);
-            count_launch(3);
-            DI_CUDA(cudaMemcpyAsync(tp.fold_run, fs.second, tp.nrun * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-            DI_CUDA(cudaMemcpyAsync(tp.fold_ptr + nslot, &tp.nrun, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-            std::vector<unsigned long long> w(tp.waves + 1);
-            DI_CUDA(cudaMemcpyAsync(w.data(), wf, (tp.waves + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                    st));
-            DI_CUDA(cudaStreamSynchronize(st));
-            tp.wave_slot.assign(tp.waves + 1, nslot);
-            for (int c = tp.waves - 1; c >= 0; --c) tp.wave_slot[c] = std::min<int64_t>((int64_t)w[c], tp.wave_slot[c + 1]);
-            for (void *p : {(void *)ff, (void *)fslot, (void *)wf, (void *)rk0, (void *)rv0, (void *)rk1, (void *)rv1})
-                DI_CUDA(cudaFreeAsync(p, st));
-        }
-        DI_CUDA(cudaMemcpyAsync(tp.seg_start + tp.nseg, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        DI_CUDA(cudaMemcpyAsync(tp.chunk_start + tp.nchunk, &tp.mh, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        DI_CUDA(cudaMemcpyAsync(tp.cfirst + tp.nchunk, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        DI_CUDA(cudaMemcpyAsync(tp.run_seg + tp.nrun, &tp.nseg, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        phase_mark(st, "heavy: index");
-        for (int64_t *p : {runf, segf, chkf, runid, segid, chkid, sbeg_d}) DI_CUDA(cudaFreeAsync(p, st));
-        DI_CUDA(cudaFreeAsync(scnt, st));
-    }
-    phase_mark(st, "tiles: heavy sort + index");
-    DI_CUDA(cudaMallocAsync(&tp.hsum, (tp.nh > 0 ? tp.nh : 1) * sizeof(double), st));
-    DI_CUDA(cudaMallocAsync(&tp.tpart, (2 * (size_t)tp.waves * 4096 + 64) * sizeof(double), st));
-    unsigned long long *mx;
-    DI_CUDA(cudaMallocAsync(&mx, sizeof(unsigned long long), st));
-    DI_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
-    if (tp.ntile > 0) {
-        k_tile_max_edges<<<grid_for(h, tp.ntile), 256, 0, st>>>(tp.ltile, tp.ntile, mx);
-        count_launch();
-    }
-    unsigned long long mxh = 0;
-    DI_CUDA(cudaMemcpyAsync(&mxh, mx, sizeof(mxh), cudaMemcpyDeviceToHost, st));
-    for (int64_t *p : {lc, rc, lrc, hc, hflag, rptr, hptr, hpos, pcnt}) DI_CUDA(cudaFreeAsync(p, st));
-    for (uint32_t *p : {k0, v0, k1, v1, hof, hh}) DI_CUDA(cudaFreeAsync(p, st));
-    DI_CUDA(cudaFreeAsync(htmp, st));
-    DI_CUDA(cudaFreeAsync(vcap, st));
-    DI_CUDA(cudaFreeAsync(mx, st));
-    DI_CUDA(cudaStreamSynchronize(st));
-    DI_CUDA(cudaGetLastError());
-    tp.max_tile_edges = (int64_t)mxh;
-    tp.built = true;
-    phase_mark(st, "tiles: free + done");
-}
-
-void build_tiles(di_graph *h) {
-    DevGraph &g = h->g;
-    if (g.tl.built || g.n == 0) return;
-    build_transpose(h);
-    switch (g.w_kind) {
-    case DI_W_F32: build_tiles_t<float>(h); break;
-    case DI_W_F64: build_tiles_t<double>(h); break;
-    default: build_tiles_t<NoW>(h);
-    }
-}
 
 // ---------------------------------------------------------------- heavy remote sums
 // Heavy targets' remote inflow, per wave, in two launches:

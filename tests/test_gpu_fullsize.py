@@ -182,3 +182,54 @@ def test_tiled_edge_order_with_bank_balance(eng):
     with _env(DIT_BANK_ORDER=1):
         _tiled_elementwise(eng, g, 4, (2,))
     _tiled_elementwise(eng, g, 4, (2,))
+
+
+def _pinned(a):
+    t = torch.empty(a.shape, dtype={np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32}[a.dtype.type],
+                    pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+
+
+def test_pipelined_create_matches_lazy_build(eng):
+    # graphs of 16M+ edges created from pinned host buffers build the tile plan
+    # while the edges upload (chunks of whole tiles); the plan -- and so every bit
+    # of the solve -- is the one the lazy build makes from device-resident data
+    spec = synth.CONFIGS[2].scaled(1_200_000, seed=31)
+    g = synth.generate(spec)
+    assert g.m >= (1 << 24)
+    rp, cl, w = _pinned(g.row_ptr), _pinned(g.col), _pinned(g.w)
+    Gp = eng.DIGraph(g.n, rp, cl, w)                  # pipelined (pinned host)
+    Hp, rp_res = Gp.solve(d=D, tol=1e-12, variant="tiled")
+    dev = torch.device("cuda", 0)
+    Gl = eng.DIGraph(g.n, torch.from_numpy(g.row_ptr).to(dev), torch.from_numpy(g.col).to(dev),
+                     torch.from_numpy(g.w).to(dev))  # device CSR: plan built at the first tiled solve
+    Hl, rl_res = Gl.solve(d=D, tol=1e-12, variant="tiled")
+    assert eng._lib.di_plan_stats(Gp.handle) == eng._lib.di_plan_stats(Gl.handle)
+    assert torch.equal(Hp, Hl) and rp_res["sweeps"] == rl_res["sweeps"]
+    ref = di.di_solve(g.n, g.row_ptr, g.col, g.w, D, tol=1e-12)
+    assert np.abs(Hp.cpu().numpy() - ref.H).sum() <= L1_BAR
+    # a push solve on the same handle (transpose built on demand) agrees too
+    Hq, _ = Gp.solve(d=D, tol=1e-12, variant="auto")
+    assert np.abs(Hq.cpu().numpy() - ref.H).sum() <= L1_BAR
+    Gp.close()
+    Gl.close()
+
+
+def test_pipelined_create_rejects_bad_input(eng):
+    from paper_1501_06350_b200 import _lib
+    spec = synth.CONFIGS[2].scaled(1_000_000, seed=32)
+    g = synth.generate(spec)
+    cl = g.col.copy()
+    cl[len(cl) // 2] = g.n + 5                        # a target out of range, in a middle chunk
+    rp, clp, w = _pinned(g.row_ptr), _pinned(cl), _pinned(g.w)
+    with pytest.raises(_lib.DIError):
+        eng.DIGraph(g.n, rp, clp, w)
+    w2 = g.w.copy()
+    w2[-3] = -1.0                                     # a negative weight in the last chunk
+    with pytest.raises(_lib.DIError):
+        eng.DIGraph(g.n, rp, _pinned(g.col), _pinned(w2))
+    G = eng.DIGraph(g.n, rp, _pinned(g.col), w)       # and the device is fine afterwards
+    H, res = G.solve(d=D, tol=1e-10, variant="tiled")
+    assert res["converged"]
+    G.close()
