@@ -196,7 +196,7 @@ def load_traffic(workload, kernel):
         return None
 
 
-KERNEL_NAMES = {"tiled": {"pull": "k_heavy_s", "tile": "k_tile"}}
+KERNEL_NAMES = {"tiled": {"pull": "k_heavy_chunks+k_heavy_fold", "tile": "k_tile"}}
 
 
 def roofline_from(prof_tot, workload, variant):

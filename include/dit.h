@@ -125,8 +125,12 @@ void di_solve_opts_default(di_solve_opts *o);
  *   stream   cudaStream_t every call on this handle runs on (NULL = the CUDA
  *            default stream, the usual CUDA convention)
  * Builds on the device (Eq. (1)): the per-source scale
- * 1/sum_k w_{j,k} (1/out(j) unweighted; 0 marks a dangling node); the
- * transpose for the pull variant is built lazily on first use.
+ * 1/sum_k w_{j,k} (1/out(j) unweighted; 0 marks a dangling node).  The
+ * transpose of the pull / push variants and the tile plan of DI_VARIANT_TILED
+ * (built straight from the CSR) are built lazily on first use --
+ * except that a graph of 2^24 edges or more given in PINNED host memory
+ * (float32 or no weights) gets its tile plan during this call, chunk by chunk
+ * while its edges upload (the plan is the same bits either way).
  * Errors: DI_ERR_INVALID (sizes, null pointers, ids out of range, w <= 0),
  *         DI_ERR_OOM, DI_ERR_CUDA.
  */

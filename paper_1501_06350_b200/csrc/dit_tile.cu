@@ -347,7 +347,12 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
     constexpr int kRS = (int)sizeof(RemRec<W>);
     double *gq = reinterpret_cast<double *>(smem);                       // [kGqSlots]: outflow, zero pad slots
     double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kVRows]: piece sums by rank
-    PrepRow *Pbuf = reinterpret_cast<PrepRow *>(smem + kOffP);           // [2][kNodeTile]
+    // prepared rows, structure of arrays [2][kNodeTile] each (consecutive threads, consecutive banks)
+    double *Pf = reinterpret_cast<double *>(smem + kOffP);
+    double *Pivi = Pf + 2 * kNodeTile;
+    double *PH = Pivi + 2 * kNodeTile;
+    float *Pwr = reinterpret_cast<float *>(PH + 2 * kNodeTile);
+    int32_t *Pdeg = reinterpret_cast<int32_t *>(Pwr + 2 * kNodeTile);
     auto rbuf = [&](int x) { return smem + kOffR + x * tile_rec_buf<W>(); };
     auto ebuf = [&](int x) { return smem + tile_off_e<W>() + x * tile_e_buf<W>(); };
     // E_full, R_full: TMA completion (count 1)
@@ -414,13 +419,13 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             long long c0 = kProf ? clock64() : 0;
             bar_sync_n(kBarPFull + x, kTileBlock);
             // f, 1/sum w and the out-degree now; H and wr from P[x] again at the state out
-            const PrepRow *prow = Pbuf + x * kNodeTile + i;
+            const int pi = x * (int)kNodeTile + i;
             double f = 0.0, pivi = 0.0;
             int32_t pdeg = 0;
             if (valid) {
-                f = prow->f;
-                pivi = prow->ivi;
-                pdeg = prow->deg;
+                f = Pf[pi];
+                pivi = Pivi[pi];
+                pdeg = Pdeg[pi];
             }
             long long c1 = kProf ? clock64() : 0;
             mbar_wait(E_full(x), ph);
@@ -497,11 +502,11 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             // state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
             if (valid) {
                 a.F[j] = f;
-                if (D != 0.0) a.H[j] = prow->H + D;
+                if (D != 0.0) a.H[j] = PH[pi] + D;
                 Anext[j] = d * D * pivi;
                 // R13: the pushes still pending carry d D(i) P_{t,i} over the pending
                 // out-edges t, i.e. |d D(i)| wr(i) with wr(i) = inv(i) sum_pending w
-                resid += fabs(f) + fabs(d * D) * (double)prow->wr;
+                resid += fabs(f) + fabs(d * D) * (double)Pwr[pi];
                 if (pdeg == 0) leak += D;             // dangling: the fluid left the system (§3.3)
             }
             if (jt + 2 * G < a.ntw) bar_arrive_n(kBarPEmpty + x, kTileBlock);   // prep syncs it before tile k + 2
@@ -612,8 +617,14 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             long long c3 = kProf ? clock64() : 0;
 #pragma unroll
             for (int u = 0; u < kPN; ++u)
-                if (p + u * kPWt < nn)
-                    Pbuf[x * kNodeTile + p + u * kPWt] = PrepRow{Fj[u] + sm[u] + hs[u], ivi[u], Hj[u], wrj[u], dg[u]};
+                if (p + u * kPWt < nn) {
+                    const int q = x * (int)kNodeTile + p + u * kPWt;
+                    Pf[q] = Fj[u] + sm[u] + hs[u];
+                    Pivi[q] = ivi[u];
+                    PH[q] = Hj[u];
+                    Pwr[q] = wrj[u];
+                    Pdeg[q] = dg[u];
+                }
             bar_arrive_n(kBarPFull + x, kTileBlock);
             bar_sync_n(kBarPW, kPWt);                      // R[x] read by every prep warp
             if (p == 0 && has_nx) issue_records<W>(a, n0, n1, rbuf(x), R_full(x));

@@ -56,7 +56,7 @@ __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w
 // Shared memory of k_tile (one CTA per SM, everything double-buffered by tile
 // parity): gq / psum of the rounds, the prepared per-node rows P, the light
 // records R (prep warps) and the edge bundles E = {layout, staged slots} (round warps).
-struct PrepRow {
+struct PrepRow {                                 // (size only: k_tile keeps the fields as arrays)
     double f, ivi, H;        // inflow-completed fluid, 1/sum w, history
     float wr;                // pending share of the out-weight (R13)
     int32_t deg;             // out-degree
