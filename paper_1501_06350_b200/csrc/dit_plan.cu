@@ -954,7 +954,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
             tp.nrun = tot >> 32;
             tp.nseg = tot & 0xffffffffLL;
         }
-        DI_CUDA(cudaMallocAsync(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t), st));
+        DI_CUDA(cudaMallocAsync(&tp.seg_start, (tp.nseg + 1) * sizeof(int64_t) + 16, st));   // +16: TMA supersets
         DI_CUDA(cudaMallocAsync(&tp.chunk_start, (tp.nchunk + 1) * sizeof(int64_t), st));
         DI_CUDA(cudaMallocAsync(&tp.cfirst, (tp.nchunk + 1) * sizeof(int64_t), st));
         DI_CUDA(cudaMallocAsync(&tp.run_h, tp.nrun * sizeof(int32_t), st));
