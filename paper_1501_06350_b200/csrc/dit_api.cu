@@ -156,7 +156,8 @@ int di_graph_create(int64_t n, int64_t m, const int64_t *row_ptr, const int32_t 
             reserve_pool(device, n, m, g->stream);
             create_graph(g, n, m, row_ptr, col, weights, w_dtype, mem, n);
         } catch (...) {
-            free_graph(g->g);
+            free_graph(g->g, g->stream);
+            cudaStreamSynchronize(g->stream);
             if (g->own_stream) cudaStreamDestroy(g->stream);
             delete g;
             throw;
@@ -169,9 +170,9 @@ int di_graph_destroy(di_graph *g) {
     if (!g) return DI_OK;
     return guarded([&] {
         cudaSetDevice(g->device);
+        free_state(g->s, g->stream);                 // stream-ordered: the memory goes back to the pool
+        free_graph(g->g, g->stream);
         cudaStreamSynchronize(g->stream);
-        free_state(g->s);
-        free_graph(g->g);
         if (g->own_stream) cudaStreamDestroy(g->stream);
         delete g;
     });
@@ -353,7 +354,8 @@ int di_shard_create(int64_t n_global, int64_t lo, int64_t hi, int64_t m, const i
             reserve_pool(device, hi - lo, m, g->stream);
             create_shard(g, n_global, lo, hi, m, row_ptr, col, weights, w_dtype, mem);
         } catch (...) {
-            free_graph(g->g);
+            free_graph(g->g, g->stream);
+            cudaStreamSynchronize(g->stream);
             if (g->own_stream) cudaStreamDestroy(g->stream);
             delete g;
             throw;

@@ -237,7 +237,7 @@ static void create_graph_pipelined(di_graph *h, int64_t n, int64_t m, const int6
         cleanup();
     } catch (...) {
         cleanup();
-        cudaFree(flags);
+        cudaFreeAsync(flags, st);
         throw;
     }
     int fl[2] = {0, 0};
@@ -300,7 +300,7 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     DI_CUDA(cudaFreeAsync(flags, st));
     DI_CUDA(cudaStreamSynchronize(st));
     if (fl[0]) {
-        cudaFree(wtmp);
+        cudaFreeAsync(wtmp, st);
         set_error(fl[0] & 1 ? "row_ptr must be non-decreasing with row_ptr[0]=0 and row_ptr[n]=m"
                             : (fl[0] & 2 ? "col ids must be in [0, n) (n_global for a shard)" : "weights must be finite and > 0"));
         throw Fail{DI_ERR_INVALID};
@@ -316,8 +316,7 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
             DI_CUDA(cudaMallocAsync(&g.w, m * sizeof(float), st));
             k_f64_to_f32<<<grid_for(h, m), 256, 0, st>>>((const double *)wtmp, (float *)g.w, m);
             count_launch();
-            DI_CUDA(cudaStreamSynchronize(st));
-            cudaFree(wtmp);
+            DI_CUDA(cudaFreeAsync(wtmp, st));
             g.w_kind = DI_W_F32;
         }
     }
@@ -325,19 +324,15 @@ void create_graph(di_graph *h, int64_t n, int64_t m, const int64_t *row_ptr, con
     phase_mark(st, "create: check + scales");    build_scales(h);
 }
 
-static void free_transpose(DevGraph &g) {
-    free_plan(g.t);
-    free_tiles(g.tl);
+static void free_transpose(DevGraph &g, cudaStream_t st) {
+    free_plan(g.t, st);
+    free_tiles(g.tl, st);
 }
 
-void free_graph(DevGraph &g) {
-    free_transpose(g);
-    cudaFree(g.ghost_ids);
-    cudaFree(g.recv_idx);
-    cudaFree(g.row_ptr);
-    cudaFree(g.col);
-    cudaFree(g.w);
-    cudaFree(g.inv);
+void free_graph(DevGraph &g, cudaStream_t st) {
+    free_transpose(g, st);
+    for (void *p : {(void *)g.ghost_ids, (void *)g.recv_idx, (void *)g.row_ptr, (void *)g.col, g.w, (void *)g.inv})
+        if (p) cudaFreeAsync(p, st);
     g = DevGraph();
 }
 
@@ -576,8 +571,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
                 k_f32_to_f64<<<grid_for(h, g.m), 256, 0, st>>>((const float *)g.w, w64, g.m);
                 count_launch();
             }
-            DI_CUDA(cudaStreamSynchronize(st));
-            cudaFree(g.w);
+            DI_CUDA(cudaFreeAsync(g.w, st));
             g.w = w64;
             g.w_kind = DI_W_F64;
         }
@@ -585,7 +579,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // (rebuilt by the next call that needs them), then allocate every buffer of
         // the new CSR before the state is touched, so that a failure (OOM) leaves
         // graph and fluid as they were
-        free_transpose(g);
+        free_transpose(g, st);
         int64_t *deg = nullptr, *nrp = nullptr, *cursor = nullptr;
         DI_CUDA(cudaMallocAsync(&deg, (n > 0 ? n : 1) * sizeof(int64_t), st));
         track(deg);
@@ -633,9 +627,9 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // swap in the new CSR (no longer temporaries), recompute the scales of changed rows
         tmp.erase(std::remove_if(tmp.begin(), tmp.end(), [&](void *p) { return p == nrp || p == ncol || p == nwt; }),
                   tmp.end());
-        cudaFree(g.row_ptr);
-        cudaFree(g.col);
-        cudaFree(g.w);
+        cudaFreeAsync(g.row_ptr, st);
+        cudaFreeAsync(g.col, st);
+        if (g.w) cudaFreeAsync(g.w, st);
         g.row_ptr = nrp;
         g.col = ncol;
         g.w = nwt;
@@ -650,7 +644,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             State &s = h->s;
             const int64_t need = n + g.m / kSplit + 1;
             if (need > s.ent_cap) {
-                cudaFree(s.ent);
+                cudaFreeAsync(s.ent, st);
                 s.ent = nullptr;
                 DI_CUDA(cudaMallocAsync(&s.ent, need * sizeof(uint4), st));
                 s.ent_cap = need;

@@ -237,9 +237,9 @@ void count_launch(int k = 1);
 // ---- builders / solver (dit_graph.cu, dit_solve.cu) ----
 void build_scales(di_graph *h);
 void build_transpose(di_graph *h);
-void free_graph(DevGraph &g);
+void free_graph(DevGraph &g, cudaStream_t st);   // stream-ordered frees (back to the pool, no device sync)
 void ensure_state(di_graph *h);
-void free_state(State &s);
+void free_state(State &s, cudaStream_t st);
 void run_sweeps(di_graph *h, double tol, const di_solve_opts &o, di_result *res);
 void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats_out);
 void launch_sweep(di_graph *h);
@@ -250,11 +250,11 @@ void launch_push(di_graph *h);
 void launch_pull(di_graph *h);
 void launch_pull_plan(di_graph *h, const PullPlan &p, const double *A, int want);
 void build_plan_pieces(di_graph *h, PullPlan &p);
-void free_plan(PullPlan &p);
+void free_plan(PullPlan &p, cudaStream_t st);
 // feed: chunks arriving during create (then `bad` = the create's validation flags:
 // nonzero after the chunks stops the build before its remote part)
 void build_tiles(di_graph *h, const PlanFeed *feed = nullptr, const int *bad = nullptr);
-void free_tiles(TilePlan &t);
+void free_tiles(TilePlan &t, cudaStream_t st);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
 void *cub_scratch(int device, size_t bytes);   // dit_pull.cu: CUB scratch cached per device

@@ -333,12 +333,12 @@ __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntil
         atomicMax(mx, (unsigned long long)(ltile[t + 1] - ltile[t]));
 }
 
-void free_tiles(TilePlan &t) {
+void free_tiles(TilePlan &t, cudaStream_t st) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
                     (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
                     (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run})
-        cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
     t = TilePlan();
 }
 
@@ -851,7 +851,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
             for (void *p : {(void *)rk0, (void *)rk1, (void *)rv0, (void *)rv1, (void *)rw64, (void *)lc, (void *)rsc,
                             (void *)rsp, (void *)pcnt, (void *)tmp, (void *)vcap})
                 cudaFreeAsync(p, st);
-            free_tiles(tp);
+            free_tiles(tp, st);
             return;                                  // the caller reports the error
         }
     }

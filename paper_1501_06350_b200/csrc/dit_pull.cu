@@ -271,14 +271,10 @@ void build_plan_pieces(di_graph *h, PullPlan &pd) {
     pd.pieces_built = true;
 }
 
-void free_plan(PullPlan &p) {
-    cudaFree(p.ptr);
-    cudaFree(p.src);
-    cudaFree(p.w);
-    cudaFree(p.pieces);
-    cudaFree(p.fix);
-    cudaFree(p.pbuf);
-    cudaFree(p.tile_start);
+void free_plan(PullPlan &p, cudaStream_t st) {
+    for (void *q : {(void *)p.ptr, (void *)p.src, p.w, (void *)p.pieces, (void *)p.fix, (void *)p.pbuf,
+                    (void *)p.tile_start})
+        if (q) cudaFreeAsync(q, st);
     p = PullPlan();
 }
 

@@ -79,7 +79,7 @@ void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t
         k_remap<<<grid_for(h, m), 256, 0, st>>>(g.col, m, lo, hi, bm, wpre, n_local);
         count_launch();
     }
-    DI_CUDA(cudaMalloc(&g.ghost_ids, (n_ghost > 0 ? n_ghost : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMallocAsync(&g.ghost_ids, (n_ghost > 0 ? n_ghost : 1) * sizeof(int32_t), st));
     if (nw > 0) {
         k_ghost_ids<<<grid_for(h, nw), 256, 0, st>>>(bm, wpre, nw, g.ghost_ids);
         count_launch();
@@ -98,9 +98,9 @@ void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t
 void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int nseg, const int64_t *seg_counts,
                     int mem) {
     DevGraph &g = h->g;
-    cudaFree(g.recv_idx);
+    if (g.recv_idx) cudaFreeAsync(g.recv_idx, h->stream);
     g.recv_idx = nullptr;
-    DI_CUDA(cudaMalloc(&g.recv_idx, (total > 0 ? total : 1) * sizeof(int32_t)));
+    DI_CUDA(cudaMallocAsync(&g.recv_idx, (total > 0 ? total : 1) * sizeof(int32_t), h->stream));
     if (total > 0)
         DI_CUDA(cudaMemcpyAsync(g.recv_idx, local_idx, total * sizeof(int32_t),
                                 mem == DI_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));

@@ -295,6 +295,28 @@ __global__ void __launch_bounds__(kThreads) k_dangling_hist(const int64_t *__res
 void launch_pull(di_graph *h);
 
 // ---------------------------------------------------------------- host side
+// pinned host mirrors of the control block, recycled across handles (cudaMallocHost /
+// cudaFreeHost per graph cost milliseconds and synchronise the device)
+static std::mutex g_ctrl_mu;
+static std::vector<Ctrl *> g_ctrl_free;
+static Ctrl *pinned_ctrl_get() {
+    {
+        std::lock_guard<std::mutex> lock(g_ctrl_mu);
+        if (!g_ctrl_free.empty()) {
+            Ctrl *c = g_ctrl_free.back();
+            g_ctrl_free.pop_back();
+            return c;
+        }
+    }
+    Ctrl *c = nullptr;
+    DI_CUDA(cudaMallocHost(&c, sizeof(Ctrl)));
+    return c;
+}
+static void pinned_ctrl_put(Ctrl *c) {
+    std::lock_guard<std::mutex> lock(g_ctrl_mu);
+    g_ctrl_free.push_back(c);
+}
+
 void ensure_state(di_graph *h) {
     State &s = h->s;
     const int64_t n = h->g.n;
@@ -304,8 +326,8 @@ void ensure_state(di_graph *h) {
     DI_CUDA(cudaMallocAsync(&s.H, nn * sizeof(double) + 16, h->stream));
     s.ent_cap = n + h->g.m / kSplit + 1;
     DI_CUDA(cudaMallocAsync(&s.ent, s.ent_cap * sizeof(uint4), h->stream));
-    DI_CUDA(cudaMalloc(&s.ctrl, sizeof(Ctrl)));
-    DI_CUDA(cudaMallocHost(&s.ctrl_host, sizeof(Ctrl)));
+    DI_CUDA(cudaMallocAsync(&s.ctrl, sizeof(Ctrl), h->stream));
+    s.ctrl_host = pinned_ctrl_get();
     std::memset(s.ctrl_host, 0, sizeof(Ctrl));
     // fixed grid for every grid-stride kernel: 8 resident 256-thread blocks per SM
     const int64_t want = (n + kThreads - 1) / kThreads;
@@ -315,17 +337,12 @@ void ensure_state(di_graph *h) {
     DI_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(Ctrl), h->stream));
 }
 
-void free_state(State &s) {
+void free_state(State &s, cudaStream_t st) {
     for (cudaEvent_t e : s.events) cudaEventDestroy(e);
-    cudaFree(s.hist);
-    cudaFree(s.F);
-    cudaFree(s.H);
-    cudaFree(s.A);
-    cudaFree(s.A2);
-    cudaFree(s.ent);
-    cudaFree(s.ctrl);
-    cudaFree(s.part);
-    if (s.ctrl_host) cudaFreeHost(s.ctrl_host);
+    for (void *p : {(void *)s.hist, (void *)s.F, (void *)s.H, (void *)s.A, (void *)s.A2, (void *)s.ent, (void *)s.ctrl,
+                    (void *)s.part})
+        if (p) cudaFreeAsync(p, st);
+    if (s.ctrl_host) pinned_ctrl_put(s.ctrl_host);
     s = State();
 }
 

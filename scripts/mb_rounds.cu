@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_rounds(const uint16_t *__res
             constexpr int kPer = kVW / kWarps;
 #pragma unroll
             for (int h = 0; h < kPer; ++h) {
-                const int vw = kPer == 1 ? wp : (h ? kVW - 1 - wp : wp);
+                const int vw = kPer == 1 ? wp : (kPer == 2 ? (h ? kVW - 1 - wp : wp) : wp + h * kWarps);
                 const int o0 = vw * 32 * K;
                 double acc = 0.0;
                 for (int s = 0; s < K; s += 4) {
@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_rounds(const uint16_t *__res
             }
             __syncthreads();
             if (i < kNode) f = psum[i] + psum[(i * 7 + 3) & 1023];
+            if (kWarps * 32 < kNode) {                // fewer threads than nodes: the second node of each thread
+                const int i2 = i + kWarps * 32;
+                if (i2 < kNode) gq[i2] = 0.85 * f * 0.1;
+            }
         }
         acc_out += f;
     }
@@ -152,8 +156,8 @@ int main() {
     cudaMalloc(&dr, S * 2);
     cudaMalloc(&dc, S * 2);
     cudaMalloc(&dw, S * 4);
-    cudaMalloc(&dout, (size_t)nsm * 2 * 1024 * 8);
-    cudaMalloc(&dcyc, nsm * 2 * 8);
+    cudaMalloc(&dout, (size_t)nsm * 3 * 1024 * 8);
+    cudaMalloc(&dcyc, nsm * 3 * 8);
     cudaMemcpy(dr, src_r.data(), S * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dc, src_c.data(), S * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dw, w.data(), S * 4, cudaMemcpyHostToDevice);
@@ -163,10 +167,12 @@ int main() {
     cudaMemcpy(db, src_b.data(), S * 2, cudaMemcpyHostToDevice);
     for (int K : {8}) {
         run<16, false>("1 CTA x 16 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
+        run<8, false>("2 CTAs x 8 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
+        run<8, false>("1 CTA x 8 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
         run<16, false>("2 CTAs x 16 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
+        run<8, false>("3 CTAs x 8 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 3);
         run<16, false>("1 CTA x 16 warps, half-warp distinct", dc, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
-        run<16, false>("2 CTAs x 16 warps, half-warp distinct", dc, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
-        run<32, false>("1 CTA x 32 warps, random", dr, dw, K, tiles, rounds, dout, dcyc, nsm, 1);
+        run<8, false>("2 CTAs x 8 warps, half-warp distinct", dc, dw, K, tiles, rounds, dout, dcyc, nsm, 2);
     }
     return 0;
 }
