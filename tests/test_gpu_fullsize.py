@@ -1,7 +1,8 @@
 """Full-size parity of the bench's workload (BASELINE configs[2]) and of the
 dynamic update (configs[4]) against the CPU oracle, plus the tiled plan's
-rarely taken build paths (several heavy source stripes, the 64-bit local-rank
-scan, our own LSD radix transpose) element by element.
+rarely taken build paths (several heavy source stripes, our own LSD radix
+sort, the bank-aware slot order, the plan built during a pinned-host create)
+element by element.
 
 north_star: ||H_gpu - H_oracle||_1 <= 1e-9 with both solved to |F|_1 <= 1e-12
 (float64 fluid), top-1000 ranking identical (R9, R11).  The oracle
@@ -165,12 +166,12 @@ def test_tiled_several_heavy_stripes_elementwise(eng):
         _tiled_elementwise(eng, g, 4, (1, 2, 5), check)
 
 
-def test_tiled_64bit_scan_and_own_radix_elementwise(eng):
-    # the plan paths a 1e9-edge single graph never takes: the 64-bit local-rank scan
-    # (m >= 2^31 edges) and our own LSD radix transpose (DIT_OWN_RADIX)
+def test_tiled_own_radix_elementwise(eng):
+    # the plan builder's sorts through our own LSD radix sort (the path of 2^31+
+    # items, DIT_OWN_RADIX) instead of the toolkit's onesweep sort: same plan bits
     spec = synth.CONFIGS[1].scaled(150_001, seed=22, weighted=True)
     g = synth.generate(spec)
-    with _env(DIT_FORCE_L64=1, DIT_OWN_RADIX=1):
+    with _env(DIT_OWN_RADIX=1):
         _tiled_elementwise(eng, g, 3, (1, 3))
 
 
