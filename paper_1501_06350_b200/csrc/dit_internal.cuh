@@ -166,7 +166,8 @@ struct PlanFeed {
     std::vector<cudaEvent_t> col_ready, w_ready;
     std::function<void(int)> on_col, on_w;
 };
-constexpr int64_t kPlanChunkEdges = (int64_t)1 << 26;   // plan chunk size without a feed
+constexpr int64_t kPlanChunkEdges = (int64_t)1 << 26;   // plan chunk of the pipelined create (~9 ms of upload)
+constexpr int64_t kPlanChunkEdgesLazy = (int64_t)1 << 28; // plan chunk of a build from resident data (fewer syncs)
 
 // Per-node weight-scale storage and raw weights.
 struct DevGraph {

@@ -709,7 +709,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
         set_error("tiled plan: graph too large for one handle (fluid slots >= 2^32)");
         throw Fail{DI_ERR_INVALID};
     }
-    // chunks of whole tiles (the feed's, else about kPlanChunkEdges edges each)
+    // chunks of whole tiles (the feed's, else about kPlanChunkEdgesLazy edges each)
     std::vector<int64_t> ctile, cedge;               // chunks: tile ranges and their first edges
     if (feed) {
         ctile = feed->tile_lo;
@@ -726,7 +726,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
         DI_CUDA(cudaFreeAsync(d, st));
         ctile.push_back(0);
         for (int64_t t = 1; t <= tp.ntile; ++t)
-            if (t == tp.ntile || rp[t] - rp[ctile.back()] >= kPlanChunkEdges) ctile.push_back(t);
+            if (t == tp.ntile || rp[t] - rp[ctile.back()] >= kPlanChunkEdgesLazy) ctile.push_back(t);
         for (int64_t t : ctile) cedge.push_back(rp[t]);
     }
     const int nch = (int)ctile.size() - 1;
