@@ -96,14 +96,22 @@ class CudaShard:
 
 
 class TorchCollectives:
-    """torch.distributed collectives for a single local shard (NCCL or gloo)."""
+    """torch.distributed collectives for a single local shard (NCCL or gloo).
 
-    def __init__(self, group=None):
+    stage_host=True moves every buffer through host memory around the
+    collective (gloo with CUDA shards: the tests run real libdit shards of
+    several processes on one GPU that way; no kernel waits on another rank)."""
+
+    def __init__(self, group=None, stage_host=False):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.stage = stage_host
+
+    def _c(self, t):
+        return t.cpu() if self.stage else t
 
     def plan(self, shards, bounds):
         (s,) = shards
@@ -111,13 +119,15 @@ class TorchCollectives:
         owner = np.searchsorted(np.asarray(bounds), ids, side="right") - 1
         send_counts = np.bincount(owner, minlength=self.world).astype(np.int64)
         dev = s.send.device
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        cdev = torch.device("cpu") if self.stage else dev
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=cdev)
         rc = torch.empty_like(sc)
         self.dist.all_to_all_single(rc, sc, group=self.group)
         recv_counts = rc.cpu().numpy()
-        recv_ids = torch.empty(int(recv_counts.sum()), dtype=torch.int32, device=dev)
-        self.dist.all_to_all_single(recv_ids, s.ghost_ids.to(dev), output_split_sizes=recv_counts.tolist(),
+        recv_ids = torch.empty(int(recv_counts.sum()), dtype=torch.int32, device=cdev)
+        self.dist.all_to_all_single(recv_ids, s.ghost_ids.to(cdev), output_split_sizes=recv_counts.tolist(),
                                     input_split_sizes=send_counts.tolist(), group=self.group)
+        recv_ids = recv_ids.to(dev)
         s.send_counts = send_counts.tolist()
         s.set_recv((recv_ids - s.lo).to(torch.int32), recv_counts.tolist())
 
@@ -125,23 +135,34 @@ class TorchCollectives:
         # one collective per sweep: every rank's {|F|_1, max|F|, leak, edges}, reduced on
         # the device in rank order by di_shard_control (deterministic, identical on all ranks)
         (s,) = shards
-        self.dist.all_gather_into_tensor(s.gathered, s.stats, group=self.group)
+        if self.stage:
+            out = torch.empty(s.gathered.shape, dtype=s.gathered.dtype)
+            self.dist.all_gather_into_tensor(out, s.stats.cpu(), group=self.group)
+            s.gathered.copy_(out)
+        else:
+            self.dist.all_gather_into_tensor(s.gathered, s.stats, group=self.group)
 
     def alltoall(self, shards):
         (s,) = shards
         if self.world == 1:
+            return
+        if self.stage:
+            out = torch.empty(sum(s.recv_counts), dtype=s.recv.dtype)
+            self.dist.all_to_all_single(out, s.send[:sum(s.send_counts)].cpu(), output_split_sizes=s.recv_counts,
+                                        input_split_sizes=s.send_counts, group=self.group)
+            s.recv[:sum(s.recv_counts)].copy_(out)
             return
         self.dist.all_to_all_single(s.recv[:sum(s.recv_counts)], s.send[:sum(s.send_counts)],
                                     output_split_sizes=s.recv_counts, input_split_sizes=s.send_counts,
                                     group=self.group)
 
     def allreduce_sum(self, values, device):
-        t = torch.tensor(values, dtype=torch.float64, device=device)
+        t = torch.tensor(values, dtype=torch.float64, device="cpu" if self.stage else device)
         self.dist.all_reduce(t, group=self.group)
         return t.cpu().tolist()
 
     def allreduce_max(self, values, device):
-        t = torch.tensor(values, dtype=torch.float64, device=device)
+        t = torch.tensor(values, dtype=torch.float64, device="cpu" if self.stage else device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t.cpu().tolist()
 
