@@ -229,7 +229,7 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     // grouped slots: four sources (and weights) per vector load
     const int lane = base & 31, o0 = base - lane;
     const int Kg = K - K % kSlotGroup;
-#pragma unroll 2
+#pragma unroll kLsUnroll
     for (; s < Kg; s += kSlotGroup) {
         const int k = o0 + 32 * s + kSlotGroup * lane;
         const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
@@ -331,11 +331,12 @@ __device__ __forceinline__ void issue_records(const TileArgs<W> &a, int64_t r0, 
         tma_load(smem_u32(buf), reinterpret_cast<const unsigned char *>(a.rrec) + rb0, (uint32_t)(rb1 - rb0), bar);
 }
 
-// Persistent kernel, one 1024-thread CTA per SM, warp-specialised:
+// Persistent kernel, one kTileBlock-thread CTA per SM, warp-specialised:
 //   round warps 0-15 -- thread i owns node i of the current tile: the `rounds`
 //     Jacobi rounds over the tile's local in-edges (Eq. (8) pushes, sliced-ELL
 //     slots from shared memory), then F, H += D, A = d D inv out;
-//   prep warps 16-31 -- meanwhile the NEXT tile's inflow: the remote pushes still
+//   prep warps 16.. (kPWt threads, kPN nodes each) -- meanwhile the NEXT tile's
+//     inflow: the remote pushes still
 //     pending (heavy sums, light records' gathered outflow) added to F, into P.
 // TMA bulk copies bring each tile's edge bundle (round warps) and light records
 // (prep warps) into the buffer of its parity; mbarriers hand P between the groups.

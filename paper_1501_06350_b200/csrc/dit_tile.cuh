@@ -10,10 +10,18 @@
 namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // build kernels: thread i owns node i of the tile
-// k_tile: one 1024-thread CTA per SM, 16 round warps (thread i owns node i) and
-// 16 prep warps (the next tile's inflow)
+// k_tile: one CTA per SM, 16 round warps (thread i owns node i) and 4 prep warps
+// (the next tile's inflow, DIT_PREP_NODES = 4 nodes per thread: 640 threads;
+// 2 nodes per thread was 2% slower, 8 and 16 starve the round warps)
 constexpr int kRW = (int)kNodeTile;
-constexpr int kPWt = (int)kNodeTile / 2;           // two nodes per prep thread
+#ifndef DIT_LS_UNROLL
+#define DIT_LS_UNROLL 2
+#endif
+constexpr int kLsUnroll = DIT_LS_UNROLL;          // k_tile: slot groups per unrolled local-sum step
+#ifndef DIT_PREP_NODES
+#define DIT_PREP_NODES 4
+#endif
+constexpr int kPWt = (int)kNodeTile / DIT_PREP_NODES;   // nodes per prep thread
 constexpr int kPN = (int)kNodeTile / kPWt;
 constexpr int kTileBlock = kRW + kPWt;
 constexpr int kTileWarps = kTileThreads / 32;
