@@ -328,6 +328,129 @@ __global__ void __launch_bounds__(kBalWarps * 32) k_ell_balance(const int64_t *_
     }
 }
 
+// Copies in shared memory: k_tile writes kGqCopies copies of the
+// outflow gq and kPsumCopies of the piece sums psum, copy c shifted by c bank
+// pairs.  A 64-bit shared load is served per half-warp, one wavefront per
+// address sharing a bank pair (equal addresses broadcast), so per load and
+// half-warp the plan matches the distinct addresses to distinct bank pairs
+// (augmenting paths; address v can use the pairs v, v+1, .., v+C-1 mod 16) and
+// encodes the copy in the index (c * stride + v).  Only the shared-memory
+// address of each read changes: values and summation order do not.
+//
+// match_copies: v[l] >= 0 an address, -1 no access, -2 a zero padding slot (the
+// padding of a load shares one zero slot, in a pair left free: *pad_bank).
+// Returns the copy of each lane in cp[l].
+__device__ __forceinline__ void match_copies(const int *v, int C, int *cp, int *pad_bank) {
+    int ju[16], uq[16], matchR[16], cu[16];
+    int nu = 0;
+    bool pad = false;
+    for (int l = 0; l < 16; ++l) {
+        matchR[l] = -1;
+        uq[l] = -1;
+        if (v[l] == -2) pad = true;
+        if (v[l] < 0) continue;
+        int u = 0;
+        while (u < nu && ju[u] != v[l]) ++u;
+        if (u == nu) ju[nu++] = v[l];
+        uq[l] = u;
+    }
+    for (int u = 0; u < nu; ++u) {
+        cu[u] = -1;
+        int su[17], sc[17], sb[17];
+        int top = 0;
+        unsigned vis = 0;
+        su[0] = u;
+        sc[0] = 0;
+        while (top >= 0) {
+            if (sc[top] == C) {
+                --top;
+                continue;
+            }
+            const int b = (ju[su[top]] + sc[top]++) & 15;
+            if ((vis >> b) & 1u) continue;
+            vis |= 1u << b;
+            sb[top] = b;
+            if (matchR[b] < 0) {                      // augment: level k takes pair sb[k]
+                for (int k = top; k >= 0; --k) {
+                    matchR[sb[k]] = su[k];
+                    cu[su[k]] = (sb[k] - ju[su[k]]) & 15;
+                }
+                break;
+            }
+            su[top + 1] = matchR[b];
+            sc[top + 1] = 0;
+            ++top;
+        }
+    }
+    int load[16];
+    for (int b = 0; b < 16; ++b) load[b] = matchR[b] >= 0;
+    for (int u = 0; u < nu; ++u)                      // no free pair in reach: the least loaded one
+        if (cu[u] < 0) {
+            int bc = 0;
+            for (int c = 1; c < C; ++c)
+                if (load[(ju[u] + c) & 15] < load[(ju[u] + bc) & 15]) bc = c;
+            cu[u] = bc;
+            load[(ju[u] + bc) & 15] += 1;
+        }
+    int bp = 0;
+    if (pad)
+        for (int b = 1; b < 16; ++b)
+            if (load[b] < load[bp]) bp = b;
+    *pad_bank = bp;
+    for (int l = 0; l < 16; ++l) cp[l] = uq[l] >= 0 ? cu[uq[l]] : 0;
+}
+
+// gq copies of the local slots: one thread per (tile, virtual warp, half-warp), per slot row
+__global__ void __launch_bounds__(128) k_ell_copies(const int64_t *__restrict__ ltile, const uint32_t *__restrict__ vofs,
+                                                    int64_t t0, int64_t t1, uint16_t *__restrict__ lsrc) {
+    const int64_t nitem = (t1 - t0) * kVWarps * 2;
+    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nitem;
+         item += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tile = t0 + item / (kVWarps * 2);
+        const int vw = (int)((item / 2) % kVWarps), half = (int)(item & 1);
+        const uint32_t o0 = vofs[tile * kVofsStride + vw];
+        const int K = (int)((vofs[tile * kVofsStride + vw + 1] - o0) >> 5);
+        const int64_t base = ltile[tile] + o0;
+        for (int s = 0; s < K; ++s) {
+            int v[16], cp[16], bp;
+            for (int l = 0; l < 16; ++l) {
+                const int x = lsrc[base + ell_slot(s, 16 * half + l, K)];
+                v[l] = x >= (int)kNodeTile ? -2 : x;
+            }
+            match_copies(v, kGqCopies, cp, &bp);
+            for (int l = 0; l < 16; ++l)
+                lsrc[base + ell_slot(s, 16 * half + l, K)] =
+                    (uint16_t)(v[l] >= 0 ? cp[l] * kGqStride + v[l] : (int)kNodeTile + bp);
+        }
+    }
+}
+
+// psum copies of the piece ranks: one thread per (tile, round warp, half-warp), per
+// piece index k of the half-warp's 16 nodes (the k-th psum load of the node sums)
+__global__ void __launch_bounds__(128) k_plist_copies(const uint16_t *__restrict__ vfirst, int64_t t0, int64_t t1,
+                                                      uint16_t *__restrict__ plist) {
+    const int64_t nitem = (t1 - t0) * kTileWarps * 2;
+    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nitem;
+         item += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tile = t0 + item / (kTileWarps * 2);
+        const int i0 = (int)(item % (kTileWarps * 2)) * 16;   // the half-warp's first node
+        int pf[16], np[16], mx = 0;
+        for (int l = 0; l < 16; ++l) {
+            pf[l] = vfirst[tile * kVfStride + i0 + l];
+            np[l] = (int)vfirst[tile * kVfStride + i0 + l + 1] - pf[l];
+            mx = max(mx, np[l]);
+        }
+        uint16_t *pl = plist + tile * kVRows;
+        for (int k = 0; k < mx; ++k) {
+            int v[16], cp[16], bp;
+            for (int l = 0; l < 16; ++l) v[l] = k < np[l] ? (int)pl[pf[l] + k] : -1;
+            match_copies(v, kPsumCopies, cp, &bp);
+            for (int l = 0; l < 16; ++l)
+                if (v[l] >= 0) pl[pf[l] + k] = (uint16_t)(cp[l] * kPsumStride + v[l]);
+        }
+    }
+}
+
 __global__ void k_tile_max_edges(const int64_t *__restrict__ ltile, int64_t ntile, unsigned long long *__restrict__ mx) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntile; t += (int64_t)gridDim.x * blockDim.x)
         atomicMax(mx, (unsigned long long)(ltile[t + 1] - ltile[t]));
@@ -810,6 +933,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
     DI_CUDA(cudaMallocAsync(&sv1, cmax * 8, st));
     phase_mark(st, "tiles: allocate");
     // ---- phase 2: local edges into the ELL, remote edges into the remote list
+    const bool bank_order = getenv("DIT_BANK_ORDER") != nullptr;
     for (int c = 0; c < nch; ++c) {
         const int64_t i0 = node_of(ctile[c]), i1 = node_of(ctile[c + 1]);
         if (feed) {
@@ -834,12 +958,24 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
                                                                  tp.vofs, tp.vfirst, tp.plist, vcap, (const SW *)g.w,
                                                                  e0, tp.lsrc, (SW *)tp.lw);
         count_launch();
+        if (ctile[c + 1] > ctile[c]) {               // k_plan_ell has placed the chunk's pieces: ranks are final
+            k_plist_copies<<<(int)grid_cap(h, (ctile[c + 1] - ctile[c]) * kTileWarps * 2, 128), 128, 0, st>>>(
+                tp.vfirst, ctile[c], ctile[c + 1], tp.plist);
+            count_launch();
+        }
+        if (!bank_order && ctile[c + 1] > ctile[c]) {
+            k_ell_copies<<<(int)grid_cap(h, (ctile[c + 1] - ctile[c]) * kVWarps * 2, 128), 128, 0, st>>>(
+                tp.ltile, tp.vofs, ctile[c], ctile[c + 1], tp.lsrc);
+            count_launch();
+        }
     }
     phase_mark(st, "tiles: local edges");
-    if (tp.mpad > 0 && getenv("DIT_BANK_ORDER")) {   // opt-in: ~1% faster rounds for ~55 ms of build (configs[2])
+    if (tp.mpad > 0 && bank_order) {                 // opt-in: ~1% faster rounds for ~55 ms of build (configs[2])
         k_ell_balance<W><<<(int)std::min<int64_t>(tp.ntile * kVWarps / kBalWarps + 1, (int64_t)h->num_sms * 16),
                            kBalWarps * 32, 0, st>>>(tp.ltile, tp.vofs, tp.ntile, tp.lsrc, (SW *)tp.lw);
-        count_launch();
+        k_ell_copies<<<(int)grid_cap(h, tp.ntile * kVWarps * 2, 128), 128, 0, st>>>(tp.ltile, tp.vofs, 0, tp.ntile,
+                                                                               tp.lsrc);
+        count_launch(2);
     }
     for (void *p : {(void *)sk0, (void *)sk1, (void *)sv0, (void *)sv1, (void *)lsc, (void *)lsp, (void *)lst})
         DI_CUDA(cudaFreeAsync(p, st));

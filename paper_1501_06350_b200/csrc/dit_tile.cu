@@ -301,8 +301,10 @@ __device__ __forceinline__ void issue_edges(const TileArgs<W> &a, int64_t tile, 
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     const int64_t cnt = ts.l1 - ts.l0 - ts.st;       // staged slots: multiples of 32 (16-byte aligned)
     const uint32_t bytes = (uint32_t)(kMetaBytes + cnt * (2 + kWB));
+#ifndef DIT_NO_EDGE_FENCE
     // order this CTA's earlier generic-proxy reads of the buffer before the async writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     mbar_arrive_tx(bar, bytes);
     const uint32_t sb = smem_u32(buf);
     tma_load(sb, a.vofs + tile * kVofsStride, kVofsStride * 4, bar);
@@ -346,8 +348,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
     constexpr bool kW = !std::is_same<W, NoW>::value;
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     constexpr int kRS = (int)sizeof(RemRec<W>);
-    double *gq = reinterpret_cast<double *>(smem);                       // [kGqSlots]: outflow, zero pad slots
-    double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kVRows]: piece sums by rank
+    double *gq = reinterpret_cast<double *>(smem);                       // [kGqCopies][kGqStride]: outflow, zero pad slots
+    double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kPsumCopies][kPsumStride]: piece sums by rank
     // prepared rows, structure of arrays [2][kNodeTile] each (consecutive threads, consecutive banks)
     double *Pf = reinterpret_cast<double *>(smem + kOffP);
     double *Pivi = Pf + 2 * kNodeTile;
@@ -384,7 +386,9 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < (int)(kGqSlots - kNodeTile)) gq[kNodeTile + tid] = 0.0;   // ELL padding reads these
+    constexpr int kPadSlots = (int)(kGqSlots - kNodeTile);
+    if (tid < kPadSlots * kGqCopies)                // ELL padding reads these
+        gq[(tid / kPadSlots) * kGqStride + kNodeTile + tid % kPadSlots] = 0.0;
     __syncthreads();
     double resid = 0.0, leak = 0.0;
     uint32_t nodes = 0;                              // per thread: <= tiles x rounds
@@ -403,7 +407,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     sc[x] = escal(blockIdx.x + x * G);
                     issue_edges<W>(a, tid_of(blockIdx.x + x * G), sc[x], ebuf(x), E_full(x));
                 }
-        long long ls_cyc = 0, b2_cyc = 0, ns_cyc = 0, b1_cyc = 0, rows_w = 0;           // DIT_TILE_TIMING: local sums, wait after them
+        long long ls_cyc = 0, b2_cyc = 0, ns_cyc = 0, b1_cyc = 0;   // DIT_TILE_TIMING: local sums, wait after them
+        long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pn[2] = {0, 0};
         int k = 0;
         for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
             const int x = k & 1;
@@ -457,7 +462,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     q = d * f * pivi;                // d F(i) / sum_k w_{i,k}
                 }
                 const long long t9 = kProf ? clock64() : 0;
-                gq[i] = q;
+#pragma unroll
+                for (int c = 0; c < kGqCopies; ++c) gq[c * kGqStride + i] = q;
                 bar_sync_n(kBarRW, kRW);
                 const long long ta = kProf ? clock64() : 0;
                 if (kProf) b1_cyc += ta - t9;
@@ -467,12 +473,12 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     const int vw = h2 ? kVWarps - 1 - wp : wp;
                     const uint32_t o0 = vofs_s[vw];
                     const int K = (int)((vofs_s[vw + 1] - o0) >> 5);
-                    if (kProf) rows_w += K;
                     if (K) {
                         double acc;
                         if ((int)o0 >= st) acc = local_sum<W>(es_sm, ew_sm, gq, (int)o0 + lane, K);
                         else acc = local_sum<W>(es_gl, ew_gl, gq, (int)o0 + lane, K);
-                        psum[vw * 32 + lane] = acc;
+#pragma unroll
+                        for (int c = 0; c < kPsumCopies; ++c) psum[c * kPsumStride + vw * 32 + lane] = acc;
                     }
                 }
                 const long long tb = kProf ? clock64() : 0;
@@ -500,6 +506,16 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 }
             }
             long long c3 = kProf ? clock64() : 0;
+            // E[x] is read by every round warp (the last node sums read pl_s): the
+            // bundle of the tile two ahead goes in now, before this thread's state-out
+            // stores (the proxy fence of the issue would wait for them to complete)
+            bar_sync_n(kBarRW, kRW);
+            const long long c4 = kProf ? clock64() : 0;
+            if (i == 0 && has_nx) {
+                sc[x] = nx;
+                issue_edges<W>(a, tid_of(jt + 2 * G), nx, E, E_full(x));
+            }
+            const long long c5 = kProf ? clock64() : 0;
             // state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
             if (valid) {
                 a.F[j] = f;
@@ -511,27 +527,37 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 if (pdeg == 0) leak += D;             // dangling: the fluid left the system (§3.3)
             }
             if (jt + 2 * G < a.ntw) bar_arrive_n(kBarPEmpty + x, kTileBlock);   // prep syncs it before tile k + 2
-            bar_sync_n(kBarRW, kRW);                       // E[x] read by every round warp
-            if (i == 0 && has_nx) {
-                sc[x] = nx;
-                issue_edges<W>(a, tid_of(jt + 2 * G), nx, E, E_full(x));
+            if (kProf) {                              // thread 0's counters, in registers until the end
+                const long long c6 = clock64();
+                pc[st == 0 ? 0 : 1] += c3 - c2;       // rounds of fully / partly staged tiles
+                pn[st == 0 ? 0 : 1] += 1;
+                pc[2] += c1 - c0;                     // waiting for the prepared rows
+                pc[3] += c2 - c1;                     // waiting for the edge bundle
+                pc[4] += c6 - c3;                     // state out
+                pc[5] += c4 - c3;                     // state out: barrier
+                pc[6] += c5 - c4;                     // state out: next bundle issued
+                pc[7] += c6 - c5;                     // state out: stores
             }
-            if (kProf && i == 0) {
-                dbg[st == 0 ? 10 : 12] += c3 - c2;    // rounds of fully / partly staged tiles
-                dbg[st == 0 ? 11 : 13] += 1;
-                dbg[0] += c1 - c0;                    // waiting for the prepared rows
-                dbg[1] += c2 - c1;                    // waiting for the edge bundle
-                dbg[2] += c3 - c2;                    // local rounds
-                dbg[3] += clock64() - c3;             // state out
-                dbg[7] += 1;
-            }
+        }
+        if (kProf && i == 0) {
+            dbg[10] += pc[0];
+            dbg[11] += pn[0];
+            dbg[12] += pc[1];
+            dbg[13] += pn[1];
+            dbg[0] += pc[2];
+            dbg[1] += pc[3];
+            dbg[2] += pc[0] + pc[1];
+            dbg[3] += pc[4];
+            dbg[32] += pc[5];
+            dbg[33] += pc[6];
+            dbg[34] += pc[7];
+            dbg[7] += pn[0] + pn[1];
         }
         if (kProf && lane == 0) {
             atomicAdd(&dbg[8], (unsigned long long)ls_cyc);
             atomicAdd(&dbg[9], (unsigned long long)b2_cyc);
             atomicAdd(&dbg[14], (unsigned long long)ns_cyc);
             atomicAdd(&dbg[16 + wp], (unsigned long long)ls_cyc);
-            atomicAdd(&dbg[32 + wp], (unsigned long long)rows_w);
             atomicAdd(&dbg[15], (unsigned long long)b1_cyc);
         }
     } else {

@@ -31,6 +31,23 @@ constexpr int kVofsStride = 36;                  // u32 per tile (kVWarps + 1, p
 constexpr int kVfStride = 520;                   // u16 per tile (kNodeTile + 1, padded to 16 B)
 constexpr int kMetaBytes = kVofsStride * 4 + kVfStride * 2 + kVRows * 2;   // per-tile layout, TMA-staged
 constexpr int64_t kGqSlots = kNodeTile + 16;     // outflow per node + one zero slot per bank pair (ELL padding)
+// k_tile keeps kGqCopies copies of gq, copy c at c * kGqStride: slot j of copy c sits
+// in bank pair (j + c) mod 16, and the plan picks per slot the copy that the
+// half-warp's other reads leave free (k_ell_copies; lsrc holds c * kGqStride + j)
+#ifndef DIT_GQ_COPIES
+#define DIT_GQ_COPIES 2
+#endif
+constexpr int kGqCopies = DIT_GQ_COPIES;
+constexpr int kGqStride = (int)kGqSlots + 1;
+static_assert(kGqCopies >= 1 && kGqCopies <= 16 && kGqStride % 16 == 1, "gq copies shift by one bank pair");
+// the same for the piece sums psum (the node sums' reads; plist holds c * kPsumStride + rank)
+#ifndef DIT_PSUM_COPIES
+#define DIT_PSUM_COPIES 1
+#endif
+constexpr int kPsumCopies = DIT_PSUM_COPIES;
+constexpr int kPsumStride = kVRows + 1;
+static_assert(kPsumCopies >= 1 && kPsumCopies <= 16 && kPsumStride % 16 == 1 && kPsumCopies * kPsumStride < 65536,
+              "psum copies shift by one bank pair");
 constexpr int kTileSmemBudget = 227 * 1024 - 2048;   // dynamic shared memory of k_tile (static arrays aside)
 static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per round warp");
 
@@ -70,8 +87,8 @@ struct PrepRow {                                 // (size only: k_tile keeps the
     int32_t deg;             // out-degree
 };
 static_assert(sizeof(PrepRow) == 32, "32-byte prepared rows");
-constexpr int kOffPsum = ((int)kGqSlots * 8 + 127) & ~127;
-constexpr int kOffP = kOffPsum + kVRows * 8;
+constexpr int kOffPsum = (kGqCopies * kGqStride * 8 + 127) & ~127;
+constexpr int kOffP = (kOffPsum + kPsumCopies * kPsumStride * 8 + 127) & ~127;
 constexpr int kOffR = kOffP + 2 * (int)kNodeTile * (int)sizeof(PrepRow);
 template <typename W>
 constexpr int tile_rec_buf() { return (((int)kLightCap * (int)sizeof(RemRec<W>) + 32) + 127) & ~127; }

@@ -34,6 +34,8 @@ print(f"{'RW node sums (per warp)':28s} {v[14]/it/16:10.0f} cycles/tile")
 print(f"{'RW gq write + barrier (per warp)':28s} {v[15]/it/16:10.0f} cycles/tile")
 print(f"rounds of fully staged tiles {v[10]/max(v[11],1):10.0f} cycles/tile over {v[11]:.0f} tiles")
 print(f"rounds of partly staged tiles {v[12]/max(v[13],1):9.0f} cycles/tile over {v[13]:.0f} tiles")
-print("per round warp: local-sum cycles/tile, slot rows/tile")
+for k, name in ((32, "RW state out: barrier"), (33, "RW state out: issue"), (34, "RW state out: stores")):
+    print(f"{name:28s} {v[k]/it:10.0f} cycles/tile")
+print("per round warp: local-sum cycles/tile")
 for w in range(16):
-    print(f"  warp {w:2d} {v[16+w]/it:8.0f} {v[32+w]/it:6.1f}")
+    print(f"  warp {w:2d} {v[16+w]/it:8.0f}")
