@@ -499,6 +499,11 @@ __global__ void k_stripe_count(const uint32_t *__restrict__ st, int64_t mh, unsi
 // Every position comes from a scan or a stable sort: the plan is the same bits
 // whatever the chunking.
 
+#ifndef DIT_CAP_ROUND
+#define DIT_CAP_ROUND 8
+#endif
+constexpr int64_t kCapRound = DIT_CAP_ROUND;
+
 // sliced-ELL layout of tile t from the local in-degrees (thread k = node k of the tile)
 __device__ void tile_layout(int64_t t, int k, int64_t dk, int eb, int64_t stage_cap, uint32_t *__restrict__ vofs,
                             uint16_t *__restrict__ vfirst, uint16_t *__restrict__ plist, int32_t *__restrict__ vcap,
@@ -510,7 +515,8 @@ __device__ void tile_layout(int64_t t, int k, int64_t dk, int eb, int64_t stage_
     __shared__ int s_scan[kNodeTile / 32 + 1];
     // cap: at most kVRows pieces (E / cap + nonzero rows <= kVRows); block sums
     const int64_t E = block_sum_512(dk, s_red), nz = block_sum_512((int64_t)(dk > 0), s_red);
-    const int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
+    int64_t cap = nz ? std::max<int64_t>(1, (E + (kVRows - nz) - 1) / (kVRows - nz)) : 1;
+    cap = (cap + kCapRound - 1) / kCapRound * kCapRound;   // full pieces: whole slot groups
     // node k's pieces: its slots in node order (exclusive scan of the piece counts)
     const int np = (int)((dk + cap - 1) / cap);
     const int first = block_exscan_512(np, s_scan);

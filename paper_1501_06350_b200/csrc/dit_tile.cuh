@@ -18,8 +18,12 @@ constexpr int kRW = (int)kNodeTile;
 #define DIT_LS_UNROLL 2
 #endif
 constexpr int kLsUnroll = DIT_LS_UNROLL;          // k_tile: slot groups per unrolled local-sum step
+#ifndef DIT_REC_UNROLL
+#define DIT_REC_UNROLL 8
+#endif
+constexpr int kRecUnroll = DIT_REC_UNROLL;        // k_tile prep: light-record gathers in flight per thread
 #ifndef DIT_PREP_NODES
-#define DIT_PREP_NODES 4
+#define DIT_PREP_NODES 2
 #endif
 constexpr int kPWt = (int)kNodeTile / DIT_PREP_NODES;   // nodes per prep thread
 constexpr int kPN = (int)kNodeTile / kPWt;
