@@ -329,80 +329,151 @@ __global__ void __launch_bounds__(kBalWarps * 32) k_ell_balance(const int64_t *_
 }
 
 // Copies in shared memory: k_tile writes kGqCopies copies of the
-// outflow gq and kPsumCopies of the piece sums psum, copy c shifted by c bank
-// pairs.  A 64-bit shared load is served per half-warp, one wavefront per
+// outflow gq, copy c shifted by c bank pairs.  A 64-bit shared load is served per half-warp, one wavefront per
 // address sharing a bank pair (equal addresses broadcast), so per load and
-// half-warp the plan matches the distinct addresses to distinct bank pairs
-// (augmenting paths; address v can use the pairs v, v+1, .., v+C-1 mod 16) and
+// half-warp the plan gives the distinct addresses distinct bank pairs where it
+// can (address v can use the pairs v, v+1, .., v+C-1 mod 16) and
 // encodes the copy in the index (c * stride + v).  Only the shared-memory
 // address of each read changes: values and summation order do not.
 //
-// match_copies: v[l] >= 0 an address, -1 no access, -2 a zero padding slot (the
-// padding of a load shares one zero slot, in a pair left free: *pad_bank).
-// Returns the copy of each lane in cp[l].
-__device__ __forceinline__ void match_copies(const int *v, int C, int *cp, int *pad_bank) {
-    int ju[16], uq[16], matchR[16], cu[16];
-    int nu = 0;
-    bool pad = false;
+// match_copies (one thread per half-warp row): v[16] >= 0 an address, -2 a
+// padding slot.  A maximum matching of the distinct addresses to bank pairs by
+// augmenting paths (Kuhn), the state packed four bits per entry in registers
+// (bank of each lane, the holder of each pair, the DFS stack); a lane left
+// unmatched keeps copy 0.  Returns the copies packed four bits per lane and the
+// zero slot's pair for the padding.
+__device__ __forceinline__ uint64_t get4(uint64_t w, int k) { return (w >> (4 * k)) & 15u; }
+__device__ __forceinline__ uint64_t set4(uint64_t w, int k, uint64_t x) {
+    return (w & ~(15ull << (4 * k))) | (x << (4 * k));
+}
+__device__ __forceinline__ uint64_t match_copies(const int (&v)[16], int C, int &pad_bank) {
+    uint64_t B = 0;                                   // bank pair of each lane's address
+    unsigned lead = 0;                                // lanes with an address (equal ones matched apart:
+#pragma unroll                                        // a pair each, rare, no conflict either way)
     for (int l = 0; l < 16; ++l) {
-        matchR[l] = -1;
-        uq[l] = -1;
-        if (v[l] == -2) pad = true;
-        if (v[l] < 0) continue;
-        int u = 0;
-        while (u < nu && ju[u] != v[l]) ++u;
-        if (u == nu) ju[nu++] = v[l];
-        uq[l] = u;
+        B |= (uint64_t)(v[l] & 15) << (4 * l);
+        if (v[l] >= 0) lead |= 1u << l;
     }
-    for (int u = 0; u < nu; ++u) {
-        cu[u] = -1;
-        int su[17], sc[17], sb[17];
+    uint64_t MR = 0, CP = 0;                          // holder of each pair, copy of each leader
+    unsigned valid = 0;                               // pairs held
+    for (unsigned U = lead; U; U &= U - 1) {
+        uint64_t SU = (uint64_t)(__ffs(U) - 1), SC = 0, SB = 0;   // DFS stack: lane, next option, pair
         int top = 0;
         unsigned vis = 0;
-        su[0] = u;
-        sc[0] = 0;
         while (top >= 0) {
-            if (sc[top] == C) {
+            const int x = (int)get4(SU, top), c = (int)get4(SC, top);
+            if (c >= C) {
                 --top;
                 continue;
             }
-            const int b = (ju[su[top]] + sc[top]++) & 15;
+            SC += 1ull << (4 * top);
+            const int b = ((int)get4(B, x) + c) & 15;
             if ((vis >> b) & 1u) continue;
             vis |= 1u << b;
-            sb[top] = b;
-            if (matchR[b] < 0) {                      // augment: level k takes pair sb[k]
+            SB = set4(SB, top, (uint64_t)b);
+            if (!((valid >> b) & 1u)) {               // augment: level k takes pair SB[k]
                 for (int k = top; k >= 0; --k) {
-                    matchR[sb[k]] = su[k];
-                    cu[su[k]] = (sb[k] - ju[su[k]]) & 15;
+                    const int bk = (int)get4(SB, k), xk = (int)get4(SU, k);
+                    MR = set4(MR, bk, (uint64_t)xk);
+                    valid |= 1u << bk;
+                    CP = set4(CP, xk, (uint64_t)((bk - (int)get4(B, xk)) & 15));
                 }
                 break;
             }
-            su[top + 1] = matchR[b];
-            sc[top + 1] = 0;
-            ++top;
+            ++top;                                    // re-route the pair's holder
+            SU = set4(SU, top, get4(MR, b));
+            SC = set4(SC, top, 0);
         }
     }
-    int load[16];
-    for (int b = 0; b < 16; ++b) load[b] = matchR[b] >= 0;
-    for (int u = 0; u < nu; ++u)                      // no free pair in reach: the least loaded one
-        if (cu[u] < 0) {
-            int bc = 0;
-            for (int c = 1; c < C; ++c)
-                if (load[(ju[u] + c) & 15] < load[(ju[u] + bc) & 15]) bc = c;
-            cu[u] = bc;
-            load[(ju[u] + bc) & 15] += 1;
+    const unsigned fr = ~valid & 0xffffu;
+    pad_bank = fr ? __ffs(fr) - 1 : 0;
+    return CP;
+}
+
+// Two copies (pairs b, b+1 for an address in pair b): the options are arcs of
+// two consecutive pairs on the 16-cycle, so a sweep over the pairs assigning
+// each pair to the waiting address with the earliest deadline (the one carried
+// over from the previous pair first) is a maximum matching; the sweep starts
+// after a pair no address starts at (no carry into it).  Addresses left over
+// take the less loaded of their two pairs.  O(16) per row.
+__device__ __forceinline__ uint64_t match_copies2(const int (&v)[16], int &pad_bank) {
+    uint32_t c2 = 0;                                  // min(addresses starting at pair b, 2), two bits each
+    uint64_t rk = 0, seen = 0;                        // rank of each lane among its pair's addresses
+    uint64_t ldr = 0;                                 // lowest lane with the same address (equal ones share)
+    unsigned lead = 0;
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        int d = l;
+#pragma unroll
+        for (int k = l - 1; k >= 0; --k)
+            if (v[k] == v[l]) d = k;
+        ldr |= (uint64_t)d << (4 * l);
+        if (v[l] >= 0 && d == l) lead |= 1u << l;
+    }
+#pragma unroll
+    for (int l = 0; l < 16; ++l)
+        if ((lead >> l) & 1u) {
+            const int b = v[l] & 15;
+            const uint32_t n = (seen >> (4 * b)) & 15u;
+            rk |= (uint64_t)n << (4 * l);
+            seen += 1ull << (4 * b);
+            if (((c2 >> (2 * b)) & 3u) < 2u) c2 += 1u << (2 * b);
         }
-    int bp = 0;
-    if (pad)
-        for (int b = 1; b < 16; ++b)
-            if (load[b] < load[bp]) bp = b;
-    *pad_bank = bp;
-    for (int l = 0; l < 16; ++l) cp[l] = uq[l] >= 0 ? cu[uq[l]] : 0;
+    int s0 = 0;                                       // a pair with no address starting just before it
+#pragma unroll
+    for (int b = 15; b >= 0; --b)
+        if (((c2 >> (2 * ((b + 15) & 15))) & 3u) == 0u) s0 = b;
+    uint32_t stay = 0, shift = 0;                     // pair b kept by one of its addresses / pair b+1 taken by one
+    uint32_t carry = 0;
+    for (int k = 0; k < 16; ++k) {
+        const int b = (s0 + k) & 15;
+        const uint32_t n = (c2 >> (2 * b)) & 3u;
+        uint32_t cn;
+        if (carry) {
+            cn = n >= 1u;
+        } else {
+            if (n >= 1u) stay |= 1u << b;
+            cn = n >= 2u;
+        }
+        if (cn && !(k == 15 && ((stay >> s0) & 1u))) shift |= 1u << b;
+        carry = cn;
+    }
+    const uint32_t used = stay | ((shift << 1) | (shift >> 15));
+    uint64_t ld = 0;                                  // addresses per pair, four bits each
+#pragma unroll
+    for (int b = 0; b < 16; ++b) ld |= (uint64_t)((used >> b) & 1u) << (4 * b);
+    uint64_t cp = 0;
+#pragma unroll
+    for (int l = 0; l < 16; ++l)
+        if ((lead >> l) & 1u) {
+            const int b = v[l] & 15, b1 = (b + 1) & 15;
+            const uint32_t r = (uint32_t)((rk >> (4 * l)) & 15u), st = (stay >> b) & 1u;
+            if (((shift >> b) & 1u) && r == st) {
+                cp |= 1ull << (4 * l);
+            } else if (!(st && r == 0)) {             // unmatched: the less loaded of its two pairs
+                if (get4(ld, b1) < get4(ld, b)) {
+                    cp |= 1ull << (4 * l);
+                    ld += 1ull << (4 * b1);
+                } else {
+                    ld += 1ull << (4 * b);
+                }
+            }
+        }
+    int bp = 0;                                       // the padding: the least loaded pair
+#pragma unroll
+    for (int b = 1; b < 16; ++b)
+        if (get4(ld, b) < get4(ld, bp)) bp = b;
+    pad_bank = bp;
+    uint64_t out = 0;                                 // equal addresses: the first one's copy
+#pragma unroll
+    for (int l = 0; l < 16; ++l) out |= get4(cp, (int)get4(ldr, l)) << (4 * l);
+    return out;
 }
 
 // gq copies of the local slots: one thread per (tile, virtual warp, half-warp), per slot row
-__global__ void __launch_bounds__(128) k_ell_copies(const int64_t *__restrict__ ltile, const uint32_t *__restrict__ vofs,
-                                                    int64_t t0, int64_t t1, uint16_t *__restrict__ lsrc) {
+__global__ void __launch_bounds__(128) k_ell_copies(const int64_t *__restrict__ ltile,
+                                                           const uint32_t *__restrict__ vofs, int64_t t0, int64_t t1,
+                                                           uint16_t *__restrict__ lsrc) {
     const int64_t nitem = (t1 - t0) * kVWarps * 2;
     for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nitem;
          item += (int64_t)gridDim.x * blockDim.x) {
@@ -412,41 +483,18 @@ __global__ void __launch_bounds__(128) k_ell_copies(const int64_t *__restrict__ 
         const int K = (int)((vofs[tile * kVofsStride + vw + 1] - o0) >> 5);
         const int64_t base = ltile[tile] + o0;
         for (int s = 0; s < K; ++s) {
-            int v[16], cp[16], bp;
+            int v[16];
+#pragma unroll
             for (int l = 0; l < 16; ++l) {
                 const int x = lsrc[base + ell_slot(s, 16 * half + l, K)];
                 v[l] = x >= (int)kNodeTile ? -2 : x;
             }
-            match_copies(v, kGqCopies, cp, &bp);
+            int bp;
+            const uint64_t cp = kGqCopies == 2 ? match_copies2(v, bp) : match_copies(v, kGqCopies, bp);
+#pragma unroll
             for (int l = 0; l < 16; ++l)
                 lsrc[base + ell_slot(s, 16 * half + l, K)] =
-                    (uint16_t)(v[l] >= 0 ? cp[l] * kGqStride + v[l] : (int)kNodeTile + bp);
-        }
-    }
-}
-
-// psum copies of the piece ranks: one thread per (tile, round warp, half-warp), per
-// piece index k of the half-warp's 16 nodes (the k-th psum load of the node sums)
-__global__ void __launch_bounds__(128) k_plist_copies(const uint16_t *__restrict__ vfirst, int64_t t0, int64_t t1,
-                                                      uint16_t *__restrict__ plist) {
-    const int64_t nitem = (t1 - t0) * kTileWarps * 2;
-    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nitem;
-         item += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t tile = t0 + item / (kTileWarps * 2);
-        const int i0 = (int)(item % (kTileWarps * 2)) * 16;   // the half-warp's first node
-        int pf[16], np[16], mx = 0;
-        for (int l = 0; l < 16; ++l) {
-            pf[l] = vfirst[tile * kVfStride + i0 + l];
-            np[l] = (int)vfirst[tile * kVfStride + i0 + l + 1] - pf[l];
-            mx = max(mx, np[l]);
-        }
-        uint16_t *pl = plist + tile * kVRows;
-        for (int k = 0; k < mx; ++k) {
-            int v[16], cp[16], bp;
-            for (int l = 0; l < 16; ++l) v[l] = k < np[l] ? (int)pl[pf[l] + k] : -1;
-            match_copies(v, kPsumCopies, cp, &bp);
-            for (int l = 0; l < 16; ++l)
-                if (v[l] >= 0) pl[pf[l] + k] = (uint16_t)(cp[l] * kPsumStride + v[l]);
+                    (uint16_t)(v[l] >= 0 ? (int)get4(cp, l) * kGqStride + v[l] : (int)kNodeTile + bp);
         }
     }
 }
@@ -812,6 +860,47 @@ static int64_t grid_cap(di_graph *h, int64_t count, int per_block = 256) {
     return std::max<int64_t>(1, std::min<int64_t>((count + per_block - 1) / per_block, (int64_t)h->num_sms * 16));
 }
 
+// A second stream for plan work nothing else in the build reads (the shared-memory
+// copies of each chunk's ELL): it runs beside the next chunks and the remote
+// phase.  join() orders the main stream after it (before anything frees or
+// reads those arrays); the destructor joins too (error paths).
+struct SideStream {
+    cudaStream_t main, s = nullptr;
+    std::vector<cudaEvent_t> evs;
+    explicit SideStream(cudaStream_t m) : main(m) {}
+    cudaEvent_t mark(cudaStream_t on) {
+        cudaEvent_t e = nullptr;
+        DI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        DI_CUDA(cudaEventRecord(e, on));
+        return e;
+    }
+    cudaStream_t after_main() {                      // ordered after the main stream's work so far
+        if (!s) DI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        DI_CUDA(cudaStreamWaitEvent(s, mark(main), 0));
+        return s;
+    }
+    void join() {
+        if (!s) return;
+        cudaStream_t x = s;
+        s = nullptr;
+        DI_CUDA(cudaStreamWaitEvent(main, mark(x), 0));
+        DI_CUDA(cudaStreamDestroy(x));               // released once its work completes
+    }
+    ~SideStream() {
+        if (s) {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(e, s);
+                cudaStreamWaitEvent(main, e, 0);
+                evs.push_back(e);
+            }
+            cudaStreamDestroy(s);
+        }
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
+};
+
 template <typename W>
 static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
     DevGraph &g = h->g;
@@ -940,6 +1029,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
     phase_mark(st, "tiles: allocate");
     // ---- phase 2: local edges into the ELL, remote edges into the remote list
     const bool bank_order = getenv("DIT_BANK_ORDER") != nullptr;
+    SideStream side(st);
     for (int c = 0; c < nch; ++c) {
         const int64_t i0 = node_of(ctile[c]), i1 = node_of(ctile[c + 1]);
         if (feed) {
@@ -964,13 +1054,9 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
                                                                  tp.vofs, tp.vfirst, tp.plist, vcap, (const SW *)g.w,
                                                                  e0, tp.lsrc, (SW *)tp.lw);
         count_launch();
-        if (ctile[c + 1] > ctile[c]) {               // k_plan_ell has placed the chunk's pieces: ranks are final
-            k_plist_copies<<<(int)grid_cap(h, (ctile[c + 1] - ctile[c]) * kTileWarps * 2, 128), 128, 0, st>>>(
-                tp.vfirst, ctile[c], ctile[c + 1], tp.plist);
-            count_launch();
-        }
-        if (!bank_order && ctile[c + 1] > ctile[c]) {
-            k_ell_copies<<<(int)grid_cap(h, (ctile[c + 1] - ctile[c]) * kVWarps * 2, 128), 128, 0, st>>>(
+        // k_plan_ell has placed the chunk's slots: their gq copies beside the next chunks
+        if (kGqCopies > 1 && !bank_order && ctile[c + 1] > ctile[c]) {
+            k_ell_copies<<<(int)grid_cap(h, (ctile[c + 1] - ctile[c]) * kVWarps * 2, 128), 128, 0, side.after_main()>>>(
                 tp.ltile, tp.vofs, ctile[c], ctile[c + 1], tp.lsrc);
             count_launch();
         }
@@ -980,7 +1066,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
         k_ell_balance<W><<<(int)std::min<int64_t>(tp.ntile * kVWarps / kBalWarps + 1, (int64_t)h->num_sms * 16),
                            kBalWarps * 32, 0, st>>>(tp.ltile, tp.vofs, tp.ntile, tp.lsrc, (SW *)tp.lw);
         k_ell_copies<<<(int)grid_cap(h, tp.ntile * kVWarps * 2, 128), 128, 0, st>>>(tp.ltile, tp.vofs, 0, tp.ntile,
-                                                                               tp.lsrc);
+                                                                              tp.lsrc);
         count_launch(2);
     }
     for (void *p : {(void *)sk0, (void *)sk1, (void *)sv0, (void *)sv1, (void *)lsc, (void *)lsp, (void *)lst})
@@ -993,6 +1079,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
             for (void *p : {(void *)rk0, (void *)rk1, (void *)rv0, (void *)rv1, (void *)rw64, (void *)lc, (void *)rsc,
                             (void *)rsp, (void *)pcnt, (void *)tmp, (void *)vcap})
                 cudaFreeAsync(p, st);
+            side.join();
             free_tiles(tp, st);
             return;                                  // the caller reports the error
         }
@@ -1166,6 +1253,7 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
     DI_CUDA(cudaFreeAsync(htmp, st));
     DI_CUDA(cudaFreeAsync(vcap, st));
     DI_CUDA(cudaFreeAsync(mx, st));
+    side.join();
     DI_CUDA(cudaStreamSynchronize(st));
     DI_CUDA(cudaGetLastError());
     tp.max_tile_edges = (int64_t)mxh;

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
     constexpr int kWB = kW ? (int)sizeof(StoreW<W>) : 0;
     constexpr int kRS = (int)sizeof(RemRec<W>);
     double *gq = reinterpret_cast<double *>(smem);                       // [kGqCopies][kGqStride]: outflow, zero pad slots
-    double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kPsumCopies][kPsumStride]: piece sums by rank
+    double *psum = reinterpret_cast<double *>(smem + kOffPsum);          // [kVRows]: piece sums by rank
     // prepared rows, structure of arrays [2][kNodeTile] each (consecutive threads, consecutive banks)
     double *Pf = reinterpret_cast<double *>(smem + kOffP);
     double *Pivi = Pf + 2 * kNodeTile;
@@ -478,8 +478,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                         double acc;
                         if ((int)o0 >= st) acc = local_sum<W>(es_sm, ew_sm, gq, (int)o0 + lane, K);
                         else acc = local_sum<W>(es_gl, ew_gl, gq, (int)o0 + lane, K);
-#pragma unroll
-                        for (int c = 0; c < kPsumCopies; ++c) psum[c * kPsumStride + vw * 32 + lane] = acc;
+                        psum[vw * 32 + lane] = acc;
                     }
                 }
                 const long long tb = kProf ? clock64() : 0;

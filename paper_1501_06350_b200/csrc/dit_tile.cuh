@@ -44,14 +44,6 @@ constexpr int64_t kGqSlots = kNodeTile + 16;     // outflow per node + one zero 
 constexpr int kGqCopies = DIT_GQ_COPIES;
 constexpr int kGqStride = (int)kGqSlots + 1;
 static_assert(kGqCopies >= 1 && kGqCopies <= 16 && kGqStride % 16 == 1, "gq copies shift by one bank pair");
-// the same for the piece sums psum (the node sums' reads; plist holds c * kPsumStride + rank)
-#ifndef DIT_PSUM_COPIES
-#define DIT_PSUM_COPIES 1
-#endif
-constexpr int kPsumCopies = DIT_PSUM_COPIES;
-constexpr int kPsumStride = kVRows + 1;
-static_assert(kPsumCopies >= 1 && kPsumCopies <= 16 && kPsumStride % 16 == 1 && kPsumCopies * kPsumStride < 65536,
-              "psum copies shift by one bank pair");
 constexpr int kTileSmemBudget = 227 * 1024 - 2048;   // dynamic shared memory of k_tile (static arrays aside)
 static_assert(kVWarps == 2 * kTileWarps, "two virtual warps per round warp");
 
@@ -92,7 +84,7 @@ struct PrepRow {                                 // (size only: k_tile keeps the
 };
 static_assert(sizeof(PrepRow) == 32, "32-byte prepared rows");
 constexpr int kOffPsum = (kGqCopies * kGqStride * 8 + 127) & ~127;
-constexpr int kOffP = (kOffPsum + kPsumCopies * kPsumStride * 8 + 127) & ~127;
+constexpr int kOffP = kOffPsum + kVRows * 8;
 constexpr int kOffR = kOffP + 2 * (int)kNodeTile * (int)sizeof(PrepRow);
 template <typename W>
 constexpr int tile_rec_buf() { return (((int)kLightCap * (int)sizeof(RemRec<W>) + 32) + 127) & ~127; }
