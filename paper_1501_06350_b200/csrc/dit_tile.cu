@@ -280,8 +280,9 @@ struct TileScalars {
 
 // named barriers (0 is __syncthreads): 1 = the round warps, 2 = the prep warps,
 // 3 + x = "P[x] full" (prep arrives, rounds sync), 5 + x = "P[x] read" (rounds
-// arrive, prep syncs): a warp waiting at a hardware barrier issues nothing
-constexpr int kBarRW = 1, kBarPW = 2, kBarPFull = 3, kBarPEmpty = 5;
+// arrive, prep and the producer sync), 7 + x = "R[x] read" (prep arrives, the
+// producer syncs): a warp waiting at a hardware barrier issues nothing
+constexpr int kBarRW = 1, kBarPW = 2, kBarPFull = 3, kBarPEmpty = 5, kBarRFree = 7;
 
 __device__ __forceinline__ void bar_sync_n(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -337,7 +338,7 @@ __device__ __forceinline__ void issue_records(const TileArgs<W> &a, int64_t r0, 
 //   round warps 0-15 -- thread i owns node i of the current tile: the `rounds`
 //     Jacobi rounds over the tile's local in-edges (Eq. (8) pushes, sliced-ELL
 //     slots from shared memory), then F, H += D, A = d D inv out;
-//   prep warps 16.. (kPWt threads, kPN nodes each) -- meanwhile the NEXT tile's
+//   prep warps 16-22 (kPWt threads, <= kPN nodes each) -- meanwhile the NEXT tile's
 //     inflow: the remote pushes still
 //     pending (heavy sums, light records' gathered outflow) added to F, into P.
 // TMA bulk copies bring each tile's edge bundle (round warps) and light records
@@ -397,16 +398,6 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
     if (is_rw) {
         // ------------------------------------------------ round warps
         const int i = tid, wp = tid >> 5;
-        auto escal = [&](int64_t jt) {
-            const int64_t t = tid_of(jt);
-            return TileScalars{a.ltile[t], a.ltile[t + 1], a.lstage[t], 0};
-        };
-        if (i == 0)
-            for (int x = 0; x < 2; ++x)
-                if (blockIdx.x + x * G < a.ntw) {
-                    sc[x] = escal(blockIdx.x + x * G);
-                    issue_edges<W>(a, tid_of(blockIdx.x + x * G), sc[x], ebuf(x), E_full(x));
-                }
         long long ls_cyc = 0, b2_cyc = 0, ns_cyc = 0, b1_cyc = 0;   // DIT_TILE_TIMING: local sums, wait after them
         long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pn[2] = {0, 0};
         int k = 0;
@@ -418,12 +409,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             const int nn = (int)min(kNodeTile, a.n - a0);
             const bool valid = i < nn;
             const int64_t j = a0 + i;
-            // scalars of the tile two ahead (loaded now, used after the rounds)
-            TileScalars nx{0, 0, 0, 0};
-            const bool has_nx = jt + 2 * G < a.ntw;
-            if (i == 0 && has_nx) nx = escal(jt + 2 * G);
             long long c0 = kProf ? clock64() : 0;
-            bar_sync_n(kBarPFull + x, kTileBlock);
+            bar_sync_n(kBarPFull + x, kRW + kPWt);
             // f, 1/sum w and the out-degree now; H and wr from P[x] again at the state out
             const int pi = x * (int)kNodeTile + i;
             double f = 0.0, pivi = 0.0;
@@ -506,16 +493,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 }
             }
             long long c3 = kProf ? clock64() : 0;
-            // E[x] is read by every round warp (the last node sums read pl_s): the
-            // bundle of the tile two ahead goes in now, before this thread's state-out
-            // stores (the proxy fence of the issue would wait for them to complete)
-            bar_sync_n(kBarRW, kRW);
-            const long long c4 = kProf ? clock64() : 0;
-            if (i == 0 && has_nx) {
-                sc[x] = nx;
-                issue_edges<W>(a, tid_of(jt + 2 * G), nx, E, E_full(x));
-            }
-            const long long c5 = kProf ? clock64() : 0;
+            const long long c4 = c3, c5 = c3;
             // state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
             if (valid) {
                 a.F[j] = f;
@@ -526,7 +504,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 resid += fabs(f) + fabs(d * D) * (double)Pwr[pi];
                 if (pdeg == 0) leak += D;             // dangling: the fluid left the system (§3.3)
             }
-            if (jt + 2 * G < a.ntw) bar_arrive_n(kBarPEmpty + x, kTileBlock);   // prep syncs it before tile k + 2
+            // P[x] and E[x] read by this warp: prep refills them for tile k + 2
+            if (jt + 2 * G < a.ntw) bar_arrive_n(kBarPEmpty + x, kTileBlock);
             if (kProf) {                              // thread 0's counters, in registers until the end
                 const long long c6 = clock64();
                 pc[st == 0 ? 0 : 1] += c3 - c2;       // rounds of fully / partly staged tiles
@@ -560,6 +539,43 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             atomicAdd(&dbg[16 + wp], (unsigned long long)ls_cyc);
             atomicAdd(&dbg[15], (unsigned long long)b1_cyc);
         }
+    } else if (tid >= kRW + kPWt) {
+        // ------------------------------------------------ producer warp: the TMA issue
+        // (a bulk copy's issue can stall ~1k cycles: off the round and prep warps)
+        auto rscal = [&](int64_t jt, int64_t &r0, int64_t &r1) {
+            const int64_t t = tid_of(jt);
+            r0 = recs_on ? a.rtile[t] : 0;
+            r1 = recs_on ? a.rtile[t + 1] : 0;
+        };
+        auto escal = [&](int64_t jt) {
+            const int64_t t = tid_of(jt);
+            return TileScalars{a.ltile[t], a.ltile[t + 1], a.lstage[t], 0};
+        };
+        if (lane == 0) {
+            int64_t r0, r1;
+            rscal(blockIdx.x, r0, r1);
+            issue_records<W>(a, r0, r1, rbuf(0), R_full(0));
+        }
+        int k = 0;
+        for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
+            const int x = k & 1;
+            // the light records of tile k + 1 once prep is done with tile k - 1
+            if (jt + G < a.ntw) {
+                if (k >= 1) bar_sync_n(kBarRFree + (x ^ 1), kPWt + 32);
+                if (lane == 0) {
+                    int64_t r0, r1;
+                    rscal(jt + G, r0, r1);
+                    issue_records<W>(a, r0, r1, rbuf(x ^ 1), R_full(x ^ 1));
+                }
+            }
+            // the edge bundle of tile k once the round warps are done with tile k - 2
+            if (k >= 2) bar_sync_n(kBarPEmpty + x, kTileBlock);
+            if (lane == 0) {
+                sc[x] = escal(jt);
+                issue_edges<W>(a, tid_of(jt), sc[x], ebuf(x), E_full(x));
+            }
+            __syncwarp();
+        }
     } else {
         // ------------------------------------------------ prep warps
         const int p = tid - kRW;
@@ -568,13 +584,6 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             r0 = recs_on ? a.rtile[t] : 0;
             r1 = recs_on ? a.rtile[t + 1] : 0;
         };
-        if (p == 0)
-            for (int x = 0; x < 2; ++x)
-                if (blockIdx.x + x * G < a.ntw) {
-                    int64_t r0, r1;
-                    rscal(blockIdx.x + x * G, r0, r1);
-                    issue_records<W>(a, r0, r1, rbuf(x), R_full(x));
-                }
         int k = 0;
         for (int64_t jt = blockIdx.x; jt < a.ntw; jt += G, ++k) {
             const int x = k & 1;
@@ -583,12 +592,9 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             const int64_t a0 = tile * kNodeTile;
             const int nn = (int)min(kNodeTile, a.n - a0);
             long long c0 = kProf ? clock64() : 0;
-            // per-node state (independent loads, in flight together): nodes p, p + kPWt
             int64_t r0 = 0, r1 = 0;
             rscal(jt, r0, r1);
-            int64_t n0 = 0, n1 = 0;
-            const bool has_nx = jt + 2 * G < a.ntw;
-            if (p == 0 && has_nx) rscal(jt + 2 * G, n0, n1);
+            // per-node state (independent loads, in flight together): nodes p, p + kPWt, ..
             double Fj[kPN], ivi[kPN], Hj[kPN];
             float wrj[kPN];
             int32_t dg[kPN], hx[kPN];
@@ -652,9 +658,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     Pwr[q] = wrj[u];
                     Pdeg[q] = dg[u];
                 }
-            bar_arrive_n(kBarPFull + x, kTileBlock);
-            bar_sync_n(kBarPW, kPWt);                      // R[x] read by every prep warp
-            if (p == 0 && has_nx) issue_records<W>(a, n0, n1, rbuf(x), R_full(x));
+            bar_arrive_n(kBarPFull + x, kRW + kPWt);
+            if (jt + 2 * G < a.ntw) bar_arrive_n(kBarRFree + x, kPWt + 32);   // R[x] read: the producer refills it
             if (kProf && p == 0) {
                 dbg[4] += c1 - c0;                    // node loads + waiting for the records
                 dbg[5] += c2 - c1;                    // gathers + sums

@@ -10,9 +10,9 @@
 namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // build kernels: thread i owns node i of the tile
-// k_tile: one CTA per SM, 16 round warps (thread i owns node i) and 4 prep warps
-// (the next tile's inflow, DIT_PREP_NODES = 4 nodes per thread: 640 threads;
-// 2 nodes per thread was 2% slower, 8 and 16 starve the round warps)
+// k_tile: one CTA per SM of 24 warps: 16 round warps (thread i owns node i), 7
+// prep warps (the next tile's inflow, up to 3 nodes per thread) and a producer
+// warp issuing the TMA bulk copies
 constexpr int kRW = (int)kNodeTile;
 #ifndef DIT_LS_UNROLL
 #define DIT_LS_UNROLL 2
@@ -22,12 +22,12 @@ constexpr int kLsUnroll = DIT_LS_UNROLL;          // k_tile: slot groups per unr
 #define DIT_REC_UNROLL 8
 #endif
 constexpr int kRecUnroll = DIT_REC_UNROLL;        // k_tile prep: light-record gathers in flight per thread
-#ifndef DIT_PREP_NODES
-#define DIT_PREP_NODES 2
+#ifndef DIT_PREP_WARPS
+#define DIT_PREP_WARPS 7
 #endif
-constexpr int kPWt = (int)kNodeTile / DIT_PREP_NODES;   // nodes per prep thread
-constexpr int kPN = (int)kNodeTile / kPWt;
-constexpr int kTileBlock = kRW + kPWt;
+constexpr int kPWt = 32 * DIT_PREP_WARPS;        // prep threads
+constexpr int kPN = ((int)kNodeTile + kPWt - 1) / kPWt;   // nodes per prep thread (at most)
+constexpr int kTileBlock = kRW + kPWt + 32;      // + the producer warp (TMA issue)
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kVRows = 2 * (int)kNodeTile;       // local-edge pieces per tile (at most)
 constexpr int kVWarps = kVRows / 32;             // virtual warps: round warp w runs w and kVWarps-1-w
