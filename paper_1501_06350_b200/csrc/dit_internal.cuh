@@ -95,7 +95,7 @@ constexpr int64_t kLightCap = DIT_LIGHT_CAP;   // light remote records per tile 
 #endif
 constexpr int64_t kHeavyTh = DIT_HEAVY_TH;       // remote in-degree above which a target is heavy
 #ifndef DIT_HEAVY_CHUNK
-#define DIT_HEAVY_CHUNK 2048
+#define DIT_HEAVY_CHUNK 1024
 #endif
 constexpr int64_t kHeavyChunk = DIT_HEAVY_CHUNK;   // heavy edges per k_heavy chunk
 
