@@ -117,7 +117,7 @@ def workload_name(spec, cfg):
 
 # ------------------------------------------------------------------ CPU oracle
 TILE_NODES = 512   # include/dit.h DI_TILE_NODES (the oracle takes the tile as a parameter)
-TILE_WAVES = 2     # include/dit.h DI_TILE_WAVES
+TILE_WAVES = 3     # include/dit.h DI_TILE_WAVES
 
 
 def oracle_run(args, spec, cols, n, sweeps):

@@ -73,7 +73,7 @@ extern "C" {
                                      the next sweep (deterministic); every node holding fluid
                                      diffuses (theta is not used). */
 #define DI_TILE_NODES 512         /* node ids per tile of DI_VARIANT_TILED */
-#define DI_TILE_WAVES 2           /* DI_VARIANT_TILED: the tiles of a sweep run in this many
+#define DI_TILE_WAVES 3           /* DI_VARIANT_TILED: the tiles of a sweep run in this many
                                      waves (tile index mod waves); a wave's pushes to tiles of
                                      later waves are taken in during the same sweep (DESIGN.md
                                      R15).  Shards number waves from their first tile; pushes to

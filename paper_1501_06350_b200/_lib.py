@@ -29,7 +29,7 @@ DI_W_NONE, DI_W_F32, DI_W_F64 = 0, 1, 2
 DI_DANGLING_DROP, DI_DANGLING_COMPLETE = 0, 1
 DI_VARIANT_AUTO, DI_VARIANT_PUSH, DI_VARIANT_PULL, DI_VARIANT_TILED = 0, 1, 2, 3
 DI_TILE_NODES = 512   # include/dit.h
-DI_TILE_WAVES = 2     # include/dit.h (shards too: cross-rank pushes wait a sweep, R16)
+DI_TILE_WAVES = 3     # include/dit.h (shards too: cross-rank pushes wait a sweep, R16)
 
 EXPORTS = ["di_solve_opts_default", "di_graph_create", "di_graph_destroy", "di_graph_info", "di_solve",
            "di_resume", "di_update_edges", "di_get_state", "di_set_state", "di_last_error",

@@ -540,8 +540,10 @@ void launch_sweep(di_graph *h) {
 }
 
 void launch_sweep_reduce(di_graph *h) {
-    if (!h->s.tiled_call) launch_reduce(h, 0);   // the tile kernel ends its own sweep
-    mark_event(h, h->s.launched, 4);
+    if (!h->s.tiled_call) {                      // the tile kernel ends its own sweep (events 0..2W)
+        launch_reduce(h, 0);
+        mark_event(h, h->s.launched, 4);
+    }
     h->s.launched += 1;
 }
 

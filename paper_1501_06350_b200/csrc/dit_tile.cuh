@@ -101,7 +101,7 @@ static_assert(kOffP % 16 == 0 && kOffR % 128 == 0 && kMetaBytes % 16 == 0, "alig
 #endif
 constexpr int64_t kStripeBytes = (int64_t)DIT_STRIPE_MB << 20;   // outflow slice per heavy stripe (L2-resident)
 #ifndef DIT_TILE_WAVES
-#define DIT_TILE_WAVES 2
+#define DIT_TILE_WAVES DI_TILE_WAVES   // include/dit.h
 #endif
 constexpr int kTileWaves = DIT_TILE_WAVES;      // tile waves per sweep (R15), single GPU
 __device__ __forceinline__ int tile_wave(int64_t node, int waves) { return (int)((node / kNodeTile) % waves); }

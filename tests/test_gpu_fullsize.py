@@ -71,7 +71,7 @@ def eq12_residual(n, row_ptr, col, w, H, d, chunk=1 << 27):
 
 
 def test_config2_full_size_vs_oracle(eng, cfg2):
-    # the bench's workload and launch configuration (tiled, 4 local rounds, 2 waves)
+    # the bench's workload and launch configuration (tiled, 4 local rounds, DI_TILE_WAVES waves)
     g = cfg2
     G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
     H, res = G.solve(d=D, tol=1e-12, variant="tiled", local_rounds=4)

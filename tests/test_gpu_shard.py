@@ -181,7 +181,7 @@ def test_nccl_world1(gpu):
 @pytest.mark.parametrize("world", [2, 4])
 def test_lockstep_tiled_full_size_sampled(gpu, world):
     # BASELINE configs[2] at full size (50M nodes, ~1B weighted edges) split over
-    # `world` lock-step shards, in the sharded bench's schedule (tiled, 4 local rounds, 2 waves
+    # `world` lock-step shards, in the sharded bench's schedule (tiled, 4 local rounds, DI_TILE_WAVES waves
     # per rank): converged to tol, and Eq. (12) H + F = F0 + d P H on sampled nodes
     # (the oracle's float64 arithmetic over the global CSR)
     from paper_1501_06350_b200 import _lib, dist
