@@ -49,9 +49,9 @@ namespace dit {
 
 // ---------------------------------------------------------------- heavy remote sums
 // Heavy targets' remote inflow, per wave, in two launches:
-//   k_heavy_chunks -- one launch per source stripe (the gathered slice of the
-//     outflow A stays L2-resident), CTAs stride over the stripe's 2048-edge
-//     chunks (a shared ticket counter was measured 2x slower: 40K same-address
+//   k_heavy_chunks -- one launch per wave, CTAs stride statically over its
+//     1024-edge chunks in source-stripe order (the gathered slice of the outflow
+//     A stays L2-resident; a shared ticket counter was measured 2x slower: 40K same-address
 //     atomics per wave serialise at one L2 slice); a CTA stages A(src) w of its
 //     chunk in shared memory, then one thread per short segment (target within
 //     chunk) / one warp per long one sums it into part;
@@ -59,7 +59,7 @@ namespace dit {
 //     stripe) and their segments summed in stripe / edge order into hsum.
 // Every sum has a fixed order whatever CTA takes which chunk: bitwise reproducible.
 
-// the chunks [c0, c1) of one stripe; CTA per chunk at a time
+// the chunks [c0, c1) of one wave (stripe order); CTA per chunk at a time
 template <typename W>
 __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__restrict__ hrec,
                                                            const int64_t *__restrict__ chunk_start,
@@ -816,10 +816,12 @@ static void launch_heavy_t(di_graph *h, int wave, int force) {
     if (tp.nh == 0) return;
     const int64_t S = tp.nstripe, g0 = (int64_t)wave * S;
     const int64_t t0 = tp.wave_slot[wave], t1 = tp.wave_slot[wave + 1];
-    // one launch per source stripe: the gathered slice of A (kStripeBytes) stays in L2
-    for (int64_t sg = 0; sg < S; ++sg) {
-        const int64_t a0 = tp.s_chunk[g0 + sg], a1 = tp.s_chunk[g0 + sg + 1];
-        if (a1 <= a0) continue;
+    // one launch over the wave's stripes in stripe order: the CTAs stride over the
+    // chunks statically and advance together, so the gathered slice of A
+    // (kStripeBytes) of the stripe being worked on stays L2-resident (one launch
+    // per stripe was 4% slower at configs[2]: 8 launch tails per wave)
+    const int64_t a0 = tp.s_chunk[g0], a1 = tp.s_chunk[g0 + S];
+    if (a1 > a0) {
         const int grid = (int)std::min<int64_t>(a1 - a0, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
         k_heavy_chunks<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
                                                             tp.cfirst, a0, a1, s.A, s.A2, tp.part, wave, tp.waves,
