@@ -29,7 +29,7 @@ struct SweepRec {
     int use_pull, pad;
 };
 constexpr int64_t kHistCap = 1 << 16;
-constexpr int kEvPerSweep = 8;          // profiling events per sweep (tiled: 2 W + 1)
+constexpr int kEvPerSweep = 17;         // profiling events per sweep (tiled: 2 W + 1; waves > 8 not timed)
 
 // Device-resident control block: the solver loop runs without host round
 // trips; the host polls `done` once per chunk of sweeps.

@@ -432,7 +432,7 @@ static void collect_profile(di_graph *h, const Ctrl &r) {
             // per heavy edge rec + 8, per heavy segment / run 24 B)
             const TilePlan &tp = g.tl;
             const double rec = g.w_kind == DI_W_F64 ? 16.0 : 8.0;
-            for (int c = 0; c < tp.waves; ++c) {
+            for (int c = 0; c < tp.waves && 2 * c + 2 < kEvPerSweep; ++c) {
                 float th, tt;
                 DI_CUDA(cudaEventElapsedTime(&th, ev(2 * c), ev(2 * c + 1)));
                 DI_CUDA(cudaEventElapsedTime(&tt, ev(2 * c + 1), ev(2 * c + 2)));
@@ -511,7 +511,7 @@ void prepare_call(di_graph *h, double tol, const di_solve_opts &o, double *stats
 
 void mark_event(di_graph *h, int64_t sweep, int k) {  // profiling events (declared in dit_internal.cuh)
     State &s = h->s;
-    if (!s.profile || sweep >= kHistCap) return;
+    if (!s.profile || sweep >= kHistCap || k >= kEvPerSweep) return;
     const size_t idx = (size_t)sweep * kEvPerSweep + k;
     while (s.events.size() <= idx) {
         cudaEvent_t e;
