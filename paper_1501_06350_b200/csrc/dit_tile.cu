@@ -233,10 +233,18 @@ __device__ __forceinline__ double local_sum(const uint16_t *es, const StoreW<W> 
     for (; s < Kg; s += kSlotGroup) {
         const int k = o0 + 32 * s + kSlotGroup * lane;
         const uint2 e = *reinterpret_cast<const uint2 *>(es + k);
+#ifdef DIT_ABL_NOGATHER
+        const double v0 = (double)(e.x & 0xffffu), v1 = (double)(e.x >> 16), v2 = (double)(e.y & 0xffffu), v3 = (double)(e.y >> 16);
+#else
         const double v0 = gq[e.x & 0xffffu], v1 = gq[e.x >> 16], v2 = gq[e.y & 0xffffu], v3 = gq[e.y >> 16];
+#endif
         if constexpr (kW) {
             if constexpr (sizeof(StoreW<W>) == 4) {
+#ifdef DIT_ABL_NOWEIGHT
+                const float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
+#else
                 const float4 w4 = *reinterpret_cast<const float4 *>(ew + k);
+#endif
                 a0 = fma(v0, (double)w4.x, a0);
                 a1 = fma(v1, (double)w4.y, a1);
                 a2 = fma(v2, (double)w4.z, a2);
@@ -354,9 +362,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
     // prepared rows, structure of arrays [2][kNodeTile] each (consecutive threads, consecutive banks)
     double *Pf = reinterpret_cast<double *>(smem + kOffP);
     double *Pivi = Pf + 2 * kNodeTile;
-    double *PH = Pivi + 2 * kNodeTile;
-    float *Pwr = reinterpret_cast<float *>(PH + 2 * kNodeTile);
-    int32_t *Pdeg = reinterpret_cast<int32_t *>(Pwr + 2 * kNodeTile);
+    int32_t *Pdeg = reinterpret_cast<int32_t *>(Pivi + 2 * kNodeTile);
     auto rbuf = [&](int x) { return smem + kOffR + x * tile_rec_buf<W>(); };
     auto ebuf = [&](int x) { return smem + tile_off_e<W>() + x * tile_e_buf<W>(); };
     // E_full, R_full: TMA completion (count 1)
@@ -439,8 +445,13 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             const int p0 = valid ? (int)vf_s[i] : 0, np = valid ? (int)vf_s[i + 1] - p0 : 0;
             const int pr0 = np > 0 ? pl_s[p0] : 0, pr1 = np > 1 ? pl_s[p0 + 1] : 0;
             const int pr2 = np > 2 ? pl_s[p0 + 2] : 0, pr3 = np > 3 ? pl_s[p0 + 3] : 0;
-            double D = 0.0;
+            double D = 0.0, Hj = 0.0;
+            float wrj = 0.f;
             for (int r = 0; r < a.rounds; ++r) {
+                if (r == a.rounds - 1 && valid) {     // for the state out, in flight during the last round
+                    Hj = a.H[j];
+                    wrj = a.wr[j];
+                }
                 double q = 0.0;
                 if (f != 0.0) {                      // invalid threads hold f = 0
                     D += f;                          // Eq. (10)
@@ -497,11 +508,11 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             // state out; the remote pushes leave as the outflow A (linearity of Eq. (8))
             if (valid) {
                 a.F[j] = f;
-                if (D != 0.0) a.H[j] = PH[pi] + D;
+                if (D != 0.0) a.H[j] = Hj + D;
                 Anext[j] = d * D * pivi;
                 // R13: the pushes still pending carry d D(i) P_{t,i} over the pending
                 // out-edges t, i.e. |d D(i)| wr(i) with wr(i) = inv(i) sum_pending w
-                resid += fabs(f) + fabs(d * D) * (double)Pwr[pi];
+                resid += fabs(f) + fabs(d * D) * (double)wrj;
                 if (pdeg == 0) leak += D;             // dangling: the fluid left the system (§3.3)
             }
             // P[x] and E[x] read by this warp: prep refills them for tile k + 2
@@ -595,24 +606,20 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             int64_t r0 = 0, r1 = 0;
             rscal(jt, r0, r1);
             // per-node state (independent loads, in flight together): nodes p, p + kPWt, ..
-            double Fj[kPN], ivi[kPN], Hj[kPN];
-            float wrj[kPN];
+            double Fj[kPN], ivi[kPN];
             int32_t dg[kPN], hx[kPN];
             int rb[kPN], re[kPN];
 #pragma unroll
             for (int u = 0; u < kPN; ++u) {
                 const int q = p + u * kPWt;
                 const int64_t j = a0 + q;
-                Fj[u] = ivi[u] = Hj[u] = 0.0;
-                wrj[u] = 0.f;
+                Fj[u] = ivi[u] = 0.0;
                 dg[u] = 0;
                 hx[u] = -1;
                 rb[u] = re[u] = 0;
                 if (q < nn) {
                     Fj[u] = a.F[j];
                     ivi[u] = a.inv[j];
-                    Hj[u] = a.H[j];
-                    wrj[u] = a.wr[j];
                     dg[u] = a.deg[j];
                     if (recs_on) {
                         hx[u] = a.hidx[j];
@@ -624,7 +631,11 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             mbar_wait(R_full(x), ph);
             long long c1 = kProf ? clock64() : 0;
             RemRec<W> *recs = reinterpret_cast<RemRec<W> *>(rbuf(x) + (r0 * kRS - ((r0 * kRS) & ~int64_t(15))));
+#ifdef DIT_ABL_NOPREP
+            const int R = 0;
+#else
             const int R = (int)(r1 - r0);
+#endif
             // remote pushes still pending: from the previous sweep, and from this
             // sweep's earlier waves (R15): light records' gathered outflow, in place
 #pragma unroll kRecUnroll
@@ -654,8 +665,6 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     const int q = x * (int)kNodeTile + p + u * kPWt;
                     Pf[q] = Fj[u] + sm[u] + hs[u];
                     Pivi[q] = ivi[u];
-                    PH[q] = Hj[u];
-                    Pwr[q] = wrj[u];
                     Pdeg[q] = dg[u];
                 }
             bar_arrive_n(kBarPFull + x, kRW + kPWt);

@@ -77,15 +77,13 @@ __device__ __forceinline__ double rec_w(const RemRec<W> &r) { return (double)r.w
 // Shared memory of k_tile (one CTA per SM, everything double-buffered by tile
 // parity): gq / psum of the rounds, the prepared per-node rows P, the light
 // records R (prep warps) and the edge bundles E = {layout, staged slots} (round warps).
-struct PrepRow {                                 // (size only: k_tile keeps the fields as arrays)
-    double f, ivi, H;        // inflow-completed fluid, 1/sum w, history
-    float wr;                // pending share of the out-weight (R13)
-    int32_t deg;             // out-degree
-};
-static_assert(sizeof(PrepRow) == 32, "32-byte prepared rows");
+// prepared row of a node (structure of arrays [2][kNodeTile] each): the
+// inflow-completed fluid f and 1/sum w (double), the out-degree (int32).  H and
+// the pending share wr are read by the round warps themselves at the state out.
+constexpr int kPrepBytes = 8 + 8 + 4;
 constexpr int kOffPsum = (kGqCopies * kGqStride * 8 + 127) & ~127;
 constexpr int kOffP = kOffPsum + kVRows * 8;
-constexpr int kOffR = kOffP + 2 * (int)kNodeTile * (int)sizeof(PrepRow);
+constexpr int kOffR = kOffP + 2 * (int)kNodeTile * kPrepBytes;
 template <typename W>
 constexpr int tile_rec_buf() { return (((int)kLightCap * (int)sizeof(RemRec<W>) + 32) + 127) & ~127; }
 template <typename W>
