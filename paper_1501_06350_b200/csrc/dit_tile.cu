@@ -29,15 +29,16 @@
 // gathered stripe by stripe, so that the slice of A being read stays in L2
 // (a random 8-byte read from HBM costs a 64-byte DRAM access on B200).
 //
-// Kernels (B200): k_tile -- one 512-thread CTA per tile, 2 CTAs per SM; the
-// tile's per-node state, piece layout and light records staged by TMA bulk
-// copies (cp.async.bulk + mbarrier, double-buffered), its local edges
-// (sliced-ELL, runs of four slots per lane) prefetched into L2 and read
-// through L1 by the rounds (staged in shared memory too with one 1024-thread
-// CTA per SM, DIT_TILE_BLOCK=1024).  k_heavy_s -- per stripe: CTA per
-// 2048-edge chunk, warp per segment; then the stripe's runs folded into
-// hsum in stripe order.  Every summation has a fixed order: bitwise
-// reproducible run to run.
+// Kernels (B200): k_tile -- persistent, one 768-thread CTA per SM walking the
+// tiles of one wave (R15), warp-specialised: 16 round warps (thread i owns
+// node i of the tile; the rounds over sliced-ELL slots staged in shared
+// memory), 7 prep warps (the next tile's inflow: per-node loads, light-record
+// gathers, heavy sums) and one producer warp issuing the TMA bulk copies
+// (cp.async.bulk + mbarrier, double-buffered edge bundles and light records);
+// named barriers hand the prepared rows from prep to rounds.
+// k_heavy_chunks / k_heavy_fold -- per wave: 1024-edge chunks in source-stripe
+// order (L2-resident slice of A), then per heavy target its runs in stripe
+// order.  Every summation has a fixed order: bitwise reproducible run to run.
 #include "dit_tile.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -493,7 +494,18 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     if (np > 1) acc += x1;
                     if (np > 2) acc += x2;
                     if (np > 3) acc += x3;
-                    for (int p = p0 + 4; p < p0 + np; ++p) acc += psum[pl_s[p]];
+                    // the rest four at a time: ranks, then values, in flight together
+                    for (int p = p0 + 4; p < p0 + np; p += 4) {
+                        const int e = p0 + np;
+                        const int q1 = p + 1 < e ? pl_s[p + 1] : 0, q2 = p + 2 < e ? pl_s[p + 2] : 0;
+                        const int q3 = p + 3 < e ? pl_s[p + 3] : 0;
+                        const double y0 = psum[pl_s[p]], y1 = p + 1 < e ? psum[q1] : 0.0;
+                        const double y2 = p + 2 < e ? psum[q2] : 0.0, y3 = p + 3 < e ? psum[q3] : 0.0;
+                        acc += y0;
+                        if (p + 1 < e) acc += y1;
+                        if (p + 2 < e) acc += y2;
+                        if (p + 3 < e) acc += y3;
+                    }
                     f = acc;
                 } else {
                     f = 0.0;
@@ -638,17 +650,39 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
 #endif
             // remote pushes still pending: from the previous sweep, and from this
             // sweep's earlier waves (R15): light records' gathered outflow, in place
-#pragma unroll kRecUnroll
-            for (int q = p; q < R; q += kPWt) {
-                const RemRec<W> rc = recs[q];
-                const bool early = tile_wave(rc.src, a.waves) < a.wave;
-                const double v = early ? Anext[rc.src] : (gather ? Aprev[rc.src] : 0.0);
-                *reinterpret_cast<double *>(&recs[q]) = v * rec_w(rc);
+            // in batches of kRecUnroll records per thread, every gather of a batch
+            // issued (predicated) before the first product is stored: a loop with a
+            // run-time trip count of ~4 ran in the compiler's remainder loop, one
+            // dependent HBM gather after another
+            for (int q0 = p; q0 < R; q0 += kRecUnroll * kPWt) {
+                RemRec<W> rc[kRecUnroll];
+                double v[kRecUnroll];
+#pragma unroll
+                for (int u = 0; u < kRecUnroll; ++u) {
+                    const int q = q0 + u * kPWt;
+                    if (q < R) rc[u] = recs[q];
+                }
+#pragma unroll
+                for (int u = 0; u < kRecUnroll; ++u) {
+                    const int q = q0 + u * kPWt;
+                    v[u] = 0.0;
+                    if (q < R) {
+                        const bool early = tile_wave(rc[u].src, a.waves) < a.wave;
+                        if (early || gather) v[u] = (early ? Anext : Aprev)[rc[u].src];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kRecUnroll; ++u) {
+                    const int q = q0 + u * kPWt;
+                    if (q < R) *reinterpret_cast<double *>(&recs[q]) = v[u] * rec_w(rc[u]);
+                }
             }
             double hs[kPN];
 #pragma unroll
             for (int u = 0; u < kPN; ++u) hs[u] = hx[u] >= 0 ? a.hsum[hx[u]] : 0.0;
+            const long long c1g = kProf ? clock64() : 0;
             bar_sync_n(kBarPW, kPWt);
+            const long long c1b = kProf ? clock64() : 0;
             double sm[kPN];
 #pragma unroll
             for (int u = 0; u < kPN; ++u) {
@@ -672,6 +706,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             if (kProf && p == 0) {
                 dbg[4] += c1 - c0;                    // node loads + waiting for the records
                 dbg[5] += c2 - c1;                    // gathers + sums
+                dbg[35] += c1g - c1;                  // gathers (this thread)
+                dbg[36] += c1b - c1g;                 // waiting for the other prep warps
                 dbg[6] += c3 - c2;                    // waiting for the round warps
             }
         }

@@ -19,7 +19,7 @@ constexpr int kRW = (int)kNodeTile;
 #endif
 constexpr int kLsUnroll = DIT_LS_UNROLL;          // k_tile: slot groups per unrolled local-sum step
 #ifndef DIT_REC_UNROLL
-#define DIT_REC_UNROLL 8
+#define DIT_REC_UNROLL 2
 #endif
 constexpr int kRecUnroll = DIT_REC_UNROLL;        // k_tile prep: light-record gathers in flight per thread
 #ifndef DIT_PREP_WARPS
@@ -102,7 +102,11 @@ constexpr int64_t kStripeBytes = (int64_t)DIT_STRIPE_MB << 20;   // outflow slic
 #define DIT_TILE_WAVES DI_TILE_WAVES   // include/dit.h
 #endif
 constexpr int kTileWaves = DIT_TILE_WAVES;      // tile waves per sweep (R15), single GPU
-__device__ __forceinline__ int tile_wave(int64_t node, int waves) { return (int)((node / kNodeTile) % waves); }
+// node ids are < 2^31 (int32 columns): 32-bit arithmetic
+static_assert(kNodeTile == 512, "tile_wave shifts by 9");
+__device__ __forceinline__ int tile_wave(int64_t node, int waves) {
+    return (int)((uint32_t)(node >> 9) % (uint32_t)waves);
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }

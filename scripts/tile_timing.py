@@ -34,7 +34,7 @@ print(f"{'RW node sums (per warp)':28s} {v[14]/it/16:10.0f} cycles/tile")
 print(f"{'RW gq write + barrier (per warp)':28s} {v[15]/it/16:10.0f} cycles/tile")
 print(f"rounds of fully staged tiles {v[10]/max(v[11],1):10.0f} cycles/tile over {v[11]:.0f} tiles")
 print(f"rounds of partly staged tiles {v[12]/max(v[13],1):9.0f} cycles/tile over {v[13]:.0f} tiles")
-for k, name in ((32, "RW state out: barrier"), (33, "RW state out: issue"), (34, "RW state out: stores")):
+for k, name in ((35, "PW gathers (thread 0)"), (36, "PW wait other prep warps"), (32, "RW state out: barrier"), (33, "RW state out: issue"), (34, "RW state out: stores")):
     print(f"{name:28s} {v[k]/it:10.0f} cycles/tile")
 print("per round warp: local-sum cycles/tile")
 for w in range(16):
