@@ -527,6 +527,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             k_check_w<<<grid_for(h, n_add), 256, 0, st>>>(aw, n_add, flags + 1);
             count_launch();
         }
+        phase_mark(st, "update: upload + checks");
         int fl[5];
         DI_CUDA(cudaMemcpyAsync(fl, flags, sizeof(fl), cudaMemcpyDeviceToHost, st));
         DI_CUDA(cudaStreamSynchronize(st));
@@ -561,8 +562,13 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             k_mark_adds<<<grid_for(h, n_add), 256, 0, st>>>(as, n_add, chg, addcnt);
             count_launch();
         }
+        phase_mark(st, "update: marks");
         const bool state = h->s.valid;
         const double d = h->s.d;
+        // the tile plan stays, corrected by delta in-edges (dit_delta.cu, DESIGN.md
+        // R18), unless the weight storage changes under it
+        bool keep_plan = delta_enabled(h) && !(g.w_kind == DI_W_F32 && aw && fl[2]);
+        DeltaBatch rem;
         // f32 weight storage must stay exact: promote to f64 if an added weight is not a float
         if (g.w_kind == DI_W_F32 && aw && fl[2]) {
             double *w64 = nullptr;
@@ -579,7 +585,8 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // (rebuilt by the next call that needs them), then allocate every buffer of
         // the new CSR before the state is touched, so that a failure (OOM) leaves
         // graph and fluid as they were
-        free_transpose(g, st);
+        if (keep_plan) free_plan(g.t, st);
+        else free_transpose(g, st);
         int64_t *deg = nullptr, *nrp = nullptr, *cursor = nullptr;
         DI_CUDA(cudaMallocAsync(&deg, (n > 0 ? n : 1) * sizeof(int64_t), st));
         track(deg);
@@ -624,6 +631,22 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         }
         DI_CUDA(cudaGetLastError());
         DI_CUDA(cudaStreamSynchronize(st));
+        phase_mark(st, "update: new CSR");
+        // the removed entries (-w) from the old CSR; any failure of the delta path
+        // drops the plan instead (rebuilt from the new CSR on the next tiled call)
+        auto drop_plan = [&]() {
+            delta_batch_free(rem, st);
+            free_tiles(g.tl, st);
+            keep_plan = false;
+        };
+        if (keep_plan) {
+            try {
+                delta_collect_removed(h, del, chg, rem);
+            } catch (const Fail &) {
+                drop_plan();
+            }
+        }
+        phase_mark(st, "update: collect removed");
         // swap in the new CSR (no longer temporaries), recompute the scales of changed rows
         tmp.erase(std::remove_if(tmp.begin(), tmp.end(), [&](void *p) { return p == nrp || p == ncol || p == nwt; }),
                   tmp.end());
@@ -634,11 +657,22 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         g.col = ncol;
         g.w = nwt;
         g.m = m2;
+        phase_mark(st, "update: withdraw");
         if (n > 0) launch_scales(h, chg);
+        if (keep_plan) {
+            try {
+                delta_commit(h, rem, as, ad, aw, n_add, chg);
+                delta_batch_free(rem, st);
+            } catch (const Fail &) {
+                drop_plan();
+            }
+        }
+        phase_mark(st, "update: scales + delta commit");
         // Theorem 4, second half: inject d P' H over the new changed columns
         if (state && n > 0) apply_column_fluid(h, chg, d);
         DI_CUDA(cudaGetLastError());
         DI_CUDA(cudaStreamSynchronize(st));
+        phase_mark(st, "update: inject");
         // the entry buffer is sized by m
         if (state) {
             State &s = h->s;
@@ -653,6 +687,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             // dangling nodes of the new graph
             set_leak_from_history(h);
         }
+        phase_mark(st, "update: leak done");
         release();
     } catch (...) {
         release();

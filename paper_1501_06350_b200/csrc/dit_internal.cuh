@@ -99,6 +99,9 @@ constexpr int64_t kHeavyTh = DIT_HEAVY_TH;       // remote in-degree above which
 #endif
 constexpr int64_t kHeavyChunk = DIT_HEAVY_CHUNK;   // heavy edges per k_heavy chunk
 
+constexpr int32_t kDegLocalDelta = 1 << 30;     // TilePlan::deg: the node has in-round delta in-edges
+constexpr int32_t kDegMask = kDegLocalDelta - 1;
+
 struct TilePlan {
     bool built = false;
     int64_t ntile = 0;             // node tiles
@@ -154,6 +157,30 @@ struct TilePlan {
     double *hsum = nullptr;        // [nh] remote inflow of each heavy target
     int64_t max_tile_edges = 0;    // most local in-edges of one tile
     int32_t *lstage = nullptr;     // [ntile] first slot (relative to ltile) that k_tile stages in shared memory
+    // delta in-edges of edge updates since the build (dit_delta.cu, R18):
+    // +w added / -w removed, sorted by (target wave, target, source)
+    int64_t nd = 0;
+    int32_t *dsrc = nullptr, *dtgt = nullptr;
+    double *dw = nullptr;
+    std::vector<int64_t> dwave;    // [waves+1] first entry of each target wave
+    int64_t *dseg = nullptr;       // [segments+1] first entry of each target's run
+    std::vector<int64_t> dsegw;    // [waves+1] first segment of each target wave
+    double *dval = nullptr;        // [nd] per-sweep scratch: A(s) w of each entry
+    // kept delta entries inside one tile (no padding slot), pushed in k_tile's rounds:
+    // per node t dl_ptr[t] .. dl_ptr[t+1] {source - tile base, w}; deg bit 30 flags t
+    int32_t *dl_ptr = nullptr;     // [n+1] or null (none)
+    uint16_t *dl_src = nullptr;
+    double *dl_w = nullptr;
+    int64_t *dbig = nullptr;       // segments of > 4096 entries (a block each), ascending
+    std::vector<int64_t> dbigw;    // [waves+1] first big segment of each wave
+    double *rw0 = nullptr;         // [n] plan-time pending out-weight (set at the first update)
+};
+
+// removed CSR entries of one update (-w), collected before the CSR swap
+struct DeltaBatch {
+    int64_t nrem = 0;
+    int32_t *s = nullptr, *t = nullptr;
+    double *w = nullptr;
 };
 
 // Chunks of whole tiles for the plan builder (dit_plan.cu): chunk c is tiles
@@ -258,6 +285,12 @@ void build_tiles(di_graph *h, const PlanFeed *feed = nullptr, const int *bad = n
 void free_tiles(TilePlan &t, cudaStream_t st);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
+bool delta_enabled(const di_graph *h);
+void delta_collect_removed(di_graph *h, const unsigned char *del, const unsigned char *chg, DeltaBatch &out);
+void delta_batch_free(DeltaBatch &b, cudaStream_t st);
+void delta_commit(di_graph *h, DeltaBatch &rem, const int32_t *as, const int32_t *ad, const double *aw, int64_t nadd,
+                  const unsigned char *chg);
+void launch_delta(di_graph *h, int wave, int force);
 void *cub_scratch(int device, size_t bytes);   // dit_pull.cu: CUB scratch cached per device
 void release_cub_scratch(int device);
 std::mutex &scratch_mutex(int device);         // builds on one device take turns on the cached scratch

@@ -508,7 +508,9 @@ void free_tiles(TilePlan &t, cudaStream_t st) {
     for (void *p : {(void *)t.rrel, (void *)t.hidx, (void *)t.wr, (void *)t.deg, (void *)t.ltile, (void *)t.rtile,
                     (void *)t.vofs, (void *)t.lstage, (void *)t.vfirst, (void *)t.plist, (void *)t.lsrc, t.lw, t.rrec, t.hrec, (void *)t.chunk_start,
                     (void *)t.seg_start, (void *)t.cfirst, (void *)t.run_h, (void *)t.run_seg, (void *)t.part,
-                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run})
+                    (void *)t.hsum, (void *)t.tpart, (void *)t.fold_ptr, (void *)t.fold_h, (void *)t.fold_run,
+                    (void *)t.dsrc, (void *)t.dtgt, (void *)t.dw, (void *)t.rw0, (void *)t.dseg, (void *)t.dval, (void *)t.dbig,
+                    (void *)t.dl_ptr, (void *)t.dl_src, (void *)t.dl_w})
         if (p) cudaFreeAsync(p, st);
     t = TilePlan();
 }

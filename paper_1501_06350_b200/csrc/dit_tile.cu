@@ -207,6 +207,9 @@ struct TileArgs {
     const StoreW<W> *lw;
     const RemRec<W> *rrec;
     const double *hsum;
+    const int32_t *dl_ptr;   // delta in-edges inside the tile (dit_delta.cu, R18) or null
+    const uint16_t *dl_src;
+    const double *dl_w;
     double *F, *H, *A0, *A1;
     double *part;            // per-CTA partials: resid [grid], leak [grid]
     unsigned long long *dbg; // optional per-CTA phase cycle counters [grid][kDbg] (DIT_TILE_TIMING)
@@ -427,6 +430,13 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 pivi = Pivi[pi];
                 pdeg = Pdeg[pi];
             }
+            // delta in-edges inside the tile left by an edge update (R18, rare): pushed in the rounds
+            int32_t db = 0, de = 0;
+            if (pdeg & kDegLocalDelta) {
+                pdeg &= kDegMask;
+                db = a.dl_ptr[j];
+                de = a.dl_ptr[j + 1];
+            }
             long long c1 = kProf ? clock64() : 0;
             mbar_wait(E_full(x), ph);
             long long c2 = kProf ? clock64() : 0;
@@ -480,6 +490,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                         psum[vw * 32 + lane] = acc;
                     }
                 }
+                double dl = 0.0;                      // (this round's gq, before the barrier)
+                for (int32_t u = db; u < de; ++u) dl += gq[a.dl_src[u]] * a.dl_w[u];
                 const long long tb = kProf ? clock64() : 0;
                 bar_sync_n(kBarRW, kRW);
                 const long long tc = kProf ? clock64() : 0;
@@ -510,6 +522,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 } else {
                     f = 0.0;
                 }
+                f += dl;
                 if (kProf) {
                     __syncwarp();
                     ns_cyc += clock64() - tc;
@@ -825,6 +838,9 @@ static TileArgs<W> tile_args(di_graph *h, int rounds) {
     a.lw = (const StoreW<W> *)tp.lw;
     a.rrec = (const RemRec<W> *)tp.rrec;
     a.hsum = tp.hsum;
+    a.dl_ptr = tp.nd > 0 ? tp.dl_ptr : nullptr;
+    a.dl_src = tp.dl_src;
+    a.dl_w = tp.dl_w;
     a.F = s.F;
     a.H = s.H;
     a.A0 = s.A;
@@ -917,6 +933,7 @@ static void launch_tile_t(di_graph *h, int rounds) {
     const int64_t k = h->s.launched;
     for (int c = 0; c < h->g.tl.waves; ++c) {          // events: [2c] heavy(c) [2c+1] tile(c) [2c+2]
         launch_heavy_t<W>(h, c, 0);
+        launch_delta(h, c, 0);
         mark_event(h, k, 2 * c + 1);
         launch_tile_kernel_t<W>(h, rounds, c);
         mark_event(h, k, 2 * c + 2);
@@ -973,7 +990,10 @@ void launch_take_ghost_sums(di_graph *h, double *out, int force) {
 
 template <typename W>
 static void launch_flush_t(di_graph *h) {
-    for (int c = 0; c < h->g.tl.waves; ++c) launch_heavy_t<W>(h, c, 1);
+    for (int c = 0; c < h->g.tl.waves; ++c) {
+        launch_heavy_t<W>(h, c, 1);
+        launch_delta(h, c, 1);
+    }
     k_tile_flush<W><<<grid_for(h, h->g.n), kThreads, 0, h->stream>>>(tile_args<W>(h, 0), h->s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());

@@ -87,6 +87,93 @@ def test_tiled_after_update(eng):
     assert np.abs(H.cpu().numpy() - cold.H).sum() <= 1e-9
 
 
+def _delta_entries(G):
+    """delta in-edges the kept tile plan carries (dit_delta.cu debug symbol)"""
+    import ctypes
+    from paper_1501_06350_b200 import _lib
+    f = _lib._lib.di_debug_delta_entries
+    f.restype, f.argtypes = ctypes.c_longlong, [ctypes.c_void_p]
+    return int(f(G.handle))
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_tiled_update_keeps_plan_two_updates(eng, weighted):
+    # DESIGN.md R18: the tile plan stays across Theorem 4 updates, corrected by
+    # delta in-edges (+w added, -w per removed CSR entry); two updates in a row,
+    # the second removing edges the first added, against cold oracle solves
+    spec = synth.CONFIGS[4].scaled(60_000, seed=21, weighted=weighted)
+    g = synth.generate(spec)
+    d1 = synth.rewire(spec, g, fraction=0.01, seed=6)
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, g.w)
+    G.solve(d=D, tol=1e-12, variant="tiled")
+    m0 = G.m
+    G.update_edges(**d1)
+    rp1, c1, w1, _ = graph.apply_delta(g.n, g.row_ptr, g.col, g.w, d1["add_src"], d1["add_dst"], d1["add_w"],
+                                       d1["rem_src"], d1["rem_dst"])
+    n_removed = m0 + len(d1["add_src"]) - len(c1)            # CSR entries (parallel copies) removed
+    # edges inside a tile patch the plan's slots; the rest stay delta entries
+    assert 0 < _delta_entries(G) < len(d1["add_src"]) + n_removed
+    H1, r1 = G.resume(tol=1e-12, variant="tiled")
+    cold1 = di.di_solve(g.n, rp1, c1, w1, D, tol=1e-12)
+    assert r1["converged"]
+    assert np.abs(H1.cpu().numpy() - cold1.H).sum() <= 1e-9
+    # second update: remove 200 distinct edges the first one added, add new ones
+    pairs = np.unique(np.stack([d1["add_src"], d1["add_dst"]], 1), axis=0)[:200]
+    rng = np.random.default_rng(3)
+    k = 500
+    a_src = rng.integers(0, g.n, size=k).astype(np.int32)
+    a_dst = rng.integers(0, g.n, size=k).astype(np.int32)
+    a_w = (0.5 + rng.random(k)).astype(np.float32) if weighted else None
+    G.update_edges(add_src=a_src, add_dst=a_dst, add_w=a_w, rem_src=pairs[:, 0].astype(np.int32),
+                   rem_dst=pairs[:, 1].astype(np.int32))
+    rp2, c2, w2, _ = graph.apply_delta(g.n, rp1, c1, w1, a_src, a_dst, a_w, pairs[:, 0], pairs[:, 1])
+    assert G.m == len(c2)
+    H2, r2 = G.resume(tol=1e-12, variant="tiled")
+    cold2 = di.di_solve(g.n, rp2, c2, w2, D, tol=1e-12)
+    assert r2["converged"]
+    assert np.abs(H2.cpu().numpy() - cold2.H).sum() <= 1e-9
+    # a fresh plan of the final graph (no delta) reaches the same solution
+    G2 = eng.DIGraph(g.n, rp2, c2, w2)
+    H3, _ = G2.solve(d=D, tol=1e-12, variant="tiled")
+    assert _delta_entries(G2) == 0
+    assert np.abs(H3.cpu().numpy() - cold2.H).sum() <= 1e-9
+
+
+def test_tiled_update_dangling_transitions(eng):
+    # nodes losing every out-edge (their fluid leaks from then on, §3.3) and
+    # dangling nodes gaining their first ones, through the kept plan; drop and
+    # 1/n completion against the dense solve of the new graph
+    rng = np.random.default_rng(8)
+    n = 2000
+    deg = rng.integers(0, 7, size=n)
+    deg[rng.random(n) < 0.1] = 0
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    col = rng.integers(0, n, size=rp[-1]).astype(np.int32)
+    local = rng.random(rp[-1]) < 0.6                       # many edges inside the 512-node tiles
+    src = np.repeat(np.arange(n), deg)
+    col[local] = ((src[local] // 512) * 512 + rng.integers(0, 512, size=local.sum())) % n
+    G = eng.DIGraph(n, rp, col)
+    G.solve(d=D, tol=1e-13, variant="tiled")
+    lose = [i for i in range(n) if deg[i] > 0][:40]       # every out-edge removed
+    rem = sorted({(i, int(t)) for i in lose for t in col[rp[i]:rp[i + 1]]})
+    gain = [i for i in range(n) if deg[i] == 0][:40]
+    # the first ten gain only a self-loop (all their fluid stays: pushed inside the rounds, R18)
+    add = [(i, i) for i in gain[:10]] + [(i, int(rng.integers(0, n))) for i in gain[10:] for _ in range(3)]
+    a = np.array(add, np.int32)
+    r_ = np.array(rem, np.int32)
+    G.update_edges(add_src=a[:, 0], add_dst=a[:, 1], rem_src=r_[:, 0], rem_dst=r_[:, 1])
+    assert _delta_entries(G) > 0
+    rp2, c2, _, _ = graph.apply_delta(n, rp, col, None, a[:, 0], a[:, 1], None, r_[:, 0], r_[:, 1])
+    P = graph.dense_P(n, *graph.column_entries(n, rp2, c2, None))
+    x = dense.dense_solve(P, D, synth.uniform_Z(n))
+    H, r = G.resume(tol=1e-13, variant="tiled")
+    assert r["converged"]
+    assert np.abs(H.cpu().numpy() - x).sum() <= 1e-9
+    xc = dense.dense_solve(P, D, synth.uniform_Z(n), completed=True)
+    Hc, _ = G.resume(tol=1e-13, variant="tiled", dangling="complete")
+    assert np.abs(Hc.cpu().numpy() - xc).sum() <= 1e-9
+
 def _stress_graph(wdtype):
     """Every tile-kernel path at once: a tile whose local edges overflow shared
     memory (unstaged rounds), a remote hub spanning several heavy chunks, a tile
