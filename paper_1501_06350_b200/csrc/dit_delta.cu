@@ -279,32 +279,30 @@ __global__ void k_delta_seg(const int64_t *__restrict__ seg, const int32_t *__re
     }
 }
 
-// one block per segment of more than kBigSeg entries (hub targets of the added edges)
-__global__ void __launch_bounds__(256) k_delta_big(const int64_t *__restrict__ seg, const int64_t *__restrict__ big,
-                                                   int64_t b0, const int32_t *__restrict__ dt,
-                                                   const double *__restrict__ v, double *__restrict__ F, int wave,
-                                                   const Ctrl *__restrict__ ctrl, int force) {
+// one 1024-thread block per segment of more than kBigSeg entries (hub targets
+// of the added edges): eight partial sums per thread, then a fixed-order tree
+__global__ void __launch_bounds__(1024) k_delta_big(const int64_t *__restrict__ seg, const int64_t *__restrict__ big,
+                                                    int64_t b0, const int32_t *__restrict__ dt,
+                                                    const double *__restrict__ v, double *__restrict__ F, int wave,
+                                                    const Ctrl *__restrict__ ctrl, int force) {
     if (!force && (ctrl->done || ctrl->use_pull != kUseTiled)) return;
     const bool gather = ctrl->gather != 0;
     if (force ? !gather : (!gather && wave == 0)) return;
-    __shared__ double ws[8];
+    __shared__ double ws[32];
     const int64_t sg = big[b0 + blockIdx.x], bb = seg[sg], be = seg[sg + 1];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int64_t q = bb + threadIdx.x;
-    for (; q + 768 < be; q += 1024) {
-        a0 += v[q];
-        a1 += v[q + 256];
-        a2 += v[q + 512];
-        a3 += v[q + 768];
+    for (; q + 7 * 1024 < be; q += 8 * 1024) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += v[q + u * 1024];
     }
-    for (; q < be; q += 256) a0 += v[q];
-    const double w = warp_sum((a0 + a1) + (a2 + a3));
+    for (; q < be; q += 1024) a[0] += v[q];
+    const double w = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
     if (lane_id() == 0) ws[threadIdx.x >> 5] = w;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double acc = 0.0;
-        for (int k = 0; k < 8; ++k) acc += ws[k];
-        F[dt[bb]] = F[dt[bb]] + acc;
+    if (threadIdx.x < 32) {
+        const double x = warp_sum(ws[threadIdx.x]);
+        if (threadIdx.x == 0) F[dt[bb]] = F[dt[bb]] + x;
     }
 }
 
@@ -351,7 +349,22 @@ __global__ void k_patch_ell(const int32_t *__restrict__ ds, const int32_t *__res
             }
             return lo;
         };
-        const int64_t lo = lower(q, (int32_t)(tile << 9)), qe = lower(lo, (int32_t)((tile + 1) << 9));
+        // most runs are short: their first 32 entries in one coalesced load decide
+        const int64_t r0 = q + lane;
+        const bool in = r0 < cnt && dt[r0] == t;
+        const int32_t sv = in ? ds[r0] : 0;
+        const unsigned m_in = __ballot_sync(0xffffffffu, in);
+        const unsigned m_lo = __ballot_sync(0xffffffffu, in && sv < (int32_t)(tile << 9));
+        const unsigned m_hi = __ballot_sync(0xffffffffu, in && sv < (int32_t)((tile + 1) << 9));
+        int64_t lo, qe;
+        if (m_in != 0xffffffffu) {                       // the run ends inside the first 32
+            lo = q + __popc(m_lo);
+            qe = q + __popc(m_hi);
+        } else {
+            lo = lower(q, (int32_t)(tile << 9));
+            qe = lower(lo, (int32_t)((tile + 1) << 9));
+        }
+        if (qe <= lo) continue;
         bool any = false;                                // this run's new entries inside the tile
         for (int64_t r = lo + lane; r < qe; r += 32) {
             const bool mine = perm[r] >= nold;
@@ -363,6 +376,7 @@ __global__ void k_patch_ell(const int32_t *__restrict__ ds, const int32_t *__res
         const int i = t & 511;
         const int p0 = vfirst[tile * kVfStride + i], p1 = vfirst[tile * kVfStride + i + 1];
         const int64_t base = ltile[tile];
+        for (int pass = 0; pass < 2; ++pass)             // removals first: their slots become free padding
         for (int p = p0; p < p1; ++p) {                  // the target's pieces, their slots
             const int rk = plist[tile * kVRows + p];
             const int vw = rk >> 5, pl = rk & 31;
@@ -379,6 +393,7 @@ __global__ void k_patch_ell(const int32_t *__restrict__ ds, const int32_t *__res
                     if (keep[r] != 2) continue;          // warp-uniform (written by lane 0 below)
                     const int sr = ds[r] & 511;
                     const double w = dw[r];
+                    if ((w < 0.0) != (pass == 0)) continue;
                     const bool match = valid && (w < 0.0 ? (src == sr && (!kW || wv == -w)) : src >= (int)kNodeTile);
                     const unsigned m = __ballot_sync(0xffffffffu, match);
                     if (m) {
@@ -488,12 +503,13 @@ bool delta_enabled(const di_graph *h) {
 
 // Before the CSR swap (old CSR resident): the plan-time pending weights (first
 // update since the plan build) and the removed entries (-w), in row order.
-void delta_collect_removed(di_graph *h, const unsigned char *del, const unsigned char *chg, DeltaBatch &out) {
+void delta_collect_removed(di_graph *h, const unsigned char *del, const unsigned char *chg, DeltaBatch &out,
+                           bool plan) {
     DevGraph &g = h->g;
     TilePlan &tp = g.tl;
     cudaStream_t st = h->stream;
     const int64_t n = g.n;
-    if (!tp.rw0) {
+    if (plan && !tp.rw0) {
         tp.rw0 = dalloc<double>(n, st);
         if (g.w_kind == DI_W_F64)
             k_pending_w<double><<<grid_for(h, n), 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, n, tp.waves,
@@ -640,6 +656,9 @@ void delta_commit(di_graph *h, DeltaBatch &rem, const int32_t *as, const int32_t
         count_launch();
         exclusive_scan_i64(flag, pos, M, st);
         const int64_t nl = sync_read(pos + M);
+        if (getenv("DIT_BUILD_TIMING"))
+            fprintf(stderr, "[dit] delta entries %lld -> kept %lld (inside a tile, in-round: %lld)\n", (long long)N,
+                    (long long)M, (long long)nl);
         uint16_t *lsrc = dalloc<uint16_t>(nl, st);
         double *lwt = dalloc<double>(nl, st);
         int32_t *lptr = dalloc<int32_t>(n + 1, st);
@@ -751,7 +770,7 @@ void launch_delta(di_graph *h, int wave, int force) {
     count_launch(2);
     const int64_t b0 = tp.dbigw[wave], b1 = tp.dbigw[wave + 1];
     if (b1 > b0) {
-        k_delta_big<<<(unsigned)(b1 - b0), 256, 0, h->stream>>>(tp.dseg, tp.dbig, b0, tp.dtgt, tp.dval, h->s.F, wave,
+        k_delta_big<<<(unsigned)(b1 - b0), 1024, 0, h->stream>>>(tp.dseg, tp.dbig, b0, tp.dtgt, tp.dval, h->s.F, wave,
                                                                h->s.ctrl, force);
         count_launch();
     }

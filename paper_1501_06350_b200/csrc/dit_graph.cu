@@ -380,20 +380,37 @@ __global__ void k_mark_adds(const int32_t *__restrict__ as, int64_t nadd, unsign
 }
 
 // F(t) += sign * d * H(j) * w_{j,t} * inv(j) over the out-edges of changed sources j
+// Theorem 4 in one pass over the NEW changed rows (after the CSR swap):
+// F += d H(j) (P' - P) e_j.  Kept entries (the row's prefix) move by
+// d H(j) w (inv'(j) - inv(j)), added ones (the suffix) by d H(j) w inv'(j); the
+// removed entries (k_removed_fluid) by -d H(j) w inv(j).  (float64 atomics: the
+// summation order into F varies run to run, R14.)
 template <typename Wt>
-__global__ void k_column_fluid(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                               const Wt *__restrict__ w, const double *__restrict__ inv,
-                               const unsigned char *__restrict__ chg, const double *__restrict__ H,
-                               double *__restrict__ F, int64_t n, double dsign) {
+__global__ void k_column_fluid_new(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                   const Wt *__restrict__ w, const double *__restrict__ inv_old,
+                                   const double *__restrict__ inv_new, const unsigned char *__restrict__ chg,
+                                   const int64_t *__restrict__ addcnt, const double *__restrict__ H,
+                                   double *__restrict__ F, int64_t n, double d) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t j = warp; j < n; j += nw) {
         if (!chg[j] || H[j] == 0.0) continue;
-        const double a = dsign * H[j] * inv[j];
-        for (int64_t e = row_ptr[j] + lane_id(); e < row_ptr[j + 1]; e += 32) {
-            const double v = w ? a * (double)w[e] : a;
-            red_add(F + col[e], v);
+        const double an = d * H[j] * inv_new[j], ak = an - d * H[j] * inv_old[j];
+        const int64_t b = row_ptr[j], e = row_ptr[j + 1], ke = e - addcnt[j];
+        for (int64_t q = b + lane_id(); q < e; q += 32) {
+            const double a = q < ke ? ak : an;
+            red_add(F + col[q], w ? a * (double)w[q] : a);
         }
+    }
+}
+
+__global__ void k_removed_fluid(const int32_t *__restrict__ rs, const int32_t *__restrict__ rt,
+                                const double *__restrict__ rw, int64_t cnt, const double *__restrict__ inv_old,
+                                const double *__restrict__ H, double *__restrict__ F, double d) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = rs[q];
+        const double h = H[j];
+        if (h != 0.0) red_add(F + rt[q], d * h * inv_old[j] * rw[q]);   // rw = -w
     }
 }
 
@@ -470,18 +487,6 @@ __global__ void k_f32_to_f64(const float *__restrict__ a, double *__restrict__ b
         b[e] = (double)a[e];
 }
 
-template <typename Wt>
-static void column_fluid(di_graph *h, const unsigned char *chg, double dsign) {
-    DevGraph &g = h->g;
-    k_column_fluid<Wt><<<h->num_sms * 8, 256, 0, h->stream>>>(g.row_ptr, g.col, (const Wt *)g.w, g.inv, chg, h->s.H,
-                                                                h->s.F, g.n, dsign);
-    count_launch();
-}
-
-static void apply_column_fluid(di_graph *h, const unsigned char *chg, double dsign) {
-    if (h->g.w_kind == DI_W_F64) column_fluid<double>(h, chg, dsign);
-    else column_fluid<float>(h, chg, dsign);   // unweighted: g.w == nullptr
-}
 
 void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int32_t *add_dst, const void *add_w,
                   int w_dtype, int64_t n_rem, const int32_t *rem_src, const int32_t *rem_dst, int mem) {
@@ -490,9 +495,11 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
     const int64_t n = g.n;
     std::vector<void *> tmp;
     auto track = [&](void *p) { tmp.push_back(p); return p; };
+    DeltaBatch rem;                                  // removed entries (-w), Theorem 4 and the kept plan
     auto release = [&]() {
         for (void *p : tmp) cudaFreeAsync(p, st);
         tmp.clear();
+        delta_batch_free(rem, st);
     };
     try {
         int32_t *as = (int32_t *)track(to_device(add_src, n_add, mem, st));
@@ -568,7 +575,6 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // the tile plan stays, corrected by delta in-edges (dit_delta.cu, DESIGN.md
         // R18), unless the weight storage changes under it
         bool keep_plan = delta_enabled(h) && !(g.w_kind == DI_W_F32 && aw && fl[2]);
-        DeltaBatch rem;
         // f32 weight storage must stay exact: promote to f64 if an added weight is not a float
         if (g.w_kind == DI_W_F32 && aw && fl[2]) {
             double *w64 = nullptr;
@@ -611,8 +617,13 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             DI_CUDA(cudaMallocAsync(&nwt, (m2 > 0 ? m2 : 1) * es, st));
             track(nwt);
         }
-        // every allocation done.  Theorem 4, first half: withdraw d P H over the old changed columns
-        if (state && n > 0) apply_column_fluid(h, chg, -d);
+        // the scales of the old graph (Theorem 4 needs P and P')
+        double *inv_old = nullptr;
+        if (state && n > 0) {
+            DI_CUDA(cudaMallocAsync(&inv_old, n * sizeof(double), st));
+            track(inv_old);
+        }
+        // every allocation done: nothing of graph or state has changed yet
         if (n > 0) {
             if (g.w_kind == DI_W_F64)
                 k_copy_kept<double><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, del, chg,
@@ -635,17 +646,11 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         // the removed entries (-w) from the old CSR; any failure of the delta path
         // drops the plan instead (rebuilt from the new CSR on the next tiled call)
         auto drop_plan = [&]() {
-            delta_batch_free(rem, st);
             free_tiles(g.tl, st);
             keep_plan = false;
         };
-        if (keep_plan) {
-            try {
-                delta_collect_removed(h, del, chg, rem);
-            } catch (const Fail &) {
-                drop_plan();
-            }
-        }
+        // (a failure here leaves graph and fluid as they were)
+        if (keep_plan || state) delta_collect_removed(h, del, chg, rem, keep_plan);
         phase_mark(st, "update: collect removed");
         // swap in the new CSR (no longer temporaries), recompute the scales of changed rows
         tmp.erase(std::remove_if(tmp.begin(), tmp.end(), [&](void *p) { return p == nrp || p == ncol || p == nwt; }),
@@ -657,19 +662,32 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         g.col = ncol;
         g.w = nwt;
         g.m = m2;
-        phase_mark(st, "update: withdraw");
+        if (inv_old) DI_CUDA(cudaMemcpyAsync(inv_old, g.inv, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
         if (n > 0) launch_scales(h, chg);
         if (keep_plan) {
             try {
                 delta_commit(h, rem, as, ad, aw, n_add, chg);
-                delta_batch_free(rem, st);
             } catch (const Fail &) {
                 drop_plan();
             }
         }
         phase_mark(st, "update: scales + delta commit");
-        // Theorem 4, second half: inject d P' H over the new changed columns
-        if (state && n > 0) apply_column_fluid(h, chg, d);
+        // Theorem 4: the corrective fluid d (P' - P) H over the changed columns
+        if (state && n > 0) {
+            if (g.w_kind == DI_W_F64)
+                k_column_fluid_new<double><<<h->num_sms * 8, 256, 0, st>>>(
+                    g.row_ptr, g.col, (const double *)g.w, inv_old, g.inv, chg, addcnt, h->s.H, h->s.F, n, d);
+            else
+                k_column_fluid_new<float><<<h->num_sms * 8, 256, 0, st>>>(
+                    g.row_ptr, g.col, (const float *)g.w, inv_old, g.inv, chg, addcnt, h->s.H, h->s.F, n, d);
+            count_launch();
+            if (rem.nrem > 0) {
+                k_removed_fluid<<<grid_for(h, rem.nrem), 256, 0, st>>>(rem.s, rem.t, rem.w, rem.nrem, inv_old, h->s.H,
+                                                                      h->s.F, d);
+                count_launch();
+            }
+        }
+        delta_batch_free(rem, st);
         DI_CUDA(cudaGetLastError());
         DI_CUDA(cudaStreamSynchronize(st));
         phase_mark(st, "update: inject");

@@ -286,7 +286,8 @@ void free_tiles(TilePlan &t, cudaStream_t st);
 void launch_tile_sweep(di_graph *h, int rounds);
 void launch_tile_flush(di_graph *h);
 bool delta_enabled(const di_graph *h);
-void delta_collect_removed(di_graph *h, const unsigned char *del, const unsigned char *chg, DeltaBatch &out);
+void delta_collect_removed(di_graph *h, const unsigned char *del, const unsigned char *chg, DeltaBatch &out,
+                           bool plan);
 void delta_batch_free(DeltaBatch &b, cudaStream_t st);
 void delta_commit(di_graph *h, DeltaBatch &rem, const int32_t *as, const int32_t *ad, const double *aw, int64_t nadd,
                   const unsigned char *chg);

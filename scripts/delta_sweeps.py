@@ -21,7 +21,9 @@ def sub(mask):
                 add_w=t(delta["add_w"][mask]) if delta["add_w"] is not None else None, rem_src=None, rem_dst=None)
 a_s, a_d = delta["add_src"].astype(np.int64), delta["add_dst"].astype(np.int64)
 cases = [("delta-adds", adds), ("rebuild-adds", adds)]
-if len(sys.argv) > 2 and sys.argv[2] == "full":
+if len(sys.argv) > 2 and sys.argv[2] == "deltaonly":
+    cases = [("delta", dd)]
+elif len(sys.argv) > 2 and sys.argv[2] == "full":
     cases = [("delta", dd), ("rebuild", dd)]
 elif len(sys.argv) > 2:
     cases = [("delta-adds-nondangling", sub(deg[a_s] > 0)), ("delta-adds-dangling", sub(deg[a_s] == 0)),
