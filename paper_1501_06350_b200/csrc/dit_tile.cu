@@ -355,7 +355,7 @@ __device__ __forceinline__ void issue_records(const TileArgs<W> &a, int64_t r0, 
 //     pending (heavy sums, light records' gathered outflow) added to F, into P.
 // TMA bulk copies bring each tile's edge bundle (round warps) and light records
 // (prep warps) into the buffer of its parity; mbarriers hand P between the groups.
-template <typename W, bool kProf>
+template <typename W, bool kProf, bool kDl>
 __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool kW = !std::is_same<W, NoW>::value;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
             }
             // delta in-edges inside the tile left by an edge update (R18, rare): pushed in the rounds
             int32_t db = 0, de = 0;
-            if (pdeg & kDegLocalDelta) {
+            if (kDl && (pdeg & kDegLocalDelta)) {
                 pdeg &= kDegMask;
                 db = a.dl_ptr[j];
                 de = a.dl_ptr[j + 1];
@@ -491,7 +491,8 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                     }
                 }
                 double dl = 0.0;                      // (this round's gq, before the barrier)
-                for (int32_t u = db; u < de; ++u) dl += gq[a.dl_src[u]] * a.dl_w[u];
+                if constexpr (kDl)
+                    for (int32_t u = db; u < de; ++u) dl += gq[a.dl_src[u]] * a.dl_w[u];
                 const long long tb = kProf ? clock64() : 0;
                 bar_sync_n(kBarRW, kRW);
                 const long long tc = kProf ? clock64() : 0;
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) k_tile(TileArgs<W> a, Ctrl *__r
                 } else {
                     f = 0.0;
                 }
-                f += dl;
+                if constexpr (kDl) f += dl;
                 if (kProf) {
                     __syncwarp();
                     ns_cyc += clock64() - tc;
@@ -904,10 +905,8 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
     TilePlan &tp = g.tl;
     static bool attr_set = false;                    // once per weight kind, off the sweep path
     if (!attr_set) {
-        DI_CUDA(cudaFuncSetAttribute(k_tile<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tile_smem_bytes<W>()));
-        DI_CUDA(cudaFuncSetAttribute(k_tile<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tile_smem_bytes<W>()));
+        for (auto f : {k_tile<W, false, false>, k_tile<W, true, false>, k_tile<W, false, true>, k_tile<W, true, true>})
+            DI_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem_bytes<W>()));
         attr_set = true;
     }
     TileArgs<W> a = tile_args<W>(h, rounds);
@@ -922,8 +921,10 @@ static void launch_tile_kernel_t(di_graph *h, int rounds, int wave) {
     a.ntw = tp.ntile > wave ? (tp.ntile - wave + tp.waves - 1) / tp.waves : 0;
     if (a.ntw == 0) return;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntw, (int64_t)h->num_sms));
-    if (a.dbg) k_tile<W, true><<<grid, kTileBlock, tile_smem_bytes<W>(), h->stream>>>(a, s.ctrl);
-    else k_tile<W, false><<<grid, kTileBlock, tile_smem_bytes<W>(), h->stream>>>(a, s.ctrl);
+    // the variant with in-round delta in-edges only after an edge update left some (R18)
+    auto kern = a.dl_ptr ? (a.dbg ? k_tile<W, true, true> : k_tile<W, false, true>)
+                         : (a.dbg ? k_tile<W, true, false> : k_tile<W, false, false>);
+    kern<<<grid, kTileBlock, tile_smem_bytes<W>(), h->stream>>>(a, s.ctrl);
     count_launch();
     DI_CUDA(cudaGetLastError());
 }
