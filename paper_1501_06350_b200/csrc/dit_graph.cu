@@ -358,16 +358,40 @@ __global__ void k_mark_removals(const int64_t *__restrict__ row_ptr, const int32
                                 const int32_t *__restrict__ rs, const int32_t *__restrict__ rd, int64_t nrem,
                                 unsigned char *__restrict__ del, unsigned char *__restrict__ chg,
                                 int *__restrict__ notfound) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nrem; q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t s = rs[q], t = rd[q];
-        int found = 0;
-        for (int64_t e = row_ptr[s]; e < row_ptr[s + 1]; ++e)
-            if (col[e] == t) {
-                del[e] = 1;
-                found = 1;
-            }
-        if (!found) atomicOr(notfound, 1);
-        chg[s] = 1;
+    // a thread per removal in a row of <= 32 entries, the warp for a longer row
+    const unsigned lane = lane_id();
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nrem; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = base + threadIdx.x;
+        int32_t s = 0, t = 0;
+        int64_t b = 0, e = 0;
+        if (q < nrem) {
+            s = rs[q];
+            t = rd[q];
+            b = row_ptr[s];
+            e = row_ptr[s + 1];
+            chg[s] = 1;
+        }
+        if (q < nrem && e - b <= 32) {
+            int found = 0;
+            for (int64_t k = b; k < e; ++k)
+                if (col[k] == t) {
+                    del[k] = 1;
+                    found = 1;
+                }
+            if (!found) atomicOr(notfound, 1);
+        }
+        for (unsigned big = __ballot_sync(0xffffffffu, q < nrem && e - b > 32); big; big &= big - 1) {
+            const int l = __ffs(big) - 1;
+            const int32_t tl = __shfl_sync(0xffffffffu, t, l);
+            const int64_t bl = __shfl_sync(0xffffffffu, b, l), el = __shfl_sync(0xffffffffu, e, l);
+            int found = 0;
+            for (int64_t k = bl + lane; k < el; k += 32)
+                if (col[k] == tl) {
+                    del[k] = 1;
+                    found = 1;
+                }
+            if (!__any_sync(0xffffffffu, found) && lane == 0) atomicOr(notfound, 1);
+        }
     }
 }
 
@@ -433,31 +457,52 @@ __global__ void k_new_deg(const int64_t *__restrict__ row_ptr, const unsigned ch
     }
 }
 
-// copy kept entries of every row in order (warp ballot compaction)
+// copy kept entries of every row in order: a thread per row of <= 32 entries
+// (32 rows per warp step), a warp per longer one (ballot compaction)
 template <typename Wt>
 __global__ void k_copy_kept(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             const Wt *__restrict__ w, const unsigned char *__restrict__ del,
                             const unsigned char *__restrict__ chg, const int64_t *__restrict__ nrp, int64_t n,
                             int32_t *__restrict__ ncol, Wt *__restrict__ nw_, int64_t *__restrict__ cursor) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwp = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lane = lane_id();
-    for (int64_t j = warp; j < n; j += nwp) {
-        const int64_t b = row_ptr[j], e = row_ptr[j + 1];
-        int64_t out = nrp[j];
-        const bool c = chg[j] != 0;
-        for (int64_t k0 = b; k0 < e; k0 += 32) {
-            const int64_t k = k0 + lane;
-            const bool keep = k < e && !(c && del[k]);
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int64_t o = out + __popc(bal & ((1u << lane) - 1u));
-                ncol[o] = col[k];
-                if (w) nw_[o] = w[k];
-            }
-            out += __popc(bal);
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = base + threadIdx.x;
+        int64_t b = 0, e = 0, out = 0;
+        bool c = false;
+        if (j < n) {
+            b = row_ptr[j];
+            e = row_ptr[j + 1];
+            out = nrp[j];
+            c = chg[j] != 0;
         }
-        if (lane == 0) cursor[j] = out;   // additions of row j go from here
+        if (j < n && e - b <= 32) {
+            for (int64_t k = b; k < e; ++k)
+                if (!(c && del[k])) {
+                    ncol[out] = col[k];
+                    if (w) nw_[out] = w[k];
+                    ++out;
+                }
+            cursor[j] = out;                          // additions of row j go from here
+        }
+        for (unsigned big = __ballot_sync(0xffffffffu, j < n && e - b > 32); big; big &= big - 1) {
+            const int l = __ffs(big) - 1;
+            const int64_t jl = __shfl_sync(0xffffffffu, j, l), bl = __shfl_sync(0xffffffffu, b, l),
+                          el = __shfl_sync(0xffffffffu, e, l);
+            int64_t o = __shfl_sync(0xffffffffu, out, l);
+            const bool cl = __shfl_sync(0xffffffffu, c, l);
+            for (int64_t k0 = bl; k0 < el; k0 += 32) {
+                const int64_t k = k0 + lane;
+                const bool keep = k < el && !(cl && del[k]);
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int64_t at = o + __popc(bal & ((1u << lane) - 1u));
+                    ncol[at] = col[k];
+                    if (w) nw_[at] = w[k];
+                }
+                o += __popc(bal);
+            }
+            if (lane == 0) cursor[jl] = o;
+        }
     }
 }
 
@@ -608,6 +653,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
         int64_t m2 = 0;
         DI_CUDA(cudaMemcpyAsync(&m2, nrp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         DI_CUDA(cudaStreamSynchronize(st));
+        phase_mark(st, "update: new degrees");
         int32_t *ncol = nullptr;
         void *nwt = nullptr;
         DI_CUDA(cudaMallocAsync(&ncol, (m2 > 0 ? m2 : 1) * sizeof(int32_t), st));
@@ -624,6 +670,7 @@ void update_edges(di_graph *h, int64_t n_add, const int32_t *add_src, const int3
             track(inv_old);
         }
         // every allocation done: nothing of graph or state has changed yet
+        phase_mark(st, "update: CSR alloc");
         if (n > 0) {
             if (g.w_kind == DI_W_F64)
                 k_copy_kept<double><<<h->num_sms * 8, 256, 0, st>>>(g.row_ptr, g.col, (const double *)g.w, del, chg,
