@@ -139,6 +139,28 @@ def test_tiled_update_keeps_plan_two_updates(eng, weighted):
     assert np.abs(H3.cpu().numpy() - cold2.H).sum() <= 1e-9
 
 
+
+def test_tiled_update_keeps_plan_f64_weights(eng):
+    # float64 weights that are not floats (stored as f64, k_patch_ell's double
+    # slots); the update's weights too; against the cold oracle solve
+    spec = synth.CONFIGS[4].scaled(40_000, seed=23, weighted=True)
+    g = synth.generate(spec)
+    rng = np.random.default_rng(5)
+    w64 = g.w.astype(np.float64) + rng.random(len(g.w)) * 1e-9
+    d1 = synth.rewire(spec, g, fraction=0.01, seed=8)
+    a_w = d1["add_w"].astype(np.float64) + 1e-10
+    G = eng.DIGraph(g.n, g.row_ptr, g.col, w64)
+    G.solve(d=D, tol=1e-12, variant="tiled")
+    G.update_edges(add_src=d1["add_src"], add_dst=d1["add_dst"], add_w=a_w, rem_src=d1["rem_src"],
+                   rem_dst=d1["rem_dst"])
+    assert _delta_entries(G) > 0
+    H, r = G.resume(tol=1e-12, variant="tiled")
+    rp2, c2, w2, _ = graph.apply_delta(g.n, g.row_ptr, g.col, w64, d1["add_src"], d1["add_dst"], a_w,
+                                       d1["rem_src"], d1["rem_dst"])
+    cold = di.di_solve(g.n, rp2, c2, w2, D, tol=1e-12)
+    assert r["converged"]
+    assert np.abs(H.cpu().numpy() - cold.H).sum() <= 1e-9
+
 def test_tiled_update_dangling_transitions(eng):
     # nodes losing every out-edge (their fluid leaks from then on, §3.3) and
     # dangling nodes gaining their first ones, through the kept plan; drop and
