@@ -262,6 +262,12 @@ int di_shard_begin(di_graph *g, double d, const double *Z, int32_t Z_mem, double
 int di_shard_control(di_graph *g, const double *gathered, int32_t nranks);
 /* one sweep (select + diffusion); ghost fluid moved to ghost_out (device double[n_ghost]) */
 int di_shard_sweep(di_graph *g, double *ghost_out);
+/* DI_VARIANT_TILED: the sweep's heavy gather of the rank's own wave-0 targets
+ * (PAPER §3.1 Eq. (8) pushes of the previous sweep), which does
+ * not depend on the exchange: call it after starting the all-to-all of the
+ * ghost fluid di_shard_sweep wrote, so the two overlap.  Optional (di_shard_apply
+ * runs it first when it was not called); a no-op for the other variants. */
+int di_shard_heavy_local(di_graph *g);
 /* F[local_idx[q]] += recv[q] (device double[total]), segment by segment */
 int di_shard_apply(di_graph *g, const double *recv);
 /* local statistics of the current F into the stats buffer given to di_shard_begin */

@@ -276,7 +276,7 @@ def di_plan_stats(h):
 # ------------------------------------------------------------------ shards (multi-GPU)
 EXPORTS += ["di_shard_create", "di_shard_info", "di_shard_ghost_ids", "di_shard_set_recv", "di_shard_begin",
             "di_shard_control", "di_shard_sweep", "di_shard_apply", "di_shard_reduce", "di_shard_poll",
-            "di_shard_finish", "di_shard_flush", "di_shard_flush_apply"]
+            "di_shard_finish", "di_shard_flush", "di_shard_flush_apply", "di_shard_heavy_local"]
 _lib.di_shard_create.argtypes = [_I64, _I64, _I64, _I64, _P, _P, _P, _I32, _I32, _I32, _P, ctypes.POINTER(_P)]
 _lib.di_shard_info.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
 _lib.di_shard_ghost_ids.argtypes = [_P, _P, _I32]
@@ -285,12 +285,13 @@ _lib.di_shard_begin.argtypes = [_P, _D, _P, _I32, _D, ctypes.POINTER(di_solve_op
 _lib.di_shard_control.argtypes = [_P, _P, _I32]
 _lib.di_shard_sweep.argtypes = [_P, _P]
 _lib.di_shard_apply.argtypes = [_P, _P]
+_lib.di_shard_heavy_local.argtypes = [_P]
 _lib.di_shard_flush.argtypes = [_P, _P]
 _lib.di_shard_flush_apply.argtypes = [_P, _P]
 _lib.di_shard_reduce.argtypes = [_P]
 _lib.di_shard_poll.argtypes = [_P, ctypes.POINTER(_I32)]
 _lib.di_shard_finish.argtypes = [_P, _D, ctypes.POINTER(di_solve_opts), _P, _I32, ctypes.POINTER(di_result)]
-for _name in EXPORTS[-11:]:
+for _name in EXPORTS[-12:]:
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -338,6 +339,10 @@ def di_shard_control(h, gathered, nranks):
 
 def di_shard_sweep(h, ghost_out):
     _check(_lib.di_shard_sweep(h, _ptr_mem(ghost_out)[0]))
+
+
+def di_shard_heavy_local(h):
+    _check(_lib.di_shard_heavy_local(h))
 
 
 def di_shard_apply(h, recv):

@@ -459,6 +459,15 @@ int di_shard_sweep(di_graph *g, double *ghost_out) {
     });
 }
 
+int di_shard_heavy_local(di_graph *g) {
+    return guarded([&] {
+        need_shard(g);
+        if (!g->s.valid) fail(DI_ERR_STATE, "di_shard_begin first");
+        use_device(g);
+        shard_heavy_local(g);
+    });
+}
+
 int di_shard_apply(di_graph *g, const double *recv) {
     return guarded([&] {
         need_shard(g);

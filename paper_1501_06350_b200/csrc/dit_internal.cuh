@@ -151,6 +151,7 @@ struct TilePlan {
     std::vector<int64_t> wave_slot;   // [waves+1]
     std::vector<int64_t> s_chunk;  // per (wave, stripe) group [W S + 1]: first chunk
     int waves = 1;                 // tile waves per sweep (R15): wave of tile t = t % waves
+    int groups = 1;                // heavy groups: the waves, + the ghost slots (group `waves`) on a shard
     int64_t nstripe = 0;           // source stripes S
     double *tpart = nullptr;       // k_tile partials [2][waves][grid]
     double *part = nullptr;        // [nseg] segment partial sums
@@ -227,6 +228,7 @@ struct State {
     int rounds = 4;                      // TILED local rounds of the current call
     bool tiled_call = false;
     bool flushing = false;               // shard: the next control follows a flush
+    bool local_pending = false;          // shard (tiled): this sweep's local wave-0 heavy gather not run yet
     int64_t last_sweeps = 0;
     double d = 0.85;
     double *F = nullptr, *H = nullptr;   // [n]
@@ -295,7 +297,7 @@ void launch_delta(di_graph *h, int wave, int force);
 void *cub_scratch(int device, size_t bytes);   // dit_pull.cu: CUB scratch cached per device
 void release_cub_scratch(int device);
 std::mutex &scratch_mutex(int device);         // builds on one device take turns on the cached scratch
-void launch_tile_heavy(di_graph *h, int force, int wave = 0);
+void launch_tile_heavy(di_graph *h, int force, int wave = 0, int group = -1);
 void launch_tile_kernel(di_graph *h, int rounds, int wave = 0);
 int tile_waves(const di_graph *h);
 void launch_take_ghost_sums(di_graph *h, double *out, int force);
@@ -314,6 +316,7 @@ void create_shard(di_graph *h, int64_t n_global, int64_t lo, int64_t hi, int64_t
 void shard_set_recv(di_graph *h, int64_t total, const int32_t *local_idx, int nseg, const int64_t *seg_counts,
                     int mem);
 void shard_sweep(di_graph *h, double *ghost_out);
+void shard_heavy_local(di_graph *h);
 void shard_apply(di_graph *h, const double *recv, int force);
 void shard_control(di_graph *h, const double *gathered, int nranks, int force);
 void shard_reduce(di_graph *h);

@@ -825,7 +825,9 @@ __global__ void k_split_remote(const uint32_t *__restrict__ sk, const uint64_t *
         if (hx >= 0) {
             const int64_t o = hptr[t] + rank;
             htmp[o] = r;
-            hkey[o] = (uint32_t)((t < n ? tile_wave(t, waves) : 0) * nstripe + r.src / stripe_nodes);
+            // heavy group: the target's wave; a shard's ghost slots form one more group (waves),
+            // gathered first in a sweep so that the exchange overlaps the local heavy gather
+            hkey[o] = (uint32_t)((t < n ? tile_wave(t, waves) : waves) * nstripe + r.src / stripe_nodes);
             hval[o] = (uint32_t)o;
             hof[o] = (uint32_t)hx;
         } else {
@@ -924,7 +926,8 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
     if (const char *e = getenv("DIT_TILE_WAVES_RT")) tp.waves = std::max(1, atoi(e));
     // empty waves dropped; at most 32 (the per-wave totals of k_tile's partials array)
     tp.waves = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(tp.waves, 32), tp.ntile));
-    const int64_t S = tp.waves * nS;                 // heavy groups (wave, stripe)
+    tp.groups = tp.waves + (g.nt > n ? 1 : 0);       // + the ghost slots' group on a shard
+    const int64_t S = tp.groups * nS;                // heavy groups (group, stripe)
     if (nt >= (int64_t)0xffffffffLL || m >= ((int64_t)1 << 40)) {
         set_error("tiled plan: graph too large for one handle (fluid slots >= 2^32)");
         throw Fail{DI_ERR_INVALID};
@@ -1197,13 +1200,13 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
                                                           tp.nh, tp.seg_start, tp.chunk_start, tp.cfirst, tp.run_h,
                                                           tp.run_seg, rk0, rv0);
         count_launch();
-        if ((int64_t)tp.waves * tp.nh >= (int64_t)0xffffffffLL) {
+        if ((int64_t)tp.groups * tp.nh >= (int64_t)0xffffffffLL) {
             set_error("tiled plan: too many heavy targets for one graph handle");
             throw Fail{DI_ERR_INVALID};
         }
-        // the heavy targets of each wave, each with its runs in stripe order (k_heavy_fold)
+        // the heavy targets of each group, each with its runs in stripe order (k_heavy_fold)
         {
-            auto fs = radix_sort_u32(rk0, rv0, rk1, rv1, tp.nrun, bits_for((int64_t)tp.waves * tp.nh + 1), st);
+            auto fs = radix_sort_u32(rk0, rv0, rk1, rv1, tp.nrun, bits_for((int64_t)tp.groups * tp.nh + 1), st);
             int64_t *ff, *fslot;
             DI_CUDA(cudaMallocAsync(&ff, (tp.nrun + 1) * sizeof(int64_t), st));
             DI_CUDA(cudaMallocAsync(&fslot, (tp.nrun + 1) * sizeof(int64_t), st));
@@ -1214,19 +1217,19 @@ static void build_tiles_t(di_graph *h, const PlanFeed *feed, const int *bad) {
             DI_CUDA(cudaMallocAsync(&tp.fold_h, (nslot + 1) * sizeof(int32_t), st));
             DI_CUDA(cudaMallocAsync(&tp.fold_run, tp.nrun * sizeof(uint32_t), st));
             unsigned long long *wf;
-            DI_CUDA(cudaMallocAsync(&wf, (tp.waves + 1) * sizeof(unsigned long long), st));
-            k_fill_u64<<<1, 64, 0, st>>>(wf, tp.waves + 1, (unsigned long long)nslot);
+            DI_CUDA(cudaMallocAsync(&wf, (tp.groups + 1) * sizeof(unsigned long long), st));
+            k_fill_u64<<<1, 64, 0, st>>>(wf, tp.groups + 1, (unsigned long long)nslot);
             k_fold_index<<<grid_for(h, tp.nrun), 256, 0, st>>>(fs.first, ff, fslot, tp.nrun, tp.nh, tp.fold_ptr,
                                                                tp.fold_h, wf);
             count_launch(3);
             DI_CUDA(cudaMemcpyAsync(tp.fold_run, fs.second, tp.nrun * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
             DI_CUDA(cudaMemcpyAsync(tp.fold_ptr + nslot, &tp.nrun, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-            std::vector<unsigned long long> w(tp.waves + 1);
-            DI_CUDA(cudaMemcpyAsync(w.data(), wf, (tp.waves + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+            std::vector<unsigned long long> w(tp.groups + 1);
+            DI_CUDA(cudaMemcpyAsync(w.data(), wf, (tp.groups + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                     st));
             DI_CUDA(cudaStreamSynchronize(st));
-            tp.wave_slot.assign(tp.waves + 1, nslot);
-            for (int c = tp.waves - 1; c >= 0; --c) tp.wave_slot[c] = std::min<int64_t>((int64_t)w[c], tp.wave_slot[c + 1]);
+            tp.wave_slot.assign(tp.groups + 1, nslot);
+            for (int c = tp.groups - 1; c >= 0; --c) tp.wave_slot[c] = std::min<int64_t>((int64_t)w[c], tp.wave_slot[c + 1]);
             for (void *p : {(void *)ff, (void *)fslot, (void *)wf, (void *)rk0, (void *)rv0, (void *)rk1, (void *)rv1})
                 DI_CUDA(cudaFreeAsync(p, st));
         }

@@ -129,19 +129,23 @@ __global__ void k_apply_seg(double *__restrict__ F, const int32_t *__restrict__ 
 __global__ void k_control(Ctrl *__restrict__ ctrl, const double *__restrict__ gathered, int nranks, int64_t m,
                           int force);
 
-// Tiled shards: the ghost slots are heavy targets of the tile
-// plan's first wave.  di_shard_sweep runs wave 0's heavy gather (the previous
-// sweep's pushes; ghost sums -> send buffer), the caller exchanges them,
-// di_shard_apply adds the received fluid to F, and di_shard_reduce runs wave
-// 0's tile kernel, then each later wave's heavy gather and tile kernel (R15,
-// R16; local rounds, residual estimate of reading R13 -> stats).
+// Tiled shards: the ghost slots are the tile plan's last heavy
+// group, gathered with wave 0's rule (the previous sweep's pushes).
+// di_shard_sweep gathers them into the send buffer; the caller starts the
+// exchange and meanwhile runs di_shard_heavy_local (wave 0's own heavy
+// targets, independent of what arrives); di_shard_apply adds the received
+// fluid to F (running the local gather first if the caller did not), and
+// di_shard_reduce runs wave 0's tile kernel, then each later wave's heavy
+// gather and tile kernel (R15, R16; local rounds, residual estimate of reading
+// R13 -> stats).  The order of every sum is the one of a single group: the
+// same bits as gathering the ghosts inside wave 0.
 void shard_sweep(di_graph *h, double *ghost_out) {
     if (h->s.tiled_call) {
         const int64_t k = h->s.launched;
         mark_event(h, k, 0);
-        launch_tile_heavy(h, 0);
+        if (h->g.tl.groups > h->g.tl.waves) launch_tile_heavy(h, 0, 0, h->g.tl.waves);
         launch_take_ghost_sums(h, ghost_out, 0);
-        mark_event(h, k, 1);
+        h->s.local_pending = true;
         return;
     }
     launch_sweep(h);
@@ -153,7 +157,15 @@ void shard_sweep(di_graph *h, double *ghost_out) {
     DI_CUDA(cudaGetLastError());
 }
 
+void shard_heavy_local(di_graph *h) {
+    if (!h->s.tiled_call || !h->s.local_pending) return;
+    launch_tile_heavy(h, 0, 0, 0);
+    mark_event(h, h->s.launched, 1);
+    h->s.local_pending = false;
+}
+
 void shard_apply(di_graph *h, const double *recv, int force) {
+    if (!force) shard_heavy_local(h);
     int64_t off = 0;
     for (int64_t c : h->g.recv_seg) {   // source ranks in order: deterministic
         if (c > 0) {
@@ -186,7 +198,7 @@ void shard_reduce(di_graph *h) {
 // after the last sweep: the pending pushes of the tiled schedule, exchanged like a sweep
 void shard_flush(di_graph *h, double *ghost_out) {
     if (h->s.tiled_call) {
-        launch_tile_heavy(h, 1);
+        if (h->g.tl.groups > h->g.tl.waves) launch_tile_heavy(h, 1, 0, h->g.tl.waves);
         launch_take_ghost_sums(h, ghost_out, 1);
     } else if (h->g.nt > h->g.n) {
         DI_CUDA(cudaMemsetAsync(ghost_out, 0, (h->g.nt - h->g.n) * sizeof(double), h->stream));

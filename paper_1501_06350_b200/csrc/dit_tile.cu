@@ -872,12 +872,13 @@ static int heavy_ctas_per_sm() {
 
 // the heavy targets' remote inflow hsum of one wave: chunks by ticket, then the fold
 template <typename W>
-static void launch_heavy_t(di_graph *h, int wave, int force) {
+static void launch_heavy_t(di_graph *h, int wave, int force, int group = -1) {
     TilePlan &tp = h->g.tl;
     State &s = h->s;
     if (tp.nh == 0) return;
-    const int64_t S = tp.nstripe, g0 = (int64_t)wave * S;
-    const int64_t t0 = tp.wave_slot[wave], t1 = tp.wave_slot[wave + 1];
+    if (group < 0) group = wave;                     // the ghost group gathers with wave 0's rule
+    const int64_t S = tp.nstripe, g0 = (int64_t)group * S;
+    const int64_t t0 = tp.wave_slot[group], t1 = tp.wave_slot[group + 1];
     // one launch over the wave's stripes in stripe order: the CTAs stride over the
     // chunks statically and advance together, so the gathered slice of A
     // (kStripeBytes) of the stripe being worked on stays L2-resident (one launch
@@ -951,12 +952,12 @@ void launch_tile_sweep(di_graph *h, int rounds) {
 }
 
 // shard sweeps run the two halves separately, the ghost exchange in between
-void launch_tile_heavy(di_graph *h, int force, int wave) {
+void launch_tile_heavy(di_graph *h, int force, int wave, int group) {
     if (h->g.tl.ntile == 0) return;
     switch (h->g.w_kind) {
-    case DI_W_F32: launch_heavy_t<float>(h, wave, force); break;
-    case DI_W_F64: launch_heavy_t<double>(h, wave, force); break;
-    default: launch_heavy_t<NoW>(h, wave, force);
+    case DI_W_F32: launch_heavy_t<float>(h, wave, force, group); break;
+    case DI_W_F64: launch_heavy_t<double>(h, wave, force, group); break;
+    default: launch_heavy_t<NoW>(h, wave, force, group);
     }
 }
 

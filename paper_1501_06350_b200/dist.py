@@ -68,6 +68,9 @@ class CudaShard:
     def sweep(self):
         _lib.di_shard_sweep(self.h, self.send)
 
+    def heavy_local(self):
+        _lib.di_shard_heavy_local(self.h)
+
     def apply(self):
         _lib.di_shard_apply(self.h, self.recv)
 
@@ -156,6 +159,22 @@ class TorchCollectives:
                                     output_split_sizes=s.recv_counts, input_split_sizes=s.send_counts,
                                     group=self.group)
 
+    def alltoall_start(self, shards):
+        """Start the ghost exchange; its wait is alltoall_finish.  NCCL: asynchronous,
+        so the rank's own wave-0 heavy gather (enqueued after this call) runs while the
+        exchange moves over NVLink; the wait orders the stream before di_shard_apply."""
+        (s,) = shards
+        if self.world == 1 or self.stage:
+            self.alltoall(shards)
+            return None
+        return self.dist.all_to_all_single(s.recv[:sum(s.recv_counts)], s.send[:sum(s.send_counts)],
+                                           output_split_sizes=s.recv_counts, input_split_sizes=s.send_counts,
+                                           group=self.group, async_op=True)
+
+    def alltoall_finish(self, work):
+        if work is not None:
+            work.wait()
+
     def allreduce_sum(self, values, device):
         t = torch.tensor(values, dtype=torch.float64, device="cpu" if self.stage else device)
         self.dist.all_reduce(t, group=self.group)
@@ -170,12 +189,15 @@ class TorchCollectives:
 def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
     """Cold sharded solve; returns (list of local H tensors, list of local result dicts).
 
-    Per sweep: sweep -> all-to-all(ghost fluid) -> apply -> reduce -> all-gather
+    Per sweep: sweep (ghost sums) -> all-to-all(ghost fluid), overlapped with
+    heavy_local (the rank's own wave-0 heavy gather) -> apply -> reduce -> all-gather
     of the ranks' {|F|_1, max |F|, leak} -> control (reduced on the device).  The host polls `done` once per chunk.
     The tiled schedule (variant 3) leaves the last sweep's remote pushes
     pending (R13): once done, they are exchanged and applied like a
     sweep (flush -> all-to-all -> flush_apply -> all-reduce -> control), and
     the sweeps go on if the exact residual is still above tol."""
+    start = getattr(coll, "alltoall_start", None) or (lambda sh: coll.alltoall(sh))
+    finish = getattr(coll, "alltoall_finish", None) or (lambda w: None)
     for s in shards:
         s.begin(d, tol, **opts)
     coll.allreduce_stats(shards)
@@ -188,7 +210,11 @@ def solve(shards, coll, d=0.85, tol=1e-12, max_chunk=64, **opts):
         for _ in range(chunk):
             for s in shards:
                 s.sweep()
-            coll.alltoall(shards)
+            # the exchange overlaps each rank's own wave-0 heavy gather (tiled)
+            work = start(shards)
+            for s in shards:
+                s.heavy_local()
+            finish(work)
             for s in shards:
                 s.apply()
                 s.reduce()

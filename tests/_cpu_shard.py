@@ -86,6 +86,9 @@ class CpuShard:
         self.send[: self.n_ghost] = torch.from_numpy(self.F[self.n_local:].copy())
         self.F[self.n_local:] = 0.0
 
+    def heavy_local(self):
+        pass                                         # the frontier sweep has no heavy gather
+
     def apply(self):
         if self.done:
             return
