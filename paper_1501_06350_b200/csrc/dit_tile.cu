@@ -29,10 +29,10 @@
 // gathered stripe by stripe, so that the slice of A being read stays in L2
 // (a random 8-byte read from HBM costs a 64-byte DRAM access on B200).
 //
-// Kernels (B200): k_tile -- persistent, one 768-thread CTA per SM walking the
+// Kernels (B200): k_tile -- persistent, one 736-thread CTA per SM walking the
 // tiles of one wave (R15), warp-specialised: 16 round warps (thread i owns
 // node i of the tile; the rounds over sliced-ELL slots staged in shared
-// memory), 7 prep warps (the next tile's inflow: per-node loads, light-record
+// memory), 6 prep warps (the next tile's inflow: per-node loads, light-record
 // gathers, heavy sums) and one producer warp issuing the TMA bulk copies
 // (cp.async.bulk + mbarrier, double-buffered edge bundles and light records);
 // named barriers hand the prepared rows from prep to rounds.

@@ -10,7 +10,7 @@
 namespace dit {
 
 constexpr int kTileThreads = (int)kNodeTile;     // build kernels: thread i owns node i of the tile
-// k_tile: one CTA per SM of 24 warps: 16 round warps (thread i owns node i), 7
+// k_tile: one CTA per SM of 23 warps: 16 round warps (thread i owns node i), 6
 // prep warps (the next tile's inflow, up to 3 nodes per thread) and a producer
 // warp issuing the TMA bulk copies
 constexpr int kRW = (int)kNodeTile;
@@ -23,7 +23,7 @@ constexpr int kLsUnroll = DIT_LS_UNROLL;          // k_tile: slot groups per unr
 #endif
 constexpr int kRecUnroll = DIT_REC_UNROLL;        // k_tile prep: light-record gathers in flight per thread
 #ifndef DIT_PREP_WARPS
-#define DIT_PREP_WARPS 7
+#define DIT_PREP_WARPS 6
 #endif
 constexpr int kPWt = 32 * DIT_PREP_WARPS;        // prep threads
 constexpr int kPN = ((int)kNodeTile + kPWt - 1) / kPWt;   // nodes per prep thread (at most)
