@@ -160,6 +160,11 @@ def test_tiled_update_keeps_plan_f64_weights(eng):
     cold = di.di_solve(g.n, rp2, c2, w2, D, tol=1e-12)
     assert r["converged"]
     assert np.abs(H.cpu().numpy() - cold.H).sum() <= 1e-9
+    # a cold solve on the same handle: the kept plan with its delta entries
+    H2, r2 = G.solve(d=D, tol=1e-12, variant="tiled")
+    assert r2["converged"]
+    assert np.abs(H2.cpu().numpy() - cold.H).sum() <= 1e-9
+
 
 def test_tiled_update_dangling_transitions(eng):
     # nodes losing every out-edge (their fluid leaks from then on, §3.3) and
