@@ -98,6 +98,10 @@ constexpr int64_t kHeavyTh = DIT_HEAVY_TH;       // remote in-degree above which
 #define DIT_HEAVY_CHUNK 1024
 #endif
 constexpr int64_t kHeavyChunk = DIT_HEAVY_CHUNK;   // heavy edges per k_heavy chunk
+#ifndef DIT_HEAVY_THREADS
+#define DIT_HEAVY_THREADS 256
+#endif
+constexpr int kHeavyThreads = DIT_HEAVY_THREADS;   // block size of k_heavy_chunks
 
 constexpr int32_t kDegLocalDelta = 1 << 30;     // TilePlan::deg: the node has in-round delta in-edges
 constexpr int32_t kDegMask = kDegLocalDelta - 1;

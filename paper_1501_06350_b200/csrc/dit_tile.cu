@@ -62,7 +62,7 @@ namespace dit {
 
 // the chunks [c0, c1) of one wave (stripe order); CTA per chunk at a time
 template <typename W>
-__global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__restrict__ hrec,
+__global__ void __launch_bounds__(kHeavyThreads) k_heavy_chunks(const RemRec<W> *__restrict__ hrec,
                                                            const int64_t *__restrict__ chunk_start,
                                                            const int64_t *__restrict__ seg_start,
                                                            const int64_t *__restrict__ cfirst, int64_t c0, int64_t c1,
@@ -83,14 +83,14 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
         const int cnt = (int)(chunk_start[c + 1] - e0);
         const int64_t sg0 = cfirst[c];
         const int ns = (int)(cfirst[c + 1] - sg0);
-        for (int q = threadIdx.x; q < ns; q += kThreads) sbnd[q] = (int)(seg_start[sg0 + q] - e0);
+        for (int q = threadIdx.x; q < ns; q += kHeavyThreads) sbnd[q] = (int)(seg_start[sg0 + q] - e0);
         if (threadIdx.x == 0) sbnd[ns] = cnt;
         // all of this thread's records first, then all their gathers (kPer loads in flight each)
-        constexpr int kPer = (int)kHeavyChunk / kThreads;
+        constexpr int kPer = (int)kHeavyChunk / kHeavyThreads;
         RemRec<W> rr[kPer];
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
-            const int k = threadIdx.x + u * kThreads;
+            const int k = threadIdx.x + u * kHeavyThreads;
             if (k < cnt) rr[u] = hrec[e0 + k];
         }
         double vv[kPer];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
         for (int u = 0; u < kPer; ++u) {
             // a source of an earlier wave pushed this sweep; the others in the previous
             // one (still pending); in the flush only the pending pushes are left (R15)
-            const int k = threadIdx.x + u * kThreads;
+            const int k = threadIdx.x + u * kHeavyThreads;
             vv[u] = 0.0;
             if (k < cnt) {
                 const bool early = tile_wave(rr[u].src, waves) < wave;
@@ -107,11 +107,11 @@ __global__ void __launch_bounds__(kThreads) k_heavy_chunks(const RemRec<W> *__re
         }
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
-            const int k = threadIdx.x + u * kThreads;
+            const int k = threadIdx.x + u * kHeavyThreads;
             if (k < cnt) vals[k] = vv[u] * rec_w(rr[u]);
         }
         __syncthreads();
-        for (int q0 = (int)(w * 32); q0 < ns; q0 += kThreads) {
+        for (int q0 = (int)(w * 32); q0 < ns; q0 += kHeavyThreads) {
             const int q = q0 + (int)lane;
             int b = 0, e = 0;
             if (q < ns) {
@@ -864,7 +864,7 @@ template <typename W>
 static int heavy_ctas_per_sm() {
     static int v = 0;
     if (!v) {
-        DI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_heavy_chunks<W>, kThreads, 0));
+        DI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_heavy_chunks<W>, kHeavyThreads, 0));
         if (v < 1) v = 1;
     }
     return v;
@@ -886,7 +886,7 @@ static void launch_heavy_t(di_graph *h, int wave, int force, int group = -1) {
     const int64_t a0 = tp.s_chunk[g0], a1 = tp.s_chunk[g0 + S];
     if (a1 > a0) {
         const int grid = (int)std::min<int64_t>(a1 - a0, (int64_t)h->num_sms * heavy_ctas_per_sm<W>());
-        k_heavy_chunks<W><<<grid, kThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
+        k_heavy_chunks<W><<<grid, kHeavyThreads, 0, h->stream>>>((const RemRec<W> *)tp.hrec, tp.chunk_start, tp.seg_start,
                                                             tp.cfirst, a0, a1, s.A, s.A2, tp.part, wave, tp.waves,
                                                             s.ctrl, force);
         count_launch();
